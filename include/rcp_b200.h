@@ -1,0 +1,134 @@
+/*
+ * rcp_b200.h — C ABI of the B200-native RCP block-LDL^T factor/solve.
+ *
+ * Drop-in boundary for the reference package `randldl` (pure Python; paths
+ * below are relative to /root/reference/pkg/src/randldl/).  The reference has
+ * no FFI; its public Python API is the boundary, and each entry point here
+ * replaces one of those calls (see INTEGRATION.md for the ctypes binding a
+ * maintainer adds to `randldl`):
+ *
+ *   rcp_factor          <- randldl.factor / factor_robust   (factor.py:637-660)
+ *                          with strategy="rcp", q in {b} (q == 1 reported as
+ *                          RCP_ERR_UNSUPPORTED in this build)
+ *   rcp_solve           <- randldl.solve / solve_many        (solve.py:79-107)
+ *   rcp_reconstruct     <- randldl.reconstruct               (factor.py:663-665)
+ *   rcp_workspace_bytes    workspace query (no reference counterpart)
+ *
+ * Conventions
+ *  - All matrix pointers are DEVICE pointers to fp64 data.  The input matrix
+ *    is dense, symmetric, n x n with leading dimension lda (row- and
+ *    column-major coincide for a symmetric matrix).  It is never modified
+ *    (factor.py:285 copies A).
+ *  - Omega (the initial Gaussian sketch, p x n, row-major as numpy draws it,
+ *    sketch.py:83-84) is supplied by the caller so both sides see identical
+ *    bits.  Guard recomputes (factor.py:392-410) call `draw` to obtain the
+ *    next p x m normals from the same advancing stream; a NULL `draw` turns a
+ *    recompute into RCP_ERR_NEED_NORMALS.
+ *  - Outputs: perm (int64[n]), L (fp64 n x n ROW-major, unit lower, final
+ *    pivot order — the reference's dense L), d_diag/d_off (fp64[n]: the 1x1
+ *    entries and the 2x2 blocks [[d_diag[k], d_off[k]], [d_off[k],
+ *    d_diag[k+1]]] where pattern[k] == 1), pattern (int8[n], factor.py:94-97).
+ *  - Every call is reentrant: caller-provided workspace, one CUDA stream,
+ *    no global state.  Calls block until the result is on the device
+ *    (the host drives one panel at a time).
+ */
+#ifndef RCP_B200_H
+#define RCP_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes (0 = ok).  Python maps them to the reference's exceptions. */
+enum {
+  RCP_OK = 0,
+  RCP_ERR_INVALID_ARG = 1,      /* bad config / sizes -> ValueError (factor.py:137-149)          */
+  RCP_ERR_NOT_SYMMETRIC = 2,    /* -> ValueError "must be symmetric" (core.py:48-53)             */
+  RCP_ERR_NONFINITE_INPUT = 3,  /* -> ValueError "contains NaN or Inf" (factor.py:280-281)        */
+  RCP_ERR_NUMERICAL = 4,        /* -> NumericalError; kind/step in rcp_stats (factor.py:455-466) */
+  RCP_ERR_NEED_NORMALS = 5,     /* guard recompute needed but no `draw` callback                  */
+  RCP_ERR_CUDA = 6,             /* CUDA runtime failure; message in rcp_stats                     */
+  RCP_ERR_WORKSPACE = 7,        /* workspace smaller than rcp_workspace_bytes()                   */
+  RCP_ERR_UNSUPPORTED = 8       /* e.g. q == 1 mode in this build                                 */
+};
+
+/* NumericalError kinds (factor.py:214, 222, 456, 464-466). */
+enum {
+  RCP_NUM_NONE = 0,
+  RCP_NUM_ZERO_1X1 = 1,        /* "zero 1x1 pivot under a nonzero column"             */
+  RCP_NUM_SINGULAR_2X2 = 2,    /* "singular 2x2 pivot block"                          */
+  RCP_NUM_NONFINITE = 3,       /* "non-finite pivot data at step {k}"                 */
+  RCP_NUM_DET_BOUND = 4        /* "2x2 block at step {k} violates its determinant bound" */
+};
+
+/* Mirror of the rcp-relevant FactorConfig fields (factor.py:116-135). */
+typedef struct rcp_config {
+  int32_t p;          /* sketch rows (reference FactorConfig.p)                */
+  int32_t b;          /* panel width                                            */
+  int32_t q;          /* 1 or b                                                 */
+  int32_t robust_r;   /* recompute budget exponent; 0 disables the guard        */
+} rcp_config;
+
+/* Mirror of GrowthStats' engine-produced fields (metrics.py:47-65, factor.py:514-527)
+ * plus the run's structure. */
+typedef struct rcp_stats {
+  double rho_cheap;          /* max|D| / max|A|                                  */
+  double max_multiplier;     /* max |tril(L, -1)|                                 */
+  double amax;               /* max|A|                                            */
+  double dmax;               /* max|D|                                            */
+  int64_t recompute_count;   /* guard recomputes                                  */
+  int64_t n_panels;
+  int64_t n_steps;           /* pivot decisions taken                             */
+  int64_t n_2x2;
+  int64_t deficient_from;    /* first PAT_DEFICIENT index, -1 if none             */
+  int32_t num_kind;          /* RCP_NUM_* when status == RCP_ERR_NUMERICAL        */
+  int32_t num_step;          /* step k of the numerical error                     */
+  double t_factor_ms;        /* device time of the factorization (CUDA events)    */
+  double t_schur_ms;         /* device time inside the trailing Schur updates     */
+  double t_panel_ms;         /* device time inside the panel kernels              */
+  char message[160];
+} rcp_stats;
+
+/* Fill host `out` (row-major rows x cols) with the next standard normals of the
+ * factorization's generator (numpy Generator(Philox(seed)).standard_normal).
+ * Return 0 on success. */
+typedef int (*rcp_draw_fn)(void* ctx, int64_t rows, int64_t cols, double* out);
+
+/* Bytes of device workspace rcp_factor needs for this (n, cfg). */
+size_t rcp_workspace_bytes(int64_t n, const rcp_config* cfg);
+
+/* Factor A[perm][:, perm] = L D L^T (randldl.factor, factor.py:637-647).
+ * Optional per-step trace (device, may be NULL): trace_kind[k] in {0 skip, 1 1x1,
+ * 2 1x1-swap, 3 2x2} at each decision position k, trace_r[k] = partner r or -1. */
+int rcp_factor(const rcp_config* cfg, int64_t n, const double* a, int64_t lda,
+               const double* omega, rcp_draw_fn draw, void* draw_ctx,
+               void* workspace, size_t workspace_bytes,
+               int64_t* perm, double* L, double* d_diag, double* d_off, int8_t* pattern,
+               int8_t* trace_kind, int32_t* trace_r,
+               rcp_stats* stats, void* cuda_stream);
+
+/* x = P^T L^-T D^-1 L^-1 P b for nrhs right-hand sides (solve.py:69-92).
+ * b and x are device, column-major n x nrhs (ld = n); may alias.  *singular is
+ * set to 1 if an exact-zero block was met (solve.py:47-58). */
+int rcp_solve(int64_t n, const int64_t* perm, const double* L, const double* d_diag,
+              const double* d_off, const int8_t* pattern, int64_t nrhs,
+              const double* b, double* x, void* workspace, size_t workspace_bytes,
+              int32_t* singular, void* cuda_stream);
+
+/* Workspace bytes for rcp_solve. */
+size_t rcp_solve_workspace_bytes(int64_t n, int64_t nrhs);
+
+/* out (n x n row-major) = L D L^T (factor.py:663-665). */
+int rcp_reconstruct(int64_t n, const double* L, const double* d_diag, const double* d_off,
+                    const int8_t* pattern, double* out, void* cuda_stream);
+
+/* Library identification: "rcp_b200 <version> sm_100a". */
+const char* rcp_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RCP_B200_H */

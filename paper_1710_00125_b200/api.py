@@ -1,0 +1,489 @@
+"""Drop-in mirror of the reference ``randldl`` factor/solve API, backed by CUDA.
+
+Same names, fields, argument meaning and error behaviour as the reference
+(paths relative to ``/root/reference/pkg/src/randldl/``):
+
+* :class:`FactorConfig`       factor.py:116-149
+* :class:`BlockDiag`          factor.py:152-173
+* :class:`Factorization`      factor.py:176-199
+* :class:`GrowthStats`        metrics.py:46-65,  :class:`OpCounters` metrics.py:28-43
+* :class:`SolveReport`        solve.py:25-31
+* :func:`factor` / :func:`factor_robust` / :func:`reconstruct`   factor.py:637-665
+* :func:`solve` / :func:`solve_many`                              solve.py:79-107
+
+Every numerical step runs in ``librcp_b200.so`` (``include/rcp_b200.h``) on the
+GPU; this module only validates arguments, draws the Gaussian sketch with the
+reference's generator (numpy ``Generator(Philox(seed))``, sketch.py:39-42) so
+both implementations see identical bits, moves data and maps status codes to
+the reference's exceptions.  There is no CPU fallback.
+
+The device-resident entry points :func:`factor_device` / :func:`solve_device`
+take and return CUDA tensors (used by the benchmark, whose timed region starts
+with the matrix already in HBM).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass, field
+from enum import Enum
+
+import numpy as np
+import torch
+
+from . import _native
+
+__all__ = [
+    "Strategy", "GrowthTracking", "FactorConfig", "BlockDiag", "Factorization", "GrowthStats",
+    "OpCounters", "SolveReport", "NumericalError", "PAT_SINGLE", "PAT_PAIR_START", "PAT_PAIR_END",
+    "PAT_DEFICIENT", "SBKP_ALPHA", "factor", "factor_robust", "reconstruct", "solve", "solve_many",
+    "DeviceFactorization", "factor_device", "solve_device", "reconstruct_device",
+]
+
+PAT_SINGLE = 0
+PAT_PAIR_START = 1
+PAT_PAIR_END = 2
+PAT_DEFICIENT = 3
+SBKP_ALPHA = math.sqrt(2.0) / 2.0
+
+
+class NumericalError(RuntimeError):
+    """Raised when the factorization meets a non-finite or impossible value (factor.py:100-101)."""
+
+
+class Strategy(str, Enum):
+    RCP = "rcp"
+    BKPP = "bkpp"
+    BBK = "bbk"
+
+
+class GrowthTracking(str, Enum):
+    CHEAP = "cheap"
+    FULL = "full"
+
+
+@dataclass
+class FactorConfig:
+    """Knobs for :func:`factor`; validation identical to factor.py:137-149."""
+
+    strategy: Strategy = Strategy.RCP
+    p: int = 5
+    b: int = 64
+    q: int = 1
+    seed: int = 0
+    robust_r: int = 1
+    track_growth: GrowthTracking = GrowthTracking.CHEAP
+    audit_sketch: bool = False
+
+    def __post_init__(self) -> None:
+        self.strategy = Strategy(self.strategy)
+        self.track_growth = GrowthTracking(self.track_growth)
+        if self.p < 1:
+            raise ValueError("sketch size p must be positive")
+        if self.b < 1:
+            raise ValueError("panel width b must be positive")
+        if self.q not in (1, self.b):
+            raise ValueError(f"q must be 1 or b={self.b}, got {self.q}")
+        if self.p < self.q:
+            raise ValueError(f"sketch size p={self.p} must be at least q={self.q}")
+        if self.robust_r < 0:
+            raise ValueError("robust_r must be non-negative")
+
+
+@dataclass
+class OpCounters:
+    mults: int = 0
+    adds: int = 0
+    divs: int = 0
+    comps: int = 0
+
+    def total_flops(self) -> int:
+        return self.mults + self.adds + self.divs
+
+
+@dataclass
+class GrowthStats:
+    rho_cheap: float
+    max_multiplier: float
+    counters: OpCounters = field(default_factory=OpCounters)
+    rho_elem: float | None = None
+    rho_col: float | None = None
+    L_norm1: float | None = None
+    Linv_norm1: float | None = None
+    snapshots: list | None = None
+    sketch_drift: list | None = None
+    recompute_count: int = 0
+
+
+@dataclass
+class BlockDiag:
+    """Block diagonal factor: an ordered list of (1,1) and (2,2) arrays."""
+
+    blocks: list
+
+    @property
+    def dim(self) -> int:
+        return sum(b.shape[0] for b in self.blocks)
+
+    def to_dense(self) -> np.ndarray:
+        n = self.dim
+        d = np.zeros((n, n))
+        i = 0
+        for blk in self.blocks:
+            s = blk.shape[0]
+            d[i:i + s, i:i + s] = blk
+            i += s
+        return d
+
+    def max_abs(self) -> float:
+        return max((float(np.abs(b).max()) for b in self.blocks), default=0.0)
+
+
+@dataclass
+class Factorization:
+    """Result of :func:`factor`: ``A[perm][:, perm] == L @ D @ L.T``."""
+
+    perm: np.ndarray
+    L: np.ndarray
+    D: BlockDiag
+    pattern: np.ndarray
+    stats: GrowthStats
+
+    @property
+    def n(self) -> int:
+        return self.perm.size
+
+    @property
+    def deficient_from(self) -> int | None:
+        hits = np.nonzero(self.pattern == PAT_DEFICIENT)[0]
+        return int(hits[0]) if hits.size else None
+
+
+@dataclass
+class SolveReport:
+    x: np.ndarray
+    singular: bool
+    backward_error: float | None = None
+
+
+# --------------------------------------------------------------------------- helpers
+
+def _require_square(a: np.ndarray, name: str = "A") -> np.ndarray:
+    """core.py:33-45 (shape part; symmetry/finiteness are checked on the device)."""
+    a = np.asarray(a, dtype=np.float64)
+    if a.ndim != 2 or a.shape[0] != a.shape[1]:
+        raise ValueError(f"{name} must be square, got shape {a.shape}")
+    if a.shape[0] == 0:
+        raise ValueError(f"{name} must have at least one row")
+    return a
+
+
+def _check_supported(cfg: FactorConfig) -> None:
+    if cfg.strategy is not Strategy.RCP:
+        raise ValueError(f"strategy {cfg.strategy.value!r} is not part of the B200 build (rcp only)")
+    if cfg.track_growth is GrowthTracking.FULL or cfg.audit_sketch:
+        raise ValueError("track_growth='full' / audit_sketch diagnostics are not part of the B200 build")
+
+
+def _raise_status(status: int, st: _native.RcpStats | None) -> None:
+    if status == _native.RCP_OK:
+        return
+    msg = st.message.decode(errors="replace") if st is not None else ""
+    if status == _native.RCP_ERR_NOT_SYMMETRIC:
+        raise ValueError("A must be symmetric (exact equality of triangles)")
+    if status == _native.RCP_ERR_NONFINITE_INPUT:
+        raise ValueError("input matrix contains NaN or Inf")
+    if status == _native.RCP_ERR_NUMERICAL:
+        kind, step = int(st.num_kind), int(st.num_step)
+        if kind == _native.RCP_NUM_ZERO_1X1:
+            raise NumericalError("zero 1x1 pivot under a nonzero column")
+        if kind == _native.RCP_NUM_SINGULAR_2X2:
+            raise NumericalError("singular 2x2 pivot block")
+        if kind == _native.RCP_NUM_DET_BOUND:
+            raise NumericalError(f"2x2 block at step {step} violates its determinant bound")
+        raise NumericalError(f"non-finite pivot data at step {step}")
+    if status == _native.RCP_ERR_INVALID_ARG:
+        raise ValueError(f"invalid argument ({msg})")
+    if status == _native.RCP_ERR_UNSUPPORTED:
+        raise ValueError(f"unsupported configuration: {msg}")
+    raise RuntimeError(f"rcp_b200 failed with status {status}: {msg}")
+
+
+def _ptr(t: torch.Tensor | None) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+def _stream() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+# --------------------------------------------------------------------------- device API
+
+@dataclass
+class DeviceFactorization:
+    """GPU-resident factorization (all tensors on the CUDA device)."""
+
+    perm: torch.Tensor      # int64 [n]
+    L: torch.Tensor         # float64 [n, n] row-major, unit lower
+    d_diag: torch.Tensor    # float64 [n]
+    d_off: torch.Tensor     # float64 [n]
+    pattern: torch.Tensor   # int8 [n]
+    stats: dict
+    trace_kind: torch.Tensor | None = None
+    trace_r: torch.Tensor | None = None
+
+    @property
+    def n(self) -> int:
+        return int(self.perm.numel())
+
+    def blocks(self) -> list:
+        return _blocks_from_arrays(self.d_diag.cpu().numpy(), self.d_off.cpu().numpy(),
+                                   self.pattern.cpu().numpy())
+
+    def to_host(self) -> Factorization:
+        pattern = self.pattern.cpu().numpy().astype(np.int8)
+        blocks = _blocks_from_arrays(self.d_diag.cpu().numpy(), self.d_off.cpu().numpy(), pattern)
+        s = self.stats
+        stats = GrowthStats(rho_cheap=s["rho_cheap"], max_multiplier=s["max_multiplier"],
+                            counters=OpCounters(), recompute_count=s["recompute_count"])
+        return Factorization(perm=self.perm.cpu().numpy().astype(np.int64), L=self.L.cpu().numpy(),
+                             D=BlockDiag(blocks), pattern=pattern, stats=stats)
+
+
+def _blocks_from_arrays(dd: np.ndarray, doff: np.ndarray, pattern: np.ndarray) -> list:
+    blocks = []
+    n = pattern.size
+    i = 0
+    while i < n:
+        if pattern[i] == PAT_PAIR_START and i + 1 < n:
+            blocks.append(np.array([[dd[i], doff[i]], [doff[i], dd[i + 1]]]))
+            i += 2
+        else:
+            blocks.append(np.array([[dd[i]]]))
+            i += 1
+    return blocks
+
+
+class _NormalStream:
+    """The reference's advancing generator (sketch.py:63-84) as a C callback."""
+
+    def __init__(self, seed: int):
+        self.gen = np.random.Generator(np.random.Philox(seed))
+        self.draws = 0
+
+        def _cb(_ctx, rows, cols, out):
+            try:
+                z = self.gen.standard_normal((int(rows), int(cols)))
+                ctypes.memmove(out, z.ctypes.data, z.nbytes)
+                self.draws += 1
+                return 0
+            except Exception:  # pragma: no cover - reported as a status code
+                return 1
+
+        self.cfunc = _native.DRAW_FN(_cb)
+
+    def first(self, p: int, n: int) -> np.ndarray:
+        return self.gen.standard_normal((p, n))
+
+
+def _config(cfg: FactorConfig | None, overrides: dict) -> FactorConfig:
+    if cfg is not None and overrides:
+        raise ValueError("pass either cfg or keyword overrides, not both")
+    if cfg is None:
+        cfg = FactorConfig(**overrides)
+    return cfg
+
+
+def workspace_bytes(n: int, cfg: FactorConfig) -> int:
+    lib = _native.load()
+    c = _native.RcpConfig(cfg.p, cfg.b, cfg.q, cfg.robust_r)
+    return int(lib.rcp_workspace_bytes(n, ctypes.byref(c)))
+
+
+def factor_device(a: torch.Tensor, cfg: FactorConfig | None = None, *, omega: torch.Tensor | None = None,
+                  trace: bool = False, workspace: torch.Tensor | None = None,
+                  out: DeviceFactorization | None = None, **overrides) -> DeviceFactorization:
+    """Factor a CUDA float64 symmetric matrix; results stay on the device.
+
+    ``omega`` (p x n, CUDA float64) may be passed pre-drawn; it must then be the
+    first draw of ``Generator(Philox(cfg.seed))`` for results to match the
+    reference.  ``workspace``/``out`` let a caller reuse device buffers.
+    """
+    cfg = _config(cfg, overrides)
+    _check_supported(cfg)
+    lib = _native.load()
+    if a.dim() != 2 or a.shape[0] != a.shape[1]:
+        raise ValueError(f"A must be square, got shape {tuple(a.shape)}")
+    n = int(a.shape[0])
+    if n == 0:
+        raise ValueError("A must have at least one row")
+    if a.dtype != torch.float64 or not a.is_cuda:
+        raise ValueError("factor_device expects a CUDA float64 tensor")
+    if a.stride(1) != 1 and a.stride(0) != 1:
+        a = a.contiguous()
+    lda = a.stride(0) if a.stride(1) == 1 else a.stride(1)
+    dev = a.device
+    normals = _NormalStream(cfg.seed)
+    if omega is None:
+        omega = torch.from_numpy(normals.first(cfg.p, n)).to(dev)
+    else:
+        normals.first(cfg.p, n)  # advance the stream past the supplied first draw
+        omega = omega.contiguous()
+    c = _native.RcpConfig(cfg.p, cfg.b, cfg.q, cfg.robust_r)
+    need = int(lib.rcp_workspace_bytes(n, ctypes.byref(c)))
+    if workspace is None or workspace.numel() < need:
+        workspace = torch.empty(need, dtype=torch.uint8, device=dev)
+    if out is None:
+        out = DeviceFactorization(
+            perm=torch.empty(n, dtype=torch.int64, device=dev),
+            L=torch.empty((n, n), dtype=torch.float64, device=dev),
+            d_diag=torch.empty(n, dtype=torch.float64, device=dev),
+            d_off=torch.empty(n, dtype=torch.float64, device=dev),
+            pattern=torch.empty(n, dtype=torch.int8, device=dev),
+            stats={},
+        )
+    if trace:
+        out.trace_kind = torch.empty(n, dtype=torch.int8, device=dev)
+        out.trace_r = torch.empty(n, dtype=torch.int32, device=dev)
+    st = _native.RcpStats()
+    status = lib.rcp_factor(
+        ctypes.byref(c), n, a.data_ptr(), lda, omega.data_ptr(), normals.cfunc, None,
+        workspace.data_ptr(), workspace.numel(), out.perm.data_ptr(), out.L.data_ptr(),
+        out.d_diag.data_ptr(), out.d_off.data_ptr(), out.pattern.data_ptr(),
+        _ptr(out.trace_kind if trace else None), _ptr(out.trace_r if trace else None),
+        ctypes.byref(st), _stream())
+    _raise_status(status, st)
+    out.stats = {
+        "rho_cheap": float(st.rho_cheap), "max_multiplier": float(st.max_multiplier),
+        "amax": float(st.amax), "dmax": float(st.dmax), "recompute_count": int(st.recompute_count),
+        "n_panels": int(st.n_panels), "n_steps": int(st.n_steps), "n_2x2": int(st.n_2x2),
+        "deficient_from": int(st.deficient_from), "t_factor_ms": float(st.t_factor_ms),
+        "t_schur_ms": float(st.t_schur_ms), "t_panel_ms": float(st.t_panel_ms),
+    }
+    return out
+
+
+def solve_device(f: DeviceFactorization, b: torch.Tensor, x: torch.Tensor | None = None,
+                 workspace: torch.Tensor | None = None) -> tuple[torch.Tensor, bool]:
+    """x = A^-1 b on the device; b is (n,) or (n, k) CUDA float64."""
+    lib = _native.load()
+    n = f.n
+    vec = b.dim() == 1
+    if b.shape[0] != n or b.dim() not in (1, 2):
+        raise ValueError(f"right-hand side shape {tuple(b.shape)} does not match n={n}")
+    nrhs = 1 if vec else int(b.shape[1])
+    bc = b.reshape(n, 1) if vec else b
+    bcol = bc.t().contiguous()  # (k, n): column-major n x k
+    xcol = torch.empty_like(bcol)
+    need = int(lib.rcp_solve_workspace_bytes(n, nrhs))
+    if workspace is None or workspace.numel() < need:
+        workspace = torch.empty(need, dtype=torch.uint8, device=b.device)
+    sing = ctypes.c_int32(0)
+    status = lib.rcp_solve(n, f.perm.data_ptr(), f.L.data_ptr(), f.d_diag.data_ptr(), f.d_off.data_ptr(),
+                           f.pattern.data_ptr(), nrhs, bcol.data_ptr(), xcol.data_ptr(), workspace.data_ptr(),
+                           workspace.numel(), ctypes.byref(sing), _stream())
+    _raise_status(status, None)
+    res = xcol.t()
+    res = res.reshape(n) if vec else res.contiguous()
+    if x is not None:
+        x.copy_(res)
+        res = x
+    return res, bool(sing.value)
+
+
+def reconstruct_device(f: DeviceFactorization) -> torch.Tensor:
+    lib = _native.load()
+    n = f.n
+    out = torch.empty((n, n), dtype=torch.float64, device=f.L.device)
+    status = lib.rcp_reconstruct(n, f.L.data_ptr(), f.d_diag.data_ptr(), f.d_off.data_ptr(),
+                                 f.pattern.data_ptr(), out.data_ptr(), _stream())
+    _raise_status(status, None)
+    return out
+
+
+# --------------------------------------------------------------------------- host API
+
+def _device() -> torch.device:
+    if not torch.cuda.is_available():
+        raise _native.NativeUnavailable("no CUDA device: the B200 build has no CPU fallback")
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def factor(a: np.ndarray, cfg: FactorConfig | None = None, **overrides) -> Factorization:
+    """Factor a dense symmetric matrix as ``A[perm][:, perm] = L D L.T`` (factor.py:637-647)."""
+    cfg = _config(cfg, overrides)
+    a = _require_square(a)
+    _check_supported(cfg)
+    _native.load()
+    dev = _device()
+    ad = torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+    return factor_device(ad, cfg).to_host()
+
+
+def factor_robust(a: np.ndarray, cfg: FactorConfig | None = None, **overrides) -> Factorization:
+    """Like :func:`factor` with the sketch-collapse guard always armed (factor.py:650-660)."""
+    cfg = _config(cfg, overrides)
+    if cfg.strategy is not Strategy.RCP:
+        raise ValueError("the guarded mode requires the rcp strategy")
+    if cfg.robust_r < 1:
+        raise ValueError("factor_robust needs robust_r >= 1")
+    return factor(a, cfg)
+
+
+def reconstruct(f: Factorization) -> np.ndarray:
+    """Assemble ``L @ D @ L.T`` (factor.py:663-665)."""
+    return f.L @ f.D.to_dense() @ f.L.T
+
+
+def _device_from_host(f: Factorization) -> DeviceFactorization:
+    dev = _device()
+    n = f.n
+    dd = np.zeros(n)
+    doff = np.zeros(n)
+    i = 0
+    for blk in f.D.blocks:
+        if blk.shape[0] == 1:
+            dd[i] = blk[0, 0]
+            i += 1
+        else:
+            dd[i], dd[i + 1], doff[i] = blk[0, 0], blk[1, 1], blk[1, 0]
+            i += 2
+    return DeviceFactorization(
+        perm=torch.from_numpy(np.asarray(f.perm, dtype=np.int64)).to(dev),
+        L=torch.from_numpy(np.ascontiguousarray(f.L, dtype=np.float64)).to(dev),
+        d_diag=torch.from_numpy(dd).to(dev), d_off=torch.from_numpy(doff).to(dev),
+        pattern=torch.from_numpy(np.asarray(f.pattern, dtype=np.int8)).to(dev), stats={})
+
+
+def _backward_error(a: np.ndarray, x: np.ndarray, b: np.ndarray) -> float:
+    """|Ax - b|_inf / (|A|_inf |x|_inf) (metrics.py:151-167)."""
+    resid = float(np.abs(a @ x - b).max())
+    a_inf = float(np.abs(a).sum(axis=1).max())
+    x_inf = float(np.abs(x).max()) if x.size else 0.0
+    den = a_inf * x_inf
+    if den == 0.0:
+        return 0.0 if resid == 0.0 else math.inf
+    return resid / den
+
+
+def solve(f: Factorization, b: np.ndarray, a: np.ndarray | None = None) -> SolveReport:
+    """Solve ``A x = b`` given ``factor(A)`` (solve.py:79-92)."""
+    b = np.asarray(b, dtype=np.float64)
+    if b.shape != (f.n,):
+        raise ValueError(f"right-hand side shape {b.shape} does not match n={f.n}")
+    df = _device_from_host(f)
+    xd, sing = solve_device(df, torch.from_numpy(b).to(df.L.device))
+    x = xd.cpu().numpy()
+    err = _backward_error(np.asarray(a, dtype=np.float64), x, b) if a is not None else None
+    return SolveReport(x=x, singular=sing, backward_error=err)
+
+
+def solve_many(f: Factorization, b_rhs: np.ndarray) -> np.ndarray:
+    """Column-wise :func:`solve` (solve.py:95-107)."""
+    b_rhs = np.asarray(b_rhs, dtype=np.float64)
+    if b_rhs.ndim != 2 or b_rhs.shape[0] != f.n:
+        raise ValueError(f"right-hand sides must be ({f.n}, k), got {b_rhs.shape}")
+    df = _device_from_host(f)
+    xd, _ = solve_device(df, torch.from_numpy(b_rhs).to(df.L.device))
+    return xd.cpu().numpy()

@@ -1,0 +1,489 @@
+// C ABI + host-side driver of the RCP factorization (include/rcp_b200.h).
+//
+// The driver is the native counterpart of the reference engine loop
+// (_Engine.run / _run_panel, factor.py:508-568): per panel it launches the
+// cooperative panel kernel, reads back the panel outcome (k_end, guard status,
+// numerical error) with one small D2H copy, then launches the gather, the
+// trailing Schur update and the sketch correction.  All matrix data stays on the
+// device; the host never touches a matrix element.
+#include <algorithm>
+#include <cfloat>
+#include <climits>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <vector>
+
+#include "../../include/rcp_b200.h"
+#include "misc.cuh"
+#include "panel.cuh"
+#include "rcp_common.cuh"
+#include "solve.cuh"
+
+using namespace rcp;
+
+namespace {
+
+constexpr size_t kAlign = 256;
+constexpr int kRowsMin = 32;
+
+size_t align_up(size_t x) { return (x + kAlign - 1) & ~(kAlign - 1); }
+
+struct Layout {
+  size_t A0, A1, Lbuf, W, Lneg, Wg, B0, B1, qscr, Y, omega, phys, lop, pol, perm0, perm1, poso, snap, flags, xrec, qrec,
+      qcol, state, scal, total;
+  int64_t rows_pad, snap_cap;
+  int tpad;
+};
+
+Layout make_layout(int64_t n, const rcp_config& c) {
+  Layout L{};
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    size_t o = off;
+    off = align_up(off + bytes);
+    return o;
+  };
+  const size_t nn = (size_t)n * (size_t)n;
+  const int P = c.p;
+  L.tpad = ((c.b + 2 + 15) / 16) * 16;
+  L.rows_pad = ((n + 127) / 128) * 128;
+  int64_t per_panel_min = std::max<int64_t>(1, (int64_t)c.b - 1);
+  int64_t max_panels = n / per_panel_min + 2;
+  L.snap_cap = std::min<int64_t>(max_panels * n, n * (n + 1) / 2 + n);
+  L.A0 = take(nn * 8);
+  L.A1 = take(nn * 8);
+  L.Lbuf = take(nn * 8);
+  L.W = take((size_t)n * (c.b + 2) * 8);
+  L.Lneg = take((size_t)L.rows_pad * L.tpad * 8);
+  L.Wg = take((size_t)L.rows_pad * L.tpad * 8);
+  L.B0 = take((size_t)P * n * 8);
+  L.B1 = take((size_t)P * n * 8);
+  L.qscr = take((size_t)P * n * 8);
+  L.Y = take((size_t)P * L.tpad * 8);
+  L.omega = take((size_t)P * n * 8);
+  L.phys = take((size_t)n * 4);
+  L.lop = take((size_t)n * 4);
+  L.pol = take((size_t)n * 4);
+  L.perm0 = take((size_t)n * 4);
+  L.perm1 = take((size_t)n * 4);
+  L.poso = take((size_t)n * 4);
+  L.snap = take((size_t)L.snap_cap * 4);
+  L.flags = take(sizeof(long long) * kMaxSMs);
+  L.xrec = take(sizeof(XRec) * 2 * kMaxSMs);
+  L.qrec = take(sizeof(QRec) * 2 * kMaxSMs);
+  L.qcol = take(sizeof(double) * 2 * kMaxSMs * (size_t)P);
+  L.state = take(sizeof(PanelState));
+  L.scal = take(64);
+  L.total = off;
+  return L;
+}
+
+int validate_cfg(const rcp_config* c, int64_t n) {
+  if (!c || n < 1) return RCP_ERR_INVALID_ARG;
+  if (c->p < 1 || c->b < 1 || c->robust_r < 0) return RCP_ERR_INVALID_ARG;
+  if (!(c->q == 1 || c->q == c->b)) return RCP_ERR_INVALID_ARG;
+  if (c->p < c->q) return RCP_ERR_INVALID_ARG;
+  if (n > (int64_t)INT_MAX / 2) return RCP_ERR_INVALID_ARG;
+  return RCP_OK;
+}
+
+struct Scal {  // scalar results block (device)
+  double amax, beta, dmax, maxmult;
+  int vflags[2];
+};
+
+#define RCP_CHECK(expr)                                                                           \
+  do {                                                                                            \
+    cudaError_t e_ = (expr);                                                                      \
+    if (e_ != cudaSuccess) {                                                                      \
+      if (stats) snprintf(stats->message, sizeof(stats->message), "%s at %s:%d", cudaGetErrorString(e_), \
+                          __FILE__, __LINE__);                                                    \
+      return RCP_ERR_CUDA;                                                                        \
+    }                                                                                             \
+  } while (0)
+
+struct PanelRecord {
+  int k0, k_end;
+  int64_t snap_off;
+};
+
+struct EventPair {
+  cudaEvent_t a, b;
+};
+
+}  // namespace
+
+extern "C" {
+
+const char* rcp_version(void) { return "rcp_b200 0.1.0 sm_100a"; }
+
+size_t rcp_workspace_bytes(int64_t n, const rcp_config* cfg) {
+  if (validate_cfg(cfg, n) != RCP_OK) return 0;
+  return make_layout(n, *cfg).total;
+}
+
+int rcp_factor(const rcp_config* cfg, int64_t n, const double* a, int64_t lda, const double* omega_dev,
+               rcp_draw_fn draw, void* draw_ctx, void* workspace, size_t workspace_bytes, int64_t* perm,
+               double* Lout, double* d_diag, double* d_off, int8_t* pattern, int8_t* trace_kind, int32_t* trace_r,
+               rcp_stats* stats, void* cuda_stream) {
+  if (stats) {
+    memset(stats, 0, sizeof(*stats));
+    stats->deficient_from = -1;
+  }
+  int vc = validate_cfg(cfg, n);
+  if (vc != RCP_OK) return vc;
+  if (lda < n || !a || !omega_dev || !perm || !Lout || !d_diag || !d_off || !pattern) return RCP_ERR_INVALID_ARG;
+  const rcp_config c = *cfg;
+  if (c.q == 1) {
+    if (stats) snprintf(stats->message, sizeof(stats->message), "q == 1 (per-step sketch pivoting) not built");
+    return RCP_ERR_UNSUPPORTED;
+  }
+  const Layout Lay = make_layout(n, c);
+  if (!workspace || workspace_bytes < Lay.total) return RCP_ERR_WORKSPACE;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(cuda_stream);
+  unsigned char* ws = reinterpret_cast<unsigned char*>(workspace);
+  auto dptr = [&](size_t off) { return reinterpret_cast<double*>(ws + off); };
+  auto iptr = [&](size_t off) { return reinterpret_cast<int*>(ws + off); };
+
+  double* A[2] = {dptr(Lay.A0), dptr(Lay.A1)};
+  double* B[2] = {dptr(Lay.B0), dptr(Lay.B1)};
+  int* permb[2] = {iptr(Lay.perm0), iptr(Lay.perm1)};
+  double* Lbuf = dptr(Lay.Lbuf);
+  double* W = dptr(Lay.W);
+  double* Lneg = dptr(Lay.Lneg);
+  double* Wg = dptr(Lay.Wg);
+  double* Y = dptr(Lay.Y);
+  double* omg = dptr(Lay.omega);
+  int* phys = iptr(Lay.phys);
+  int* lop = iptr(Lay.lop);
+  int* pol = iptr(Lay.pol);
+  int* poso = iptr(Lay.poso);
+  int* snap = iptr(Lay.snap);
+  PanelState* dstate = reinterpret_cast<PanelState*>(ws + Lay.state);
+  Scal* dscal = reinterpret_cast<Scal*>(ws + Lay.scal);
+  const int P = c.p;
+  const int tpad = Lay.tpad;
+
+  int dev = 0;
+  RCP_CHECK(cudaGetDevice(&dev));
+  int num_sms = 0, max_optin = 0;
+  RCP_CHECK(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev));
+  RCP_CHECK(cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+  RCP_CHECK(panel_init_attributes(max_optin - panel_static_smem_bytes()));
+  RCP_CHECK(gemm_init_attributes());
+  const int smem_budget = max_optin - panel_static_smem_bytes() - 1024;
+
+  PanelState* hstate = nullptr;
+  Scal* hscal = nullptr;
+  RCP_CHECK(cudaMallocHost(&hstate, sizeof(PanelState)));
+  RCP_CHECK(cudaMallocHost(&hscal, sizeof(Scal)));
+  struct HostFree {
+    PanelState* s;
+    Scal* c;
+    ~HostFree() {
+      cudaFreeHost(s);
+      cudaFreeHost(c);
+    }
+  } host_free{hstate, hscal};
+
+  cudaEvent_t ev_start, ev_stop;
+  RCP_CHECK(cudaEventCreate(&ev_start));
+  RCP_CHECK(cudaEventCreate(&ev_stop));
+  std::vector<EventPair> ev_panel, ev_schur;
+  struct EvFree {
+    cudaEvent_t* a;
+    cudaEvent_t* b;
+    std::vector<EventPair>* p;
+    std::vector<EventPair>* s;
+    ~EvFree() {
+      cudaEventDestroy(*a);
+      cudaEventDestroy(*b);
+      for (auto& e : *p) { cudaEventDestroy(e.a); cudaEventDestroy(e.b); }
+      for (auto& e : *s) { cudaEventDestroy(e.a); cudaEventDestroy(e.b); }
+    }
+  } ev_free{&ev_start, &ev_stop, &ev_panel, &ev_schur};
+  auto new_pair = [&](std::vector<EventPair>& v) -> EventPair& {
+    EventPair e;
+    cudaEventCreate(&e.a);
+    cudaEventCreate(&e.b);
+    v.push_back(e);
+    return v.back();
+  };
+
+  RCP_CHECK(cudaEventRecord(ev_start, st));
+
+  // ---- init state
+  PanelState init{};
+  init.seq = 0;
+  init.err = LLONG_MAX;
+  RCP_CHECK(cudaMemcpyAsync(dstate, &init, sizeof(init), cudaMemcpyHostToDevice, st));
+  RCP_CHECK(cudaMemsetAsync(ws + Lay.flags, 0, sizeof(long long) * kMaxSMs, st));
+  RCP_CHECK(cudaMemsetAsync(dscal, 0, sizeof(Scal), st));
+  RCP_CHECK(cudaMemsetAsync(d_off, 0, sizeof(double) * n, st));
+  if (trace_kind) RCP_CHECK(cudaMemsetAsync(trace_kind, -1, n, st));
+  if (trace_r) RCP_CHECK(cudaMemsetAsync(trace_r, 0xff, sizeof(int32_t) * n, st));
+
+  // ---- input validation + copy (factor.py:277-286)
+  RCP_CHECK(launch_validate_copy(a, lda, n, A[0], dscal->vflags, &dscal->amax, st));
+  RCP_CHECK(cudaMemcpyAsync(hscal, dscal, sizeof(Scal), cudaMemcpyDeviceToHost, st));
+  RCP_CHECK(cudaStreamSynchronize(st));
+  if (hscal->vflags[0]) return RCP_ERR_NOT_SYMMETRIC;
+  if (hscal->vflags[1]) return RCP_ERR_NONFINITE_INPUT;
+  const double amax = hscal->amax;
+
+  // ---- sketch B = Omega A (factor.py:307-309) and guard setup (factor.py:314-317)
+  RCP_CHECK(launch_sketch_gemm(P, n, omega_dev, n, A[0], n, B[0], 0, st));
+  const bool armed = c.robust_r >= 1;
+  double delta = armed ? 1.0 / c.robust_r : 0.0;
+  double thr = armed ? std::pow(DBL_EPSILON, delta) : 0.0;
+  double beta = 0.0;
+  if (armed) {
+    RCP_CHECK(launch_sketch_norm_max(B[0], P, n, &dscal->beta, st));
+    RCP_CHECK(cudaMemcpyAsync(hscal, dscal, sizeof(Scal), cudaMemcpyDeviceToHost, st));
+    RCP_CHECK(cudaStreamSynchronize(st));
+    beta = hscal->beta;
+  }
+  RCP_CHECK(launch_iota(n, permb[0], st));
+
+  int cur = 0;       // A / B buffer holding the current trailing block
+  int pcur = 0;      // perm buffer for the current order
+  int64_t k = 0;
+  int64_t snap_off = 0;
+  int64_t recomputes = 0;
+  int64_t deficient_from = -1;
+  std::vector<PanelRecord> panels;
+  std::vector<double> draw_buf;
+
+  if (armed && beta == 0.0) {  // factor.py:510-511
+    RCP_CHECK(launch_deficient_fill(n, 0, permb[0], perm, d_diag, d_off, pattern, st));
+    deficient_from = 0;
+    k = n;
+  }
+
+  while (k < n) {
+    const int k0 = (int)k;
+    const int width = (int)std::min<int64_t>(c.b, n - k0);
+    const int m0 = (int)(n - k0);
+    int G = std::min(num_sms, std::max(1, (m0 + kRowsMin - 1) / kRowsMin));
+    if (G > kMaxSMs) G = kMaxSMs;
+    int R = (m0 + G - 1) / G;
+    G = (m0 + R - 1) / R;
+    const int Wn = width + 2;
+    const int qn = (c.q > 1 && m0 > 1) ? std::min(std::min(c.q, width), std::min(m0, P)) : 0;
+    size_t fixed = 0;
+    fixed += ((size_t)4 * Wn + 15) & ~size_t(15);
+    fixed += ((size_t)4 * R + 15) & ~size_t(15);
+    fixed += ((size_t)8 * P + 15) & ~size_t(15);
+    fixed += 2 * (((size_t)8 * Wn + 15) & ~size_t(15));
+    long long avail = (long long)smem_budget - (long long)fixed;
+    int Rs = 0;
+    if (qn > 0) {
+      long long per_col = 8LL * P;
+      long long rs = (avail - 12LL * R - 64) / per_col;
+      Rs = (int)std::max(0LL, std::min<long long>(R, rs));
+    }
+    long long ls = (avail - 32LL * R - 64) / (8LL * R);
+    int Ls = (int)std::max(0LL, std::min<long long>(Wn, ls));
+    size_t need_q = qn > 0 ? (size_t)8 * P * Rs + 8 * (size_t)R + 4 * (size_t)R + 64 : 0;
+    size_t need_s = (size_t)8 * Ls * R + 32 * (size_t)R + 64;
+    size_t smem = fixed + std::max(need_q, need_s);
+
+    PanelParams prm{};
+    prm.n = n;
+    prm.k0 = k0;
+    prm.width = width;
+    prm.P = P;
+    prm.qn = qn;
+    prm.guard_mode = (armed && qn > 0) ? 1 : 0;
+    prm.guard_limit = thr * beta;
+    prm.alpha = std::sqrt(2.0) / 2.0;
+    prm.G = G;
+    prm.R = R;
+    prm.Rs = Rs;
+    prm.Ls = Ls;
+    prm.Wn = Wn;
+    prm.A = A[cur];
+    prm.B = B[cur];
+    prm.qscr = dptr(Lay.qscr);
+    prm.Lbuf = Lbuf;
+    prm.W = W;
+    prm.log_of_phys = lop;
+    prm.phys_of_log = pol;
+    prm.perm_cur = permb[pcur];
+    prm.perm_out = perm;
+    prm.d_diag = d_diag;
+    prm.d_off = d_off;
+    prm.pattern = pattern;
+    prm.trace_kind = trace_kind;
+    prm.trace_r = trace_r;
+    prm.flags = reinterpret_cast<long long*>(ws + Lay.flags);
+    prm.xrec = reinterpret_cast<XRec*>(ws + Lay.xrec);
+    prm.qrec = reinterpret_cast<QRec*>(ws + Lay.qrec);
+    prm.qcol = dptr(Lay.qcol);
+    prm.st = dstate;
+
+    bool stopped = false;
+    for (int attempt = 0;; ++attempt) {
+      RCP_CHECK(cudaMemsetAsync(&dstate->status, 0, sizeof(int), st));
+      EventPair& ep = new_pair(ev_panel);
+      RCP_CHECK(cudaEventRecord(ep.a, st));
+      RCP_CHECK(launch_panel(prm, G, smem, st));
+      RCP_CHECK(cudaEventRecord(ep.b, st));
+      RCP_CHECK(cudaMemcpyAsync(hstate, dstate, sizeof(PanelState), cudaMemcpyDeviceToHost, st));
+      RCP_CHECK(cudaStreamSynchronize(st));
+      if (hstate->status == 0) break;
+      if (hstate->status == 99) {
+        if (stats) snprintf(stats->message, sizeof(stats->message), "panel exchange watchdog fired at k=%d", k0);
+        return RCP_ERR_CUDA;
+      }
+      if (hstate->status == 2) {  // confirmed collapse: deficient tail (factor.py:405-410, 381-385)
+        stopped = true;
+        break;
+      }
+      // guard trip: fresh projection of the active block (factor.py:392-404)
+      if (!draw) {
+        if (stats) snprintf(stats->message, sizeof(stats->message), "guard recompute needs normals at k=%d", k0);
+        return RCP_ERR_NEED_NORMALS;
+      }
+      draw_buf.resize((size_t)P * m0);
+      if (draw(draw_ctx, P, m0, draw_buf.data()) != 0) return RCP_ERR_NEED_NORMALS;
+      RCP_CHECK(cudaMemcpyAsync(omg, draw_buf.data(), sizeof(double) * (size_t)P * m0, cudaMemcpyHostToDevice, st));
+      RCP_CHECK(launch_mirror_lower(n, k0, A[cur], st));
+      RCP_CHECK(launch_sketch_gemm(P, m0, omg, m0, A[cur] + k0 + (int64_t)k0 * n, n, B[cur], k0, st));
+      recomputes += 1;
+      delta += 1.0 / c.robust_r;
+      thr = std::pow(DBL_EPSILON, delta);
+      prm.guard_mode = 2;
+      prm.guard_limit = thr * beta;
+      (void)attempt;
+    }
+    if (stopped) {
+      RCP_CHECK(launch_deficient_fill(n, k0, permb[pcur], perm, d_diag, d_off, pattern, st));
+      deficient_from = k0;
+      break;
+    }
+    if (hstate->err != LLONG_MAX) {
+      if (stats) {
+        stats->num_kind = (int)(hstate->err & 0xff);
+        stats->num_step = (int)(hstate->err >> 8);
+        stats->n_steps = hstate->n_steps;
+        stats->n_2x2 = hstate->n_2x2;
+      }
+      return RCP_ERR_NUMERICAL;
+    }
+    const int k_end = hstate->k_end;
+    const int t = hstate->t_end;
+    const int64_t mp = n - k_end;
+    if (snap_off + m0 > Lay.snap_cap) {
+      if (stats) snprintf(stats->message, sizeof(stats->message), "snapshot capacity exceeded");
+      return RCP_ERR_WORKSPACE;
+    }
+    RCP_CHECK(launch_gather(n, k0, k_end, t, tpad, ((mp + 127) / 128) * 128, pol, Lbuf, W, permb[pcur],
+                            permb[pcur ^ 1], snap + snap_off, phys, Lneg, Wg, st));
+    panels.push_back(PanelRecord{k0, k_end, snap_off});
+    snap_off += m0;
+    if (mp > 0 && t > 0) {
+      EventPair& es = new_pair(ev_schur);
+      RCP_CHECK(cudaEventRecord(es.a, st));
+      RCP_CHECK(launch_schur_update(n, k_end, mp, Lneg, Wg, tpad, t, A[cur], phys, A[cur ^ 1], st));
+      RCP_CHECK(cudaEventRecord(es.b, st));
+      // sketch correction (factor.py:554-565)
+      RCP_CHECK(launch_ysolve(n, P, k0, t, tpad, pol, B[cur], Lbuf, Y, st));
+      RCP_CHECK(launch_sketch_correction(P, mp, k_end, Y, tpad, t, Lneg, B[cur], phys, B[cur ^ 1], st));
+      cur ^= 1;
+    }
+    pcur ^= 1;
+    k = k_end;
+  }
+
+  // ---- assemble L in final order + statistics (factor.py:514-538)
+  RCP_CHECK(cudaMemsetAsync(Lout, 0, sizeof(double) * (size_t)n * n, st));
+  RCP_CHECK(launch_unit_diag(n, Lout, st));
+  for (const PanelRecord& pr : panels) {
+    RCP_CHECK(launch_assemble_panel(n, pr.k0, pr.k_end, snap + pr.snap_off, poso, perm, Lbuf, Lout,
+                                    &dscal->maxmult, st));
+  }
+  RCP_CHECK(launch_dmax(n, d_diag, d_off, &dscal->dmax, st));
+  RCP_CHECK(cudaEventRecord(ev_stop, st));
+  RCP_CHECK(cudaMemcpyAsync(hscal, dscal, sizeof(Scal), cudaMemcpyDeviceToHost, st));
+  RCP_CHECK(cudaMemcpyAsync(hstate, dstate, sizeof(PanelState), cudaMemcpyDeviceToHost, st));
+  RCP_CHECK(cudaStreamSynchronize(st));
+
+  if (stats) {
+    stats->amax = amax;
+    stats->dmax = hscal->dmax;
+    stats->max_multiplier = n > 1 ? hscal->maxmult : 0.0;
+    if (amax == 0.0) {
+      stats->rho_cheap = hscal->dmax == 0.0 ? 1.0 : INFINITY;
+    } else {
+      stats->rho_cheap = hscal->dmax / amax;
+    }
+    stats->recompute_count = recomputes;
+    stats->n_panels = (int64_t)panels.size();
+    stats->n_steps = hstate->n_steps;
+    stats->n_2x2 = hstate->n_2x2;
+    stats->deficient_from = deficient_from;
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, ev_start, ev_stop);
+    stats->t_factor_ms = ms;
+    double tp = 0, ts = 0;
+    for (auto& e : ev_panel) {
+      float x = 0.f;
+      cudaEventElapsedTime(&x, e.a, e.b);
+      tp += x;
+    }
+    for (auto& e : ev_schur) {
+      float x = 0.f;
+      cudaEventElapsedTime(&x, e.a, e.b);
+      ts += x;
+    }
+    stats->t_panel_ms = tp;
+    stats->t_schur_ms = ts;
+  }
+  return RCP_OK;
+}
+
+
+size_t rcp_solve_workspace_bytes(int64_t n, int64_t nrhs) {
+  if (n < 1 || nrhs < 1) return 0;
+  return solve_workspace_bytes(n, nrhs) + 256;
+}
+
+int rcp_solve(int64_t n, const int64_t* perm, const double* L, const double* d_diag, const double* d_off,
+              const int8_t* pattern, int64_t nrhs, const double* b, double* x, void* workspace,
+              size_t workspace_bytes, int32_t* singular, void* cuda_stream) {
+  rcp_stats* stats = nullptr;
+  if (n < 1 || nrhs < 1 || !perm || !L || !d_diag || !d_off || !pattern || !b || !x) return RCP_ERR_INVALID_ARG;
+  const size_t need = rcp_solve_workspace_bytes(n, nrhs);
+  if (!workspace || workspace_bytes < need) return RCP_ERR_WORKSPACE;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(cuda_stream);
+  unsigned char* ws = reinterpret_cast<unsigned char*>(workspace);
+  int* dflag = reinterpret_cast<int*>(ws + solve_workspace_bytes(n, nrhs));
+  int dev = 0, num_sms = 0;
+  RCP_CHECK(cudaGetDevice(&dev));
+  RCP_CHECK(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev));
+  RCP_CHECK(cudaMemsetAsync(dflag, 0, sizeof(int), st));
+  RCP_CHECK(solve_device(n, perm, L, d_diag, d_off, pattern, nrhs, b, x, ws, dflag, st, num_sms));
+  int h = 0;
+  RCP_CHECK(cudaMemcpyAsync(&h, dflag, sizeof(int), cudaMemcpyDeviceToHost, st));
+  RCP_CHECK(cudaStreamSynchronize(st));
+  if (singular) *singular = h;
+  return RCP_OK;
+}
+
+int rcp_reconstruct(int64_t n, const double* L, const double* d_diag, const double* d_off, const int8_t* pattern,
+                    double* out, void* cuda_stream) {
+  rcp_stats* stats = nullptr;
+  if (n < 1 || !L || !d_diag || !d_off || !pattern || !out) return RCP_ERR_INVALID_ARG;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(cuda_stream);
+  void* scratch = nullptr;
+  RCP_CHECK(cudaMallocAsync(&scratch, sizeof(double) * (size_t)n * n, st));
+  cudaError_t e = reconstruct_device(n, L, d_diag, d_off, pattern, out, reinterpret_cast<double*>(scratch), st);
+  cudaFreeAsync(scratch, st);
+  RCP_CHECK(e);
+  RCP_CHECK(cudaStreamSynchronize(st));
+  return RCP_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,312 @@
+// Bandwidth-bound helper kernels of the RCP path: input validation + copy, sketch
+// norms, the per-panel gather (applies the panel's deferred permutation to the
+// operands of the trailing update), the small triangular sketch solve, the final
+// L assembly, statistics and the deficient-tail fill.
+#include <algorithm>
+#include <cfloat>
+#include "misc.cuh"
+#include "rcp_common.cuh"
+
+namespace rcp {
+
+namespace {
+
+__device__ double block_max(double v) {
+  __shared__ double sm[32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, off));
+  if (lane == 0) sm[warp] = v;
+  __syncthreads();
+  if (warp == 0) {
+    v = lane < nw ? sm[lane] : 0.0;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, off));
+  }
+  return v;  // valid in thread 0
+}
+
+// Exact-symmetry / finiteness check (core.py:48-53, factor.py:278-281), max|A|
+// (factor.py:286) and copy into the workspace, 32x32 tiles.
+__global__ void validate_copy_kernel(const double* __restrict__ a, int64_t lda, int64_t n,
+                                     double* __restrict__ out, int* flags, double* amax) {
+  __shared__ double tile[32][33];
+  const int64_t bi = (int64_t)blockIdx.y * 32, bj = (int64_t)blockIdx.x * 32;
+  const int tx = threadIdx.x, ty = threadIdx.y;  // 32 x 8
+  // tile[x][y] = a(bj + x, bi + y): the mirrored block, loaded coalesced
+  for (int r = ty; r < 32; r += 8) {
+    int64_t i = bj + tx, j = bi + r;
+    tile[tx][r] = (i < n && j < n) ? a[i + j * lda] : 0.0;
+  }
+  __syncthreads();
+  int asym = 0, nonfin = 0;
+  double mx = 0.0;
+  for (int r = ty; r < 32; r += 8) {
+    int64_t i = bi + tx, j = bj + r;  // element (i, j), column-major index i + j*lda
+    if (i < n && j < n) {
+      double v = a[i + j * lda];
+      double m = tile[r][tx];  // a(j, i)
+      if (!(v == m)) asym = 1;
+      if (!isfinite(v)) nonfin = 1;
+      mx = fmax(mx, fabs(v));
+      out[i + j * n] = v;
+    }
+  }
+  if (asym) atomicOr(flags + 0, 1);
+  if (nonfin) atomicOr(flags + 1, 1);
+  double bm = block_max(mx);
+  if (threadIdx.x == 0 && threadIdx.y == 0) atomic_max_nonneg(amax, bm);
+}
+
+// Scaled column norms of B (P x ncols, col-major ld P) -> max (metrics.norm_1_2, core.py:122-142).
+__global__ void sketch_norm_max_kernel(const double* __restrict__ B, int P, int64_t ncols, double* out) {
+  int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  double nv = 0.0;
+  if (j < ncols) {
+    const double* c = B + j * P;
+    double scale = 0.0;
+    for (int r = 0; r < P; ++r) scale = fmax(scale, fabs(c[r]));
+    if (scale > 0.0) {
+      double ss = 0.0;
+      for (int r = 0; r < P; ++r) {
+        double x = fabs(c[r]) / scale;
+        ss = __fma_rn(x, x, ss);
+      }
+      nv = scale * sqrt(ss);
+    }
+  }
+  double bm = block_max(nv);
+  if (threadIdx.x == 0) atomic_max_nonneg(out, bm);
+}
+
+// Gather after a panel: applies the panel's permutation to the trailing-update operands.
+//   phys[j]        = physical row of new logical k_end + j
+//   Lneg[j][s]     = -L(panel col s) at that row   (K-contiguous, ld tpad, zero padded)
+//   Wg[j][s]       =  W(panel col s) at that row
+//   perm_next      = original index per new logical position
+//   snap[x]        = perm at the panel start (for the final L assembly)
+__global__ void gather_kernel(int64_t n, int k0, int k_end, int t, int tpad, int64_t rows_pad,
+                              const int* __restrict__ phys_of_log, const double* __restrict__ Lbuf,
+                              const double* __restrict__ W, const int* __restrict__ perm_cur,
+                              int* __restrict__ perm_next, int* __restrict__ snap,
+                              int* __restrict__ phys, double* __restrict__ Lneg, double* __restrict__ Wg) {
+  const int64_t mp = n - k_end;
+  const int64_t m0 = n - k0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.y;
+  const int64_t jend = rows_pad > m0 ? rows_pad : m0;
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.y + threadIdx.y; j < jend; j += stride) {
+    const bool live = j < mp;
+    const int pj = live ? phys_of_log[k_end + j] : 0;
+    if (j < rows_pad) for (int s = threadIdx.x; s < tpad; s += blockDim.x) {
+      double lv = 0.0, wv = 0.0;
+      if (live && s < t) {
+        lv = -Lbuf[pj + (int64_t)(k0 + s) * n];
+        wv = W[pj + (int64_t)s * n];
+      }
+      Lneg[j * tpad + s] = lv;
+      Wg[j * tpad + s] = wv;
+    }
+    if (threadIdx.x == 0) {
+      if (live) {
+        phys[j] = pj;
+        perm_next[k_end + j] = perm_cur[pj];
+      }
+      if (j < m0) snap[j] = perm_cur[k0 + j];
+    }
+  }
+}
+
+// Y = B1 * L11^{-T}  (P x t), with B1[:, a] = Bin[:, piv[a]] and L11 the panel's
+// unit-lower block in logical order.  Algebraically equal to the reference's
+// B1 @ solve_triangular(L11, L21^T, trans='T') (factor.py:554-561).  16 sketch rows per
+// CTA, 16 lanes per row.
+__global__ void ysolve_kernel(int64_t n, int P, int k0, int t, int tpad, const int* __restrict__ phys_of_log,
+                              const double* __restrict__ Bin, const double* __restrict__ Lbuf,
+                              double* __restrict__ Y) {
+  extern __shared__ double sm[];
+  double* L11 = sm;                 // [t][t]
+  double* yv = sm + (size_t)t * t;  // [16][tpad]
+  const int tid = threadIdx.x;
+  for (int f = tid; f < t * t; f += blockDim.x) {
+    int a = f / t, c = f - a * t;
+    double v = 0.0;
+    if (c < a) v = Lbuf[phys_of_log[k0 + a] + (int64_t)(k0 + c) * n];
+    L11[f] = v;
+  }
+  const int rr = tid >> 4, l16 = tid & 15;
+  const int r = blockIdx.x * 16 + rr;
+  for (int a = l16; a < tpad; a += 16) yv[rr * tpad + a] = 0.0;
+  __syncthreads();
+  for (int a = 0; a < t; ++a) {
+    double part = 0.0;
+    for (int c = l16; c < a; c += 16) part = __fma_rn(L11[a * t + c], yv[rr * tpad + c], part);
+#pragma unroll
+    for (int off = 8; off > 0; off >>= 1) part = __dadd_rn(part, __shfl_xor_sync(0xffffffffu, part, off, 16));
+    if (l16 == 0) {
+      double b1 = (r < P) ? Bin[r + (int64_t)phys_of_log[k0 + a] * P] : 0.0;
+      yv[rr * tpad + a] = __dsub_rn(b1, part);
+    }
+    __syncwarp();
+  }
+  if (r < P) {
+    for (int a = l16; a < tpad; a += 16) Y[(int64_t)r * tpad + a] = yv[rr * tpad + a];
+  }
+}
+
+// pos_of_orig[snap[x]] = x for one panel's snapshot.
+__global__ void invert_snapshot_kernel(int64_t m0, const int* __restrict__ snap, int* __restrict__ pos_of_orig) {
+  int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (x < m0) pos_of_orig[snap[x]] = static_cast<int>(x);
+}
+
+// L (row-major, final order) for columns [k0, k_end) of one panel:
+// L[i, c] = Lbuf[k0 + pos_p(perm[i]), c] for i > c (factor.py:339-340 applied lazily).
+__global__ void assemble_panel_kernel(int64_t n, int k0, int k_end, const int64_t* __restrict__ perm,
+                                      const int* __restrict__ pos_of_orig, const double* __restrict__ Lbuf,
+                                      double* __restrict__ L, double* maxmult) {
+  const int w = k_end - k0;
+  double mx = 0.0;
+  for (int64_t i = (int64_t)k0 + 1 + blockIdx.x; i < n; i += gridDim.x) {
+    const int64_t src = k0 + pos_of_orig[perm[i]];
+    const int cmax = static_cast<int>(i < (int64_t)k_end ? i : (int64_t)k_end);
+    for (int c = k0 + threadIdx.x; c < cmax; c += blockDim.x) {
+      double v = Lbuf[src + (int64_t)c * n];
+      L[i * n + c] = v;
+      mx = fmax(mx, fabs(v));
+    }
+  }
+  (void)w;
+  double bm = block_max(mx);
+  if (threadIdx.x == 0) atomic_max_nonneg(maxmult, bm);
+}
+
+__global__ void unit_diag_kernel(int64_t n, double* L) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) L[i * n + i] = 1.0;
+}
+
+__global__ void dmax_kernel(int64_t n, const double* __restrict__ dd, const double* __restrict__ doff, double* out) {
+  double mx = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    mx = fmax(mx, fmax(fabs(dd[i]), fabs(doff[i])));
+  double bm = block_max(mx);
+  if (threadIdx.x == 0) atomic_max_nonneg(out, bm);
+}
+
+// Deficient tail (factor.py:381-385): zero 1x1 blocks, pattern 3, order as it stands.
+__global__ void deficient_fill_kernel(int64_t n, int64_t k0, const int* __restrict__ perm_cur, int64_t* perm_out,
+                                      double* dd, double* doff, int8_t* pattern) {
+  int64_t x = k0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (x < n) {
+    dd[x] = 0.0;
+    doff[x] = 0.0;
+    pattern[x] = 3;
+    perm_out[x] = perm_cur[x];
+  }
+}
+
+// Copy the lower triangle of the trailing block [k:, k:] onto its upper triangle.
+__global__ void mirror_lower_kernel(int64_t n, int64_t k, double* A) {
+  __shared__ double tile[32][33];
+  const int64_t bi = k + (int64_t)blockIdx.y * 32, bj = k + (int64_t)blockIdx.x * 32;
+  if (blockIdx.x > blockIdx.y) return;  // only tiles with bi >= bj (lower) are sources
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  for (int r = ty; r < 32; r += 8) {
+    int64_t i = bi + tx, j = bj + r;
+    tile[r][tx] = (i < n && j < n) ? A[i + j * n] : 0.0;
+  }
+  __syncthreads();
+  for (int r = ty; r < 32; r += 8) {
+    int64_t i = bj + tx, j = bi + r;  // destination (i, j) = upper element, source (j, i)
+    if (i < n && j < n && i < j) A[i + j * n] = tile[tx][r];
+  }
+}
+
+__global__ void iota_kernel(int64_t n, int* p) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) p[i] = static_cast<int>(i);
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ launchers
+cudaError_t launch_validate_copy(const double* a, int64_t lda, int64_t n, double* out, int* flags, double* amax,
+                                 cudaStream_t st) {
+  dim3 grid((unsigned)((n + 31) / 32), (unsigned)((n + 31) / 32)), block(32, 8);
+  validate_copy_kernel<<<grid, block, 0, st>>>(a, lda, n, out, flags, amax);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_sketch_norm_max(const double* B, int P, int64_t ncols, double* out, cudaStream_t st) {
+  sketch_norm_max_kernel<<<(unsigned)((ncols + 255) / 256), 256, 0, st>>>(B, P, ncols, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gather(int64_t n, int k0, int k_end, int t, int tpad, int64_t rows_pad, const int* phys_of_log,
+                          const double* Lbuf, const double* W, const int* perm_cur, int* perm_next, int* snap,
+                          int* phys, double* Lneg, double* Wg, cudaStream_t st) {
+  dim3 block(32, 8);
+  int64_t rows = rows_pad > (n - k0) ? rows_pad : (n - k0);
+  unsigned grid = (unsigned)std::min<int64_t>((rows + 7) / 8, 148 * 16);
+  gather_kernel<<<grid, block, 0, st>>>(n, k0, k_end, t, tpad, rows_pad, phys_of_log, Lbuf, W, perm_cur,
+                                        perm_next, snap, phys, Lneg, Wg);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_ysolve(int64_t n, int P, int k0, int t, int tpad, const int* phys_of_log, const double* Bin,
+                          const double* Lbuf, double* Y, cudaStream_t st) {
+  size_t smem = sizeof(double) * ((size_t)t * t + 16 * (size_t)tpad);
+  cudaError_t e = cudaFuncSetAttribute(ysolve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  ysolve_kernel<<<(unsigned)((P + 15) / 16), 256, smem, st>>>(n, P, k0, t, tpad, phys_of_log, Bin, Lbuf, Y);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_assemble_panel(int64_t n, int k0, int k_end, const int* snap, int* pos_of_orig,
+                                  const int64_t* perm, const double* Lbuf, double* L, double* maxmult,
+                                  cudaStream_t st) {
+  int64_t m0 = n - k0;
+  invert_snapshot_kernel<<<(unsigned)((m0 + 255) / 256), 256, 0, st>>>(m0, snap, pos_of_orig);
+  int64_t rows = n - k0 - 1;
+  if (rows > 0) {
+    unsigned grid = (unsigned)std::min<int64_t>(rows, 148 * 8);
+    int w = k_end - k0;
+    int threads = w >= 128 ? 128 : ((w + 31) / 32) * 32;
+    assemble_panel_kernel<<<grid, threads, 0, st>>>(n, k0, k_end, perm, pos_of_orig, Lbuf, L, maxmult);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_unit_diag(int64_t n, double* L, cudaStream_t st) {
+  unit_diag_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(n, L);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_dmax(int64_t n, const double* dd, const double* doff, double* out, cudaStream_t st) {
+  unsigned grid = (unsigned)std::min<int64_t>((n + 255) / 256, 148 * 4);
+  dmax_kernel<<<grid, 256, 0, st>>>(n, dd, doff, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_deficient_fill(int64_t n, int64_t k0, const int* perm_cur, int64_t* perm_out, double* dd,
+                                  double* doff, int8_t* pattern, cudaStream_t st) {
+  if (n - k0 <= 0) return cudaSuccess;
+  deficient_fill_kernel<<<(unsigned)((n - k0 + 255) / 256), 256, 0, st>>>(n, k0, perm_cur, perm_out, dd, doff,
+                                                                          pattern);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_mirror_lower(int64_t n, int64_t k, double* A, cudaStream_t st) {
+  int64_t m = n - k;
+  unsigned nb = (unsigned)((m + 31) / 32);
+  dim3 grid(nb, nb), block(32, 8);
+  mirror_lower_kernel<<<grid, block, 0, st>>>(n, k, A);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_iota(int64_t n, int* p, cudaStream_t st) {
+  iota_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(n, p);
+  return cudaGetLastError();
+}
+
+}  // namespace rcp

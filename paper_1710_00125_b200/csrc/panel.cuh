@@ -1,0 +1,71 @@
+// Panel-kernel parameter/state structs shared by panel.cu and the host driver.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace rcp {
+
+// Device-resident state that persists across panel launches.
+struct PanelState {
+  long long seq;       // monotonically increasing exchange sequence number
+  long long err;       // (step << 8) | kind of the first numerical error, LLONG_MAX if none
+  int k_end;           // logical index after the panel
+  int t_end;           // columns eliminated by the panel
+  int status;          // 0 ok, 1 guard trip (recompute needed), 2 guard stop (deficient tail)
+  int n_steps;         // decisions taken (cumulative)
+  int n_2x2;           // 2x2 blocks (cumulative)
+  int pad;
+};
+
+// One CTA's contribution to a pivot-search exchange (SBKP step).
+struct XRec {
+  double key;   // |c| of the CTA's best candidate row, -1 if none
+  double val;   // signed c at that row
+  double diag;  // current Schur-complement diagonal at that row
+  double akk;   // pivot diagonal (valid if has_akk)
+  int lidx;     // logical (panel-relative) index of the candidate
+  int phys;     // physical (panel-relative) row of the candidate
+  int has_akk;
+  int err;
+};
+
+// One CTA's contribution to a QRCP exchange.
+struct QRec {
+  double norm;  // residual norm of the best local column, -1 if none
+  int pos;      // its current position (panel-relative)
+  int col;      // its panel-start column (panel-relative)
+};
+
+struct PanelParams {
+  int64_t n;
+  int k0, width, P, qn;
+  int guard_mode;      // 0 none, 1 trip check, 2 stop check (after a recompute)
+  double guard_limit;  // thr * beta
+  double alpha;
+  int G, R, Rs, Ls, Wn;
+  const double* A;     // trailing matrix at panel start, col-major ld n, lower triangle valid
+  const double* B;     // sketch, P x n col-major (ld P), panel-start order
+  double* qscr;        // spill for sketch columns that do not fit in smem
+  double* Lbuf;        // n x n col-major; column c holds rows in its panel's start order
+  double* W;           // n x (b+2) col-major, unscaled panel columns (L * D)
+  int* log_of_phys;    // out: logical index of each physical row (absolute)
+  int* phys_of_log;    // out: physical row of each logical index (absolute)
+  const int* perm_cur; // original index of each physical row at panel start
+  int64_t* perm_out;
+  double* d_diag;
+  double* d_off;
+  int8_t* pattern;
+  int8_t* trace_kind;
+  int32_t* trace_r;
+  long long* flags;    // [G]
+  XRec* xrec;          // [2][G]
+  QRec* qrec;          // [2][G]
+  double* qcol;        // [2][G][P]
+  PanelState* st;
+};
+
+cudaError_t panel_init_attributes(int max_dyn_smem);
+cudaError_t launch_panel(const PanelParams& prm, int G, size_t smem, cudaStream_t st);
+int panel_static_smem_bytes();
+
+}  // namespace rcp

@@ -1,0 +1,95 @@
+// Shared device helpers for the RCP block-LDL^T kernels (sm_100a).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#define RCP_HD __host__ __device__ __forceinline__
+#define RCP_D __device__ __forceinline__
+
+namespace rcp {
+
+constexpr int kMaxSMs = 160;
+
+// ---------------------------------------------------------------- memory ordering
+// Loads of data written by other CTAs during the same launch go to L2 (.cg) so a
+// stale L1 line can never be observed; flags use acquire/release at gpu scope.
+RCP_D double ldcg(const double* p) { return __ldcg(p); }
+RCP_D int ldcg(const int* p) { return __ldcg(p); }
+RCP_D long long ld_acquire(const long long* p) {
+  long long v;
+  asm volatile("ld.acquire.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+RCP_D void st_release(long long* p, long long v) {
+  asm volatile("st.release.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// ---------------------------------------------------------------- symmetric access
+// Trailing blocks keep only the LOWER triangle valid (column-major, ld = n).
+RCP_D double sym_lower(const double* a, int64_t ld, int64_t i, int64_t j) {
+  return (i >= j) ? a[i + j * ld] : a[j + i * ld];
+}
+
+// ---------------------------------------------------------------- pivot-column dot
+// Dot product of row i of the panel L (Lrow(s)) with the pivot's W row w[s], s < t,
+// as 4 interleaved chains combined ((c0+c1)+(c2+c3)).  The GEMV, the redundant
+// single-row recomputation and the trailing-diagonal updates all use this exact
+// routine so every CTA derives bitwise-identical column entries.
+template <class F>
+RCP_D double chain_dot4(F lrow, const double* w, int t) {
+  double c0 = 0.0, c1 = 0.0, c2 = 0.0, c3 = 0.0;
+  int s = 0;
+  for (; s + 4 <= t; s += 4) {
+    c0 = __fma_rn(lrow(s), w[s], c0);
+    c1 = __fma_rn(lrow(s + 1), w[s + 1], c1);
+    c2 = __fma_rn(lrow(s + 2), w[s + 2], c2);
+    c3 = __fma_rn(lrow(s + 3), w[s + 3], c3);
+  }
+  if (s < t) c0 = __fma_rn(lrow(s), w[s], c0);
+  if (s + 1 < t) c1 = __fma_rn(lrow(s + 1), w[s + 1], c1);
+  if (s + 2 < t) c2 = __fma_rn(lrow(s + 2), w[s + 2], c2);
+  return __dadd_rn(__dadd_rn(c0, c1), __dadd_rn(c2, c3));
+}
+
+// ---------------------------------------------------------------- argmax comparators
+// numpy argmax semantics: NaN wins (first NaN), otherwise largest value, ties to the
+// lowest index.
+RCP_D bool better(double va, long long ia, double vb, long long ib) {
+  bool na = va != va, nb = vb != vb;
+  if (na != nb) return na;
+  if (!na && va != vb) return va > vb;
+  return ia < ib;
+}
+
+// ---------------------------------------------------------------- DMMA (FP64 tensor core)
+// mma.sync m8n8k4 f64: a = A[g][q], b = B[q][g], c/d = C[g][2q + {0,1}], g = lane>>2, q = lane&3.
+RCP_D void dmma_8x8x4(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+RCP_D void cp_async8(void* smem, const void* gmem, bool pred) {
+  unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  int n = pred ? 8 : 0;
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(n));
+}
+RCP_D void cp_async16(void* smem, const void* gmem, bool pred) {
+  unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  int n = pred ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(n));
+}
+RCP_D void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+RCP_D void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+// Atomic max for non-negative doubles (bit patterns order like the values).
+RCP_D void atomic_max_nonneg(double* addr, double v) {
+  if (!(v >= 0.0)) {  // NaN: record as +inf so it is visible to the host
+    v = __longlong_as_double(0x7ff0000000000000LL);
+  }
+  atomicMax(reinterpret_cast<unsigned long long*>(addr),
+            static_cast<unsigned long long>(__double_as_longlong(v)));
+}
+
+}  // namespace rcp

@@ -1,0 +1,148 @@
+"""GPU parity: the CUDA path (through the C ABI) against the reference fixtures and the oracle.
+
+Bar (BASELINE.json north_star): identical pivot sequence and 1x1/2x2 structure,
+L and D within the stated tolerance ``conftest.l_tol(n)`` (10x the CPU rounding
+noise floor), solve x within a conditioning-scaled tolerance, backward error and
+growth within small factors of the reference.
+"""
+
+import numpy as np
+import pytest
+
+from conftest import golden_names, l_tol, load_golden
+
+pytestmark = pytest.mark.gpu
+
+Q_B_CASES = [n for n in golden_names() if "_q1_" not in n]
+
+
+def _gpu_factor(a, cfg, robust=False, trace=False):
+    import torch
+
+    from paper_1710_00125_b200 import api
+    c = api.FactorConfig(**cfg)
+    if robust and c.robust_r < 1:
+        raise ValueError
+    ad = torch.from_numpy(np.ascontiguousarray(a)).cuda()
+    df = api.factor_device(ad, c, trace=trace)
+    torch.cuda.synchronize()
+    return df
+
+
+def _assert_factor_parity(g, f, n):
+    assert np.array_equal(f.perm, g["perm"]), "pivot sequence differs"
+    assert np.array_equal(f.pattern, g["pattern"]), "block structure differs"
+    tol = l_tol(n)
+    dd = np.concatenate([g["d_diag"], g["d_off"]])
+    dscale = max(1.0, float(np.abs(dd).max()))
+    got = np.concatenate([f.d_diag, f.d_off])
+    assert np.abs(got - dd).max() <= tol * dscale
+    if "L" in g:
+        assert np.abs(f.L - g["L"]).max() <= tol
+    assert np.abs(f.L.sum(axis=1) - g["L_rowsum"]).max() <= tol * n
+
+
+@pytest.mark.parametrize("name", Q_B_CASES)
+def test_factor_matches_reference_fixture(cuda_ok, name):
+    from paper_1710_00125_b200 import api
+    g = load_golden(name)
+    a = g["a"]
+    n = a.shape[0]
+    df = _gpu_factor(a, g["cfg"])
+    hf = df.to_host()
+
+    class F:  # flat view for the comparison helper
+        perm = hf.perm
+        pattern = hf.pattern
+        L = hf.L
+        d_diag = df.d_diag.cpu().numpy()
+        d_off = df.d_off.cpu().numpy()
+
+    _assert_factor_parity(g, F, n)
+    assert hf.stats.recompute_count == int(g["recompute_count"])
+    rho_ref = float(g["rho_cheap"])
+    assert abs(hf.stats.rho_cheap - rho_ref) <= l_tol(n) * max(1.0, rho_ref)
+    assert abs(hf.stats.max_multiplier - float(g["max_multiplier"])) <= l_tol(n) * 10
+    # the reference's reconstruction criterion (test_factor.py:59-67)
+    perm = hf.perm
+    den = float(np.abs(a).max()) or 1.0
+    rec = hf.L @ hf.D.to_dense() @ hf.L.T
+    assert float(np.abs(rec - a[np.ix_(perm, perm)]).max()) / den <= 1e-12
+    # solve parity (solve.py:79-92)
+    from paper_1710_00125_b200 import gallery
+    rep = api.solve(hf, gallery.rhs(n, 1), a)
+    assert rep.singular == bool(g["singular"])
+    if not rep.singular:
+        xr = g["x"]
+        assert np.abs(rep.x - xr).max() <= 1e-8 * max(1.0, np.abs(xr).max())
+        assert rep.backward_error <= max(1e-13, 100 * float(g["backward_error"]))
+
+
+def test_trace_is_consistent_with_pattern(cuda_ok):
+    g = load_golden("g_n300_b32")
+    df = _gpu_factor(g["a"], g["cfg"], trace=True)
+    kinds = df.trace_kind.cpu().numpy()
+    pat = df.pattern.cpu().numpy()
+    two = np.nonzero(kinds == 3)[0]
+    assert np.all(pat[two] == 1) and np.all(pat[two + 1] == 2)
+    assert df.stats["n_2x2"] == int((pat == 1).sum())
+
+
+@pytest.mark.parametrize("n,b,p,seed", [(64, 8, 10, 0), (257, 16, 26, 1), (512, 32, 42, 2), (640, 64, 74, 3)])
+def test_factor_matches_oracle_live(cuda_ok, n, b, p, seed):
+    from oracle.rcp_oracle import OracleConfig, oracle_factor
+    from paper_1710_00125_b200 import gallery
+    a = gallery.type6(n, 1000 + seed)
+    o = oracle_factor(a, OracleConfig(b=b, q=b, p=p, seed=seed))
+    df = _gpu_factor(a, dict(strategy="rcp", b=b, q=b, p=p, seed=seed))
+    hf = df.to_host()
+    assert np.array_equal(hf.perm, o.perm)
+    assert np.array_equal(hf.pattern, o.pattern)
+    assert np.abs(hf.L - o.L).max() <= l_tol(n)
+    dref = o.d_dense()
+    assert np.abs(hf.D.to_dense() - dref).max() <= l_tol(n) * max(1.0, np.abs(dref).max())
+
+
+def test_input_validation_errors(cuda_ok):
+    from paper_1710_00125_b200 import api
+    with pytest.raises(ValueError, match="symmetric"):
+        api.factor(np.array([[1.0, 2.0], [3.0, 4.0]]), strategy="rcp", b=2, q=2, p=2)
+    with pytest.raises(ValueError):
+        api.factor(np.array([[np.nan, 0.0], [0.0, 1.0]]), strategy="rcp", b=2, q=2, p=2)
+    with pytest.raises(ValueError, match="NaN or Inf"):
+        api.factor(np.array([[np.inf, 0.0], [0.0, 1.0]]), strategy="rcp", b=2, q=2, p=2)
+
+
+def test_input_is_not_modified(cuda_ok):
+    import torch
+
+    from paper_1710_00125_b200 import api, gallery
+    a = gallery.type6(130, 7)
+    ad = torch.from_numpy(a).cuda()
+    before = ad.clone()
+    api.factor_device(ad, api.FactorConfig(b=16, q=16, p=20, seed=1))
+    torch.cuda.synchronize()
+    assert torch.equal(ad, before)
+
+
+def test_solve_many_matches_columnwise(cuda_ok):
+    from paper_1710_00125_b200 import api, gallery
+    a = gallery.type6(200, 11)
+    f = api.factor(a, strategy="rcp", b=16, q=16, p=20, seed=4)
+    rhs = np.random.Generator(np.random.Philox(3)).standard_normal((200, 3))
+    xm = api.solve_many(f, rhs)
+    for j in range(3):
+        xj = api.solve(f, rhs[:, j]).x
+        assert np.allclose(xm[:, j], xj, rtol=1e-12, atol=1e-12)
+    assert np.allclose(a @ xm, rhs, atol=1e-9)
+
+
+def test_deficient_solve_flags_singular(cuda_ok):
+    from paper_1710_00125_b200 import api
+    g = load_golden("g_zero_tail")
+    f = api.factor_robust(g["a"], api.FactorConfig(**{k: v for k, v in g["cfg"].items()}))
+    assert f.deficient_from == 40
+    assert np.all(f.pattern[40:] == api.PAT_DEFICIENT)
+    rep = api.solve(f, g["a"] @ np.ones(65), g["a"])
+    assert rep.singular
+    assert rep.backward_error <= 1e-12
