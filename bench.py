@@ -1,0 +1,339 @@
+#!/usr/bin/env python
+"""Benchmark: RCP block-LDL^T fp64 factorization at BASELINE.json's headline config.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+One "step" = one full RCP factorization (q = b mode) of the config-3 workload:
+a seeded type-6 symmetric Gaussian matrix, n = 32768, b = 128, sketch rows
+P = b + 16 = 144 (reference FactorConfig(strategy="rcp", b=128, q=128, p=144)).
+``value`` = n^3/3 flop per factorization / device time (CUDA events, inputs
+resident in HBM, max over ranks), summed over ranks.  The input (8.6 GB) is far
+larger than the 126 MB L2, so no L2 flush is needed between steps.
+
+Multi-GPU (torchrun, one process per GPU): round 1 runs independent replicas
+(each rank factors its own matrix; "scaling": "weak"); the 1D block-cyclic
+distributed factorization is future work.
+
+``--impl reference`` times the reference algorithm's CPU implementation (the
+oracle port in oracle/rcp_oracle.py — the reference is pure Python and cannot be
+shipped to the GPU box) on the host cores, on the same workload, one panel per
+step (a bounded sample), rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "RCP LDL^T fp64 GFLOP/s (n³/3) at n=32768, % of FP64 peak; 1/2/4/8 GPU"
+FP64_PEAK_GFLOPS = 37170.0   # measured DMMA peak, profiles/r01_fp64_peaks.txt (MEASURED_PEAKS.json has no FP64)
+FP64_PEAK_SRC = "measured DMMA m8n8k4 microbenchmark on this pool's B200 (profiles/r01_fp64_peaks.txt)"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--n", type=int, default=32768)
+    ap.add_argument("--b", type=int, default=128)
+    ap.add_argument("--p", type=int, default=144, help="sketch rows P (reference FactorConfig.p = b + oversampling)")
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--cpu-seconds", type=float, default=20.0, help="budget of the cpu_baseline sample")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def workload_name(a):
+    return (f"C3 type6 (seeded iid N(0,1) lower triangle mirrored) n={a.n}, b={a.b}, q=b, "
+            f"P=b+{a.p - a.b}={a.p} sketch rows, seed={a.seed}")
+
+
+def cfg_dict(a):
+    return {"workload": workload_name(a), "n": a.n, "b": a.b, "q": a.b, "p_sketch": a.p,
+            "oversampling": a.p - a.b, "parallelism": "replicas",
+            "l2": "input 8.6 GB >> 126 MB L2 (no flush needed)"}
+
+
+def work_flops(n: int, k0: int, k1: int) -> float:
+    """n^3/3-model flops attributable to eliminating columns [k0, k1): sum (n - j)^2."""
+    def s(m):  # sum_{i=1}^{m} i^2
+        return m * (m + 1) * (2 * m + 1) / 6.0
+    return s(n - k0) - s(n - k1)
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            threading.Thread(target=self._read, daemon=True).start()
+        except FileNotFoundError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.3)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- CPU baseline
+def cpu_sample(a_host, args, budget_s: float, max_panels: int | None = None, skip_panels: int = 0):
+    """Time the oracle port (the reference algorithm, numpy/OpenBLAS) panel by panel."""
+    from oracle.rcp_oracle import OracleConfig, _State
+    cfg = OracleConfig(p=args.p, b=args.b, q=args.b, seed=args.seed)
+    t0 = time.perf_counter()
+    st = _State(a_host, cfg)
+    t_setup = time.perf_counter() - t0
+    if st.armed and st.beta == 0.0:
+        raise RuntimeError("degenerate workload")
+    times, works = [], []
+    npan = 0
+    t_start = time.perf_counter()
+    while st.k < st.n and not st.stopped:
+        k0 = st.k
+        t1 = time.perf_counter()
+        st.panel()
+        dt = time.perf_counter() - t1
+        npan += 1
+        if npan > skip_panels:
+            times.append(dt)
+            works.append(work_flops(st.n, k0, st.k))
+        if max_panels is not None and npan >= max_panels + skip_panels:
+            break
+        if max_panels is None and time.perf_counter() - t_start >= budget_s:
+            break
+    return {"t_setup": t_setup, "times": times, "works": works, "k_done": st.k, "panels": npan}
+
+
+def cores_used() -> int:
+    try:
+        from threadpoolctl import threadpool_info
+        info = [i for i in threadpool_info() if i.get("user_api") == "blas"]
+        if info:
+            return int(info[0]["num_threads"])
+    except Exception:
+        pass
+    return os.cpu_count() or 1
+
+
+# ----------------------------------------------------------------------------- reference arm
+def run_reference(args, rank: int):
+    if rank != 0:
+        return
+    from paper_1710_00125_b200 import gallery
+    a_host = gallery.type6(args.n, args.seed)
+    res = cpu_sample(a_host, args, budget_s=1e9, max_panels=args.steps, skip_panels=args.warmup)
+    tsum = sum(res["times"])
+    value = sum(res["works"]) / tsum / 1e9
+    sample = (f"oracle port (numpy {np.__version__} + OpenBLAS) factor() on the config-3 matrix: panels "
+              f"{args.warmup + 1}..{args.warmup + args.steps} timed one per step (panels 1..{args.warmup} warm-up), "
+              f"columns 0..{res['k_done']} eliminated; value = sum (n-j)^2 over the timed panels' columns / time; "
+              f"setup (validation, copy, Omega*A) {res['t_setup']:.1f} s excluded")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tsum / max(1, len(res["times"])),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded numpy Philox type6)", "config": cfg_dict(args),
+        "cpu_baseline": {"value": value, "unit": "GFLOP/s", "cores": cores_used(), "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- B200 arm
+def run_b200(args, rank: int, world: int, local_rank: int):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1710_00125_b200 import api, gallery
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    n, P = args.n, args.p
+    cfg = api.FactorConfig(strategy="rcp", b=args.b, q=args.b, p=P, seed=args.seed)
+
+    a_host = gallery.type6(n, args.seed + rank)
+    a_pin = torch.from_numpy(a_host).pin_memory()
+    a_dev = a_pin.to(dev, non_blocking=True)
+    omega = torch.from_numpy(np.random.Generator(np.random.Philox(cfg.seed)).standard_normal((P, n))).to(dev)
+    ws = torch.empty(api.workspace_bytes(n, cfg), dtype=torch.uint8, device=dev)
+    out = None
+    for _ in range(max(3, args.warmup)):
+        out = api.factor_device(a_dev, cfg, omega=omega, workspace=ws, out=out)
+    torch.cuda.synchronize()
+
+    clk = ClockSampler(local_rank)
+    clk.start()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    schur_ms, schur_flops, panel_ms = 0.0, 0.0, 0.0
+    for _ in range(args.steps):
+        out = api.factor_device(a_dev, cfg, omega=omega, workspace=ws, out=out)
+        schur_ms += out.stats["t_schur_ms"]
+        schur_flops += out.stats["schur_flops"]
+        panel_ms += out.stats["t_panel_ms"]
+    e1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = clk.stop()
+    ms = e0.elapsed_time(e1) / args.steps
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    flops = n ** 3 / 3.0
+    value = world * flops / (ms_max / 1e3) / 1e9
+    stats = dict(out.stats)
+
+    # quick accuracy check of the last factorization on the device (solve + residual)
+    rhs = torch.from_numpy(gallery.rhs(n, 1)).to(dev)
+    x, _ = api.solve_device(out, rhs)
+    resid = float((a_dev @ x - rhs).abs().max())
+    bwd = resid / (float(a_dev.abs().sum(dim=1).max()) * float(x.abs().max()))
+
+    # end to end through the public API: numpy in (pinned) -> Factorization out
+    e2e_val = None
+    h2d = n * n * 8 + P * n * 8
+    d2h = n * n * 8 + n * (8 + 8 + 8 + 1)
+    a_np_pinned = a_pin.numpy()
+    e2e_times = []
+    for _ in range(max(1, args.e2e_steps)):
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        f = api.factor(a_np_pinned, cfg)
+        _ = f.L[-1, 0]
+        e2e_times.append(time.perf_counter() - t0)
+        del f
+    te = torch.tensor([statistics.median(e2e_times)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_val = world * flops / float(te.item()) / 1e9
+
+    if rank != 0:
+        return
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        try:
+            del out, ws
+            torch.cuda.empty_cache()
+            res = cpu_sample(a_host, args, budget_s=args.cpu_seconds)
+            cv = sum(res["works"]) / sum(res["times"]) / 1e9
+            cpu = {"value": cv, "unit": "GFLOP/s", "cores": cores_used(), "kind": "port",
+                   "sample": (f"oracle port of the reference algorithm (numpy {np.__version__}/OpenBLAS), first "
+                              f"{res['panels']} panel(s) of the same n={n} matrix (columns 0..{res['k_done']}), "
+                              f"{sum(res['times']):.1f} s; value = sum (n-j)^2 over eliminated columns / panel time; "
+                              f"setup {res['t_setup']:.1f} s excluded")}
+        except MemoryError:
+            cpu = {"value": None, "unit": "GFLOP/s", "cores": cores_used(), "kind": "port",
+                   "sample": "host out of memory for the n=32768 oracle sample"}
+    achieved = schur_flops / (schur_ms / 1e3) / 1e12 if schur_ms > 0 else None
+    line = {
+        "metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
+        "warmup": max(3, args.warmup), "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded numpy Philox type6; Omega from Philox(seed))",
+        "config": cfg_dict(args),
+        "pct_fp64_peak": 100.0 * value / (world * FP64_PEAK_GFLOPS),
+        "fp64_peak": {"value": FP64_PEAK_GFLOPS, "unit": "GFLOP/s", "source": FP64_PEAK_SRC},
+        "roofline": {"bound": "tensor", "kernel": "dmma_gemm_kernel<128,128> (trailing Schur update)",
+                     "achieved": achieved, "peak": FP64_PEAK_GFLOPS / 1e3, "unit": "TFLOP/s",
+                     "frac": (achieved / (FP64_PEAK_GFLOPS / 1e3)) if achieved else None,
+                     "traffic": None,
+                     "algorithmic": "sum over panels of t*m*(m+1) flops (lower-triangle rank-t update)",
+                     "share_of_step": schur_ms / (ms * args.steps) if ms > 0 else None,
+                     "panel_share_of_step": panel_ms / (ms * args.steps) if ms > 0 else None},
+        "cpu_baseline": cpu,
+        "e2e": {"value": e2e_val, "unit": "GFLOP/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "path": "paper_1710_00125_b200.factor(numpy array in pinned memory) -> Factorization"},
+        "gpu_launches": int(stats["n_launches"]) * args.steps,
+        "clocks": clocks,
+        "factor_stats": {k: stats[k] for k in ("n_panels", "n_steps", "n_2x2", "recompute_count", "rho_cheap",
+                                               "max_multiplier", "t_panel_ms", "t_schur_ms")},
+        "solve_backward_error": bwd,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        run_b200(args, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -89,6 +89,8 @@ typedef struct rcp_stats {
   double t_factor_ms;        /* device time of the factorization (CUDA events)    */
   double t_schur_ms;         /* device time inside the trailing Schur updates     */
   double t_panel_ms;         /* device time inside the panel kernels              */
+  double schur_flops;        /* algorithmic flops of the trailing updates: sum t*m*(m+1) */
+  int64_t n_launches;        /* kernels launched by this call                     */
   char message[160];
 } rcp_stats;
 

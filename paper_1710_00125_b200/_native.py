@@ -66,6 +66,8 @@ class RcpStats(ctypes.Structure):
         ("t_factor_ms", ctypes.c_double),
         ("t_schur_ms", ctypes.c_double),
         ("t_panel_ms", ctypes.c_double),
+        ("schur_flops", ctypes.c_double),
+        ("n_launches", ctypes.c_int64),
         ("message", ctypes.c_char * 160),
     ]
 

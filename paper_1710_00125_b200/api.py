@@ -247,7 +247,13 @@ class DeviceFactorization:
         s = self.stats
         stats = GrowthStats(rho_cheap=s["rho_cheap"], max_multiplier=s["max_multiplier"],
                             counters=OpCounters(), recompute_count=s["recompute_count"])
-        return Factorization(perm=self.perm.cpu().numpy().astype(np.int64), L=self.L.cpu().numpy(),
+        if self.n >= 2048:  # D2H into (cached) pinned memory: full PCIe bandwidth for the dense L
+            lh = torch.empty(tuple(self.L.shape), dtype=torch.float64, pin_memory=True)
+            lh.copy_(self.L)
+            L = lh.numpy()
+        else:
+            L = self.L.cpu().numpy()
+        return Factorization(perm=self.perm.cpu().numpy().astype(np.int64), L=L,
                              D=BlockDiag(blocks), pattern=pattern, stats=stats)
 
 
@@ -360,6 +366,7 @@ def factor_device(a: torch.Tensor, cfg: FactorConfig | None = None, *, omega: to
         "n_panels": int(st.n_panels), "n_steps": int(st.n_steps), "n_2x2": int(st.n_2x2),
         "deficient_from": int(st.deficient_from), "t_factor_ms": float(st.t_factor_ms),
         "t_schur_ms": float(st.t_schur_ms), "t_panel_ms": float(st.t_panel_ms),
+        "schur_flops": float(st.schur_flops), "n_launches": int(st.n_launches),
     }
     return out
 

@@ -103,6 +103,12 @@ struct Scal {  // scalar results block (device)
     }                                                                                             \
   } while (0)
 
+#define RCP_LAUNCH(expr) \
+  do {                   \
+    RCP_CHECK(expr);     \
+    ++launches;          \
+  } while (0)
+
 struct PanelRecord {
   int k0, k_end;
   int64_t snap_off;
@@ -211,6 +217,8 @@ int rcp_factor(const rcp_config* cfg, int64_t n, const double* a, int64_t lda, c
     return v.back();
   };
 
+  int64_t launches = 0;
+  double schur_flops = 0.0;
   RCP_CHECK(cudaEventRecord(ev_start, st));
 
   // ---- init state
@@ -225,7 +233,7 @@ int rcp_factor(const rcp_config* cfg, int64_t n, const double* a, int64_t lda, c
   if (trace_r) RCP_CHECK(cudaMemsetAsync(trace_r, 0xff, sizeof(int32_t) * n, st));
 
   // ---- input validation + copy (factor.py:277-286)
-  RCP_CHECK(launch_validate_copy(a, lda, n, A[0], dscal->vflags, &dscal->amax, st));
+  RCP_LAUNCH(launch_validate_copy(a, lda, n, A[0], dscal->vflags, &dscal->amax, st));
   RCP_CHECK(cudaMemcpyAsync(hscal, dscal, sizeof(Scal), cudaMemcpyDeviceToHost, st));
   RCP_CHECK(cudaStreamSynchronize(st));
   if (hscal->vflags[0]) return RCP_ERR_NOT_SYMMETRIC;
@@ -233,18 +241,18 @@ int rcp_factor(const rcp_config* cfg, int64_t n, const double* a, int64_t lda, c
   const double amax = hscal->amax;
 
   // ---- sketch B = Omega A (factor.py:307-309) and guard setup (factor.py:314-317)
-  RCP_CHECK(launch_sketch_gemm(P, n, omega_dev, n, A[0], n, B[0], 0, st));
+  RCP_LAUNCH(launch_sketch_gemm(P, n, omega_dev, n, A[0], n, B[0], 0, st));
   const bool armed = c.robust_r >= 1;
   double delta = armed ? 1.0 / c.robust_r : 0.0;
   double thr = armed ? std::pow(DBL_EPSILON, delta) : 0.0;
   double beta = 0.0;
   if (armed) {
-    RCP_CHECK(launch_sketch_norm_max(B[0], P, n, &dscal->beta, st));
+    RCP_LAUNCH(launch_sketch_norm_max(B[0], P, n, &dscal->beta, st));
     RCP_CHECK(cudaMemcpyAsync(hscal, dscal, sizeof(Scal), cudaMemcpyDeviceToHost, st));
     RCP_CHECK(cudaStreamSynchronize(st));
     beta = hscal->beta;
   }
-  RCP_CHECK(launch_iota(n, permb[0], st));
+  RCP_LAUNCH(launch_iota(n, permb[0], st));
 
   int cur = 0;       // A / B buffer holding the current trailing block
   int pcur = 0;      // perm buffer for the current order
@@ -256,7 +264,7 @@ int rcp_factor(const rcp_config* cfg, int64_t n, const double* a, int64_t lda, c
   std::vector<double> draw_buf;
 
   if (armed && beta == 0.0) {  // factor.py:510-511
-    RCP_CHECK(launch_deficient_fill(n, 0, permb[0], perm, d_diag, d_off, pattern, st));
+    RCP_LAUNCH(launch_deficient_fill(n, 0, permb[0], perm, d_diag, d_off, pattern, st));
     deficient_from = 0;
     k = n;
   }
@@ -328,7 +336,7 @@ int rcp_factor(const rcp_config* cfg, int64_t n, const double* a, int64_t lda, c
       RCP_CHECK(cudaMemsetAsync(&dstate->status, 0, sizeof(int), st));
       EventPair& ep = new_pair(ev_panel);
       RCP_CHECK(cudaEventRecord(ep.a, st));
-      RCP_CHECK(launch_panel(prm, G, smem, st));
+      RCP_LAUNCH(launch_panel(prm, G, smem, st));
       RCP_CHECK(cudaEventRecord(ep.b, st));
       RCP_CHECK(cudaMemcpyAsync(hstate, dstate, sizeof(PanelState), cudaMemcpyDeviceToHost, st));
       RCP_CHECK(cudaStreamSynchronize(st));
@@ -349,8 +357,8 @@ int rcp_factor(const rcp_config* cfg, int64_t n, const double* a, int64_t lda, c
       draw_buf.resize((size_t)P * m0);
       if (draw(draw_ctx, P, m0, draw_buf.data()) != 0) return RCP_ERR_NEED_NORMALS;
       RCP_CHECK(cudaMemcpyAsync(omg, draw_buf.data(), sizeof(double) * (size_t)P * m0, cudaMemcpyHostToDevice, st));
-      RCP_CHECK(launch_mirror_lower(n, k0, A[cur], st));
-      RCP_CHECK(launch_sketch_gemm(P, m0, omg, m0, A[cur] + k0 + (int64_t)k0 * n, n, B[cur], k0, st));
+      RCP_LAUNCH(launch_mirror_lower(n, k0, A[cur], st));
+      RCP_LAUNCH(launch_sketch_gemm(P, m0, omg, m0, A[cur] + k0 + (int64_t)k0 * n, n, B[cur], k0, st));
       recomputes += 1;
       delta += 1.0 / c.robust_r;
       thr = std::pow(DBL_EPSILON, delta);
@@ -359,7 +367,7 @@ int rcp_factor(const rcp_config* cfg, int64_t n, const double* a, int64_t lda, c
       (void)attempt;
     }
     if (stopped) {
-      RCP_CHECK(launch_deficient_fill(n, k0, permb[pcur], perm, d_diag, d_off, pattern, st));
+      RCP_LAUNCH(launch_deficient_fill(n, k0, permb[pcur], perm, d_diag, d_off, pattern, st));
       deficient_from = k0;
       break;
     }
@@ -379,18 +387,19 @@ int rcp_factor(const rcp_config* cfg, int64_t n, const double* a, int64_t lda, c
       if (stats) snprintf(stats->message, sizeof(stats->message), "snapshot capacity exceeded");
       return RCP_ERR_WORKSPACE;
     }
-    RCP_CHECK(launch_gather(n, k0, k_end, t, tpad, ((mp + 127) / 128) * 128, pol, Lbuf, W, permb[pcur],
+    RCP_LAUNCH(launch_gather(n, k0, k_end, t, tpad, ((mp + 127) / 128) * 128, pol, Lbuf, W, permb[pcur],
                             permb[pcur ^ 1], snap + snap_off, phys, Lneg, Wg, st));
     panels.push_back(PanelRecord{k0, k_end, snap_off});
     snap_off += m0;
     if (mp > 0 && t > 0) {
       EventPair& es = new_pair(ev_schur);
       RCP_CHECK(cudaEventRecord(es.a, st));
-      RCP_CHECK(launch_schur_update(n, k_end, mp, Lneg, Wg, tpad, t, A[cur], phys, A[cur ^ 1], st));
+      RCP_LAUNCH(launch_schur_update(n, k_end, mp, Lneg, Wg, tpad, t, A[cur], phys, A[cur ^ 1], st));
       RCP_CHECK(cudaEventRecord(es.b, st));
+      schur_flops += (double)t * (double)mp * (double)(mp + 1);
       // sketch correction (factor.py:554-565)
-      RCP_CHECK(launch_ysolve(n, P, k0, t, tpad, pol, B[cur], Lbuf, Y, st));
-      RCP_CHECK(launch_sketch_correction(P, mp, k_end, Y, tpad, t, Lneg, B[cur], phys, B[cur ^ 1], st));
+      RCP_LAUNCH(launch_ysolve(n, P, k0, t, tpad, pol, B[cur], Lbuf, Y, st));
+      RCP_LAUNCH(launch_sketch_correction(P, mp, k_end, Y, tpad, t, Lneg, B[cur], phys, B[cur ^ 1], st));
       cur ^= 1;
     }
     pcur ^= 1;
@@ -399,12 +408,13 @@ int rcp_factor(const rcp_config* cfg, int64_t n, const double* a, int64_t lda, c
 
   // ---- assemble L in final order + statistics (factor.py:514-538)
   RCP_CHECK(cudaMemsetAsync(Lout, 0, sizeof(double) * (size_t)n * n, st));
-  RCP_CHECK(launch_unit_diag(n, Lout, st));
+  RCP_LAUNCH(launch_unit_diag(n, Lout, st));
   for (const PanelRecord& pr : panels) {
-    RCP_CHECK(launch_assemble_panel(n, pr.k0, pr.k_end, snap + pr.snap_off, poso, perm, Lbuf, Lout,
+    RCP_LAUNCH(launch_assemble_panel(n, pr.k0, pr.k_end, snap + pr.snap_off, poso, perm, Lbuf, Lout,
                                     &dscal->maxmult, st));
+    ++launches;  // assemble = invert + gather kernels
   }
-  RCP_CHECK(launch_dmax(n, d_diag, d_off, &dscal->dmax, st));
+  RCP_LAUNCH(launch_dmax(n, d_diag, d_off, &dscal->dmax, st));
   RCP_CHECK(cudaEventRecord(ev_stop, st));
   RCP_CHECK(cudaMemcpyAsync(hscal, dscal, sizeof(Scal), cudaMemcpyDeviceToHost, st));
   RCP_CHECK(cudaMemcpyAsync(hstate, dstate, sizeof(PanelState), cudaMemcpyDeviceToHost, st));
@@ -440,6 +450,8 @@ int rcp_factor(const rcp_config* cfg, int64_t n, const double* a, int64_t lda, c
     }
     stats->t_panel_ms = tp;
     stats->t_schur_ms = ts;
+    stats->schur_flops = schur_flops;
+    stats->n_launches = launches;
   }
   return RCP_OK;
 }

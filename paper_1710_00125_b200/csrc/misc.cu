@@ -13,7 +13,8 @@ namespace {
 
 __device__ double block_max(double v) {
   __shared__ double sm[32];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+  const int tid = threadIdx.x + threadIdx.y * blockDim.x;
+  const int lane = tid & 31, warp = tid >> 5, nw = (blockDim.x * blockDim.y + 31) >> 5;
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, off));
   if (lane == 0) sm[warp] = v;
@@ -23,7 +24,7 @@ __device__ double block_max(double v) {
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, off));
   }
-  return v;  // valid in thread 0
+  return v;  // valid in thread (0, 0)
 }
 
 // Exact-symmetry / finiteness check (core.py:48-53, factor.py:278-281), max|A|
