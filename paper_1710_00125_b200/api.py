@@ -367,6 +367,10 @@ def factor_device(a: torch.Tensor, cfg: FactorConfig | None = None, *, omega: to
         "deficient_from": int(st.deficient_from), "t_factor_ms": float(st.t_factor_ms),
         "t_schur_ms": float(st.t_schur_ms), "t_panel_ms": float(st.t_panel_ms),
         "schur_flops": float(st.schur_flops), "n_launches": int(st.n_launches),
+        "panel_prof_ms": dict(zip(("qrcp", "qrcp_exchange", "sbkp_gemv", "sbkp_exchange", "sbkp_eliminate",
+                                   "next_pivot", "qrcp_reflect", "total", "sbkp_local_argmax",
+                                   "qrcp_local_argmax", "qrcp_householder"),
+                                  [round(float(x), 3) for x in st.panel_prof_ms])),
     }
     return out
 

@@ -31,7 +31,7 @@ size_t align_up(size_t x) { return (x + kAlign - 1) & ~(kAlign - 1); }
 
 struct Layout {
   size_t A0, A1, Lbuf, W, Lneg, Wg, B0, B1, qscr, Y, omega, phys, lop, pol, perm0, perm1, poso, snap, flags, xrec, qrec,
-      qcol, state, scal, total;
+      qcol, sdec, qdec, state, scal, total;
   int64_t rows_pad, snap_cap;
   int tpad;
 };
@@ -69,10 +69,12 @@ Layout make_layout(int64_t n, const rcp_config& c) {
   L.perm1 = take((size_t)n * 4);
   L.poso = take((size_t)n * 4);
   L.snap = take((size_t)L.snap_cap * 4);
-  L.flags = take(sizeof(long long) * kMaxSMs);
-  L.xrec = take(sizeof(XRec) * 2 * kMaxSMs);
-  L.qrec = take(sizeof(QRec) * 2 * kMaxSMs);
-  L.qcol = take(sizeof(double) * 2 * kMaxSMs * (size_t)P);
+  L.flags = take(0);
+  L.xrec = take(8 * 2 * kMaxSMs * (size_t)kXWords);
+  L.qrec = take(8 * 2 * kMaxSMs * (size_t)kQWords);
+  L.qcol = take(8 * 2 * kMaxSMs * 2 * (size_t)P);
+  L.sdec = take(8 * 2 * (size_t)kXWords);
+  L.qdec = take(8 * 2 * (8 + 2 * (size_t)P));
   L.state = take(sizeof(PanelState));
   L.scal = take(64);
   L.total = off;
@@ -226,7 +228,7 @@ int rcp_factor(const rcp_config* cfg, int64_t n, const double* a, int64_t lda, c
   init.seq = 0;
   init.err = LLONG_MAX;
   RCP_CHECK(cudaMemcpyAsync(dstate, &init, sizeof(init), cudaMemcpyHostToDevice, st));
-  RCP_CHECK(cudaMemsetAsync(ws + Lay.flags, 0, sizeof(long long) * kMaxSMs, st));
+  RCP_CHECK(cudaMemsetAsync(ws + Lay.xrec, 0, Lay.state - Lay.xrec, st));  // LL exchange buffers: no stale tags
   RCP_CHECK(cudaMemsetAsync(dscal, 0, sizeof(Scal), st));
   RCP_CHECK(cudaMemsetAsync(d_off, 0, sizeof(double) * n, st));
   if (trace_kind) RCP_CHECK(cudaMemsetAsync(trace_kind, -1, n, st));
@@ -279,22 +281,28 @@ int rcp_factor(const rcp_config* cfg, int64_t n, const double* a, int64_t lda, c
     G = (m0 + R - 1) / R;
     const int Wn = width + 2;
     const int qn = (c.q > 1 && m0 > 1) ? std::min(std::min(c.q, width), std::min(m0, P)) : 0;
-    size_t fixed = 0;
-    fixed += ((size_t)4 * Wn + 15) & ~size_t(15);
-    fixed += ((size_t)4 * R + 15) & ~size_t(15);
-    fixed += ((size_t)8 * P + 15) & ~size_t(15);
-    fixed += 2 * (((size_t)8 * Wn + 15) & ~size_t(15));
-    long long avail = (long long)smem_budget - (long long)fixed;
-    int Rs = 0;
+    auto a16 = [](size_t x) { return (x + 15) & ~size_t(15); };
+    const size_t fixed = a16(4 * (size_t)Wn) + a16(4 * (size_t)R) + a16(8 * (size_t)P) + 4 * a16(8 * (size_t)Wn);
+    const long long avail = (long long)smem_budget - (long long)fixed;
+    // QRCP: register mode (one sketch column per thread, rows >= 32 in smem) when it fits
+    int qmode = 0, Rs = 0;
+    size_t need_q = 0;
     if (qn > 0) {
-      long long per_col = 8LL * P;
-      long long rs = (avail - 12LL * R - 64) / per_col;
-      Rs = (int)std::max(0LL, std::min<long long>(R, rs));
+      const int ps_reg = P - std::min(P, 32);
+      const long long need_reg = 8LL * ps_reg * R + 64;
+      if (R <= 256 && need_reg <= avail) {
+        qmode = 1;
+        Rs = R;
+        need_q = (size_t)need_reg;
+      } else {
+        long long rs = (avail - 12LL * R - 64) / (8LL * P);
+        Rs = (int)std::max(0LL, std::min<long long>(R, rs));
+        need_q = (size_t)8 * P * Rs + 12 * (size_t)R + 64;
+      }
     }
-    long long ls = (avail - 32LL * R - 64) / (8LL * R);
+    long long ls = (avail - 24LL * R - 64) / (8LL * R);
     int Ls = (int)std::max(0LL, std::min<long long>(Wn, ls));
-    size_t need_q = qn > 0 ? (size_t)8 * P * Rs + 8 * (size_t)R + 4 * (size_t)R + 64 : 0;
-    size_t need_s = (size_t)8 * Ls * R + 32 * (size_t)R + 64;
+    size_t need_s = (size_t)8 * Ls * R + 24 * (size_t)R + 64;
     size_t smem = fixed + std::max(need_q, need_s);
 
     PanelParams prm{};
@@ -311,6 +319,7 @@ int rcp_factor(const rcp_config* cfg, int64_t n, const double* a, int64_t lda, c
     prm.Rs = Rs;
     prm.Ls = Ls;
     prm.Wn = Wn;
+    prm.qmode = qmode;
     prm.A = A[cur];
     prm.B = B[cur];
     prm.qscr = dptr(Lay.qscr);
@@ -325,10 +334,11 @@ int rcp_factor(const rcp_config* cfg, int64_t n, const double* a, int64_t lda, c
     prm.pattern = pattern;
     prm.trace_kind = trace_kind;
     prm.trace_r = trace_r;
-    prm.flags = reinterpret_cast<long long*>(ws + Lay.flags);
-    prm.xrec = reinterpret_cast<XRec*>(ws + Lay.xrec);
-    prm.qrec = reinterpret_cast<QRec*>(ws + Lay.qrec);
-    prm.qcol = dptr(Lay.qcol);
+    prm.xll = reinterpret_cast<unsigned long long*>(ws + Lay.xrec);
+    prm.qll = reinterpret_cast<unsigned long long*>(ws + Lay.qrec);
+    prm.qcll = reinterpret_cast<unsigned long long*>(ws + Lay.qcol);
+    prm.sdll = reinterpret_cast<unsigned long long*>(ws + Lay.sdec);
+    prm.qdll = reinterpret_cast<unsigned long long*>(ws + Lay.qdec);
     prm.st = dstate;
 
     bool stopped = false;
@@ -357,7 +367,6 @@ int rcp_factor(const rcp_config* cfg, int64_t n, const double* a, int64_t lda, c
       draw_buf.resize((size_t)P * m0);
       if (draw(draw_ctx, P, m0, draw_buf.data()) != 0) return RCP_ERR_NEED_NORMALS;
       RCP_CHECK(cudaMemcpyAsync(omg, draw_buf.data(), sizeof(double) * (size_t)P * m0, cudaMemcpyHostToDevice, st));
-      RCP_LAUNCH(launch_mirror_lower(n, k0, A[cur], st));
       RCP_LAUNCH(launch_sketch_gemm(P, m0, omg, m0, A[cur] + k0 + (int64_t)k0 * n, n, B[cur], k0, st));
       recomputes += 1;
       delta += 1.0 / c.robust_r;
@@ -451,6 +460,9 @@ int rcp_factor(const rcp_config* cfg, int64_t n, const double* a, int64_t lda, c
     stats->t_panel_ms = tp;
     stats->t_schur_ms = ts;
     stats->schur_flops = schur_flops;
+    int clk_khz = 0;
+    cudaDeviceGetAttribute(&clk_khz, cudaDevAttrClockRate, dev);
+    for (int i = 0; i < 16; ++i) stats->panel_prof_ms[i] = clk_khz > 0 ? (double)hstate->cyc[i] / clk_khz : 0.0;
     stats->n_launches = launches;
   }
   return RCP_OK;

@@ -3,13 +3,15 @@
 //   - sketch                  B   <- Omega * A
 //   - sketch correction       B2  <- B2 - Y * L21^T      (permuted gather-in)
 //
-// acc[m][n] = init(m, n) + sum_k Aop[m][k] * Bop[n][k]
-// Both operands are K-contiguous row arrays (row r at base + r * ld).  Tiles are staged
-// into shared memory with a cp.async ring (STAGES deep) and consumed by
-// mma.sync.m8n8k4.f64 (SASS DMMA.8x8x4, the FP64 tensor pipe of sm_100a).  Epilogue
-// functors provide the accumulator initialisation (gather of the previous matrix) and
-// the store, so the permutation and the symmetric "lower only" rule are fused into
-// the GEMM instead of separate passes.
+// out[m][n] = cin[m][n] + sum_k Aop[m][k] * Bop[n][k]
+// Both operands are K-contiguous row arrays (row r at base + r * ld), staged into
+// shared memory by a cp.async ring (STAGES deep) and consumed by
+// mma.sync.m8n8k4.f64 (SASS DMMA.8x8x4, the FP64 tensor pipe of sm_100a).
+// The accumulators start at zero; the C-in tile (a gather through the panel
+// permutation, supplied by the epilogue functor) is fetched with cp.async into a
+// shared-memory tile together with the LAST operand stage, so its latency hides
+// behind the remaining MMAs.  The epilogue adds the accumulators into that tile and
+// writes it back column-wise (coalesced).
 #pragma once
 #include "rcp_common.cuh"
 
@@ -17,8 +19,8 @@ namespace rcp {
 
 constexpr int kGemmThreads = 256;  // 8 warps: 2 (M) x 4 (N)
 constexpr int kBK = 16;
-constexpr int kPad = 4;            // smem row stride BK+4 doubles -> conflict-free fragment loads
-constexpr int kStages = 3;
+constexpr int kPad = 4;            // operand smem row stride BK+4 doubles -> conflict-free fragment loads
+constexpr int kCPad = 1;           // C tile column stride BM+1 doubles (conflict-free row and column reads)
 
 struct OperandDesc {
   const double* ptr;
@@ -27,17 +29,20 @@ struct OperandDesc {
   int64_t k;     // valid K (others read as 0)
 };
 
-template <int BM, int BN>
+template <int BM, int BN, int STAGES>
 struct GemmSmem {
-  double a[kStages][BM][kBK + kPad];
-  double b[kStages][BN][kBK + kPad];
+  double a[STAGES][BM][kBK + kPad];
+  double b[STAGES][BN][kBK + kPad];
+  double c[BN][BM + kCPad];
+  int rowmap[BM];  // epilogue index maps (e.g. physical rows of the permuted C-in)
+  int colmap[BN];
 };
 
 template <int ROWS, int VEC>
 RCP_D void load_tile(double (*dst)[kBK + kPad], const OperandDesc& op, int64_t row0, int64_t k0) {
-  // ROWS x kBK tile; VEC doubles per cp.async (1 -> 8 B, 2 -> 16 B).
   constexpr int kChunksPerRow = kBK / VEC;
   constexpr int kChunks = ROWS * kChunksPerRow;
+#pragma unroll
   for (int c = threadIdx.x; c < kChunks; c += kGemmThreads) {
     int r = c / kChunksPerRow;
     int kk = (c % kChunksPerRow) * VEC;
@@ -52,15 +57,28 @@ RCP_D void load_tile(double (*dst)[kBK + kPad], const OperandDesc& op, int64_t r
   }
 }
 
+// C-in gather: element (m0+i, n0+j) -> smem c[j][i]; threads run along i (coalesced).
+template <int BM, int BN, class Epi>
+RCP_D void load_cin(double (*c)[BM + kCPad], const int* rowmap, const int* colmap, const Epi& epi, int64_t m0,
+                    int64_t n0) {
+  for (int e = threadIdx.x; e < BM * BN; e += kGemmThreads) {
+    const int j = e / BM, i = e - j * BM;
+    const double* src = epi.cin(m0 + i, n0 + j, rowmap[i], colmap[j]);
+    cp_async8(&c[j][i], src ? src : epi.dummy(), src != nullptr);
+  }
+}
+
 // Generic tile-GEMM body.  TileMap: bool map(int bid, int64_t& m0, int64_t& n0).
-// Epi: double init(m, n, valid) / void store(m, n, v) / bool need_init.
-template <int BM, int BN, int VEC, class TileMap, class Epi>
+// Epi: int map_row(m), int map_col(n) (staged once per tile), const double* cin(m, n, row, col)
+//      (nullptr -> 0), double* cout(m, n) (nullptr -> skip), const double* dummy(),
+//      static constexpr bool kHasInput.
+template <int BM, int BN, int STAGES, int VEC, class TileMap, class Epi>
 __global__ void __launch_bounds__(kGemmThreads, 1)
 dmma_gemm_kernel(OperandDesc A, OperandDesc B, int64_t K, TileMap map, Epi epi) {
   constexpr int WM = BM / 2, WN = BN / 4;
   constexpr int MF = WM / 8, NF = WN / 8;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  auto& sm = *reinterpret_cast<GemmSmem<BM, BN>*>(smem_raw);
+  auto& sm = *reinterpret_cast<GemmSmem<BM, BN, STAGES>*>(smem_raw);
 
   int64_t m0, n0;
   if (!map(blockIdx.x, m0, n0)) return;
@@ -74,40 +92,41 @@ dmma_gemm_kernel(OperandDesc A, OperandDesc B, int64_t K, TileMap map, Epi epi) 
   for (int i = 0; i < MF; ++i)
 #pragma unroll
     for (int j = 0; j < NF; ++j) {
-      if (Epi::kNeedInit) {
-        int64_t m = m0 + wm0 + 8 * i + g;
-        int64_t n = n0 + wn0 + 8 * j + 2 * q;
-        acc[i][j][0] = epi.init(m, n);
-        acc[i][j][1] = epi.init(m, n + 1);
-      } else {
-        acc[i][j][0] = 0.0;
-        acc[i][j][1] = 0.0;
-      }
+      acc[i][j][0] = 0.0;
+      acc[i][j][1] = 0.0;
     }
 
+  if (Epi::kHasInput) {
+    for (int i = threadIdx.x; i < BM; i += kGemmThreads) sm.rowmap[i] = epi.map_row(m0 + i);
+    for (int j = threadIdx.x; j < BN; j += kGemmThreads) sm.colmap[j] = epi.map_col(n0 + j);
+    __syncthreads();
+  }
   const int KT = static_cast<int>((K + kBK - 1) / kBK);
+  // prologue: STAGES-1 operand stages; the C-in gather joins the group of the last stage
 #pragma unroll
-  for (int s = 0; s < kStages - 1; ++s) {
+  for (int s = 0; s < STAGES - 1; ++s) {
     if (s < KT) {
       load_tile<BM, VEC>(sm.a[s], A, m0, (int64_t)s * kBK);
       load_tile<BN, VEC>(sm.b[s], B, n0, (int64_t)s * kBK);
     }
+    if (Epi::kHasInput && s == STAGES - 2 && KT <= STAGES - 1) load_cin<BM, BN>(sm.c, sm.rowmap, sm.colmap, epi, m0, n0);
     cp_async_commit();
   }
 
   for (int kt = 0; kt < KT; ++kt) {
-    cp_async_wait<kStages - 2>();
+    cp_async_wait<STAGES - 2>();
     __syncthreads();
     {
-      int nk = kt + kStages - 1;
+      int nk = kt + STAGES - 1;
       if (nk < KT) {
-        int st = nk % kStages;
+        int st = nk % STAGES;
         load_tile<BM, VEC>(sm.a[st], A, m0, (int64_t)nk * kBK);
         load_tile<BN, VEC>(sm.b[st], B, n0, (int64_t)nk * kBK);
+        if (Epi::kHasInput && nk == KT - 1) load_cin<BM, BN>(sm.c, sm.rowmap, sm.colmap, epi, m0, n0);
       }
       cp_async_commit();
     }
-    const int st = kt % kStages;
+    const int st = kt % STAGES;
 #pragma unroll
     for (int kk = 0; kk < kBK; kk += 4) {
       double af[MF], bf[NF];
@@ -121,17 +140,43 @@ dmma_gemm_kernel(OperandDesc A, OperandDesc B, int64_t K, TileMap map, Epi epi) 
         for (int j = 0; j < NF; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
     }
   }
+  if (Epi::kHasInput && KT == 0) load_cin<BM, BN>(sm.c, sm.rowmap, sm.colmap, epi, m0, n0), cp_async_commit();
   cp_async_wait<0>();
+  __syncthreads();
 
+  // accumulate into the C tile (c[n][m]), then coalesced column-wise store
 #pragma unroll
   for (int i = 0; i < MF; ++i)
 #pragma unroll
     for (int j = 0; j < NF; ++j) {
-      int64_t m = m0 + wm0 + 8 * i + g;
-      int64_t n = n0 + wn0 + 8 * j + 2 * q;
-      epi.store(m, n, acc[i][j][0]);
-      epi.store(m, n + 1, acc[i][j][1]);
+      const int mi = wm0 + 8 * i + g;
+      const int nj = wn0 + 8 * j + 2 * q;
+      if (Epi::kHasInput) {
+        sm.c[nj][mi] = __dadd_rn(sm.c[nj][mi], acc[i][j][0]);
+        sm.c[nj + 1][mi] = __dadd_rn(sm.c[nj + 1][mi], acc[i][j][1]);
+      } else {
+        sm.c[nj][mi] = acc[i][j][0];
+        sm.c[nj + 1][mi] = acc[i][j][1];
+      }
     }
+  __syncthreads();
+  for (int e = threadIdx.x; e < BM * BN; e += kGemmThreads) {
+    const int j = e / BM, i = e - j * BM;
+    double* dst = epi.cout(m0 + i, n0 + j);
+    if (dst) *dst = sm.c[j][i];
+  }
+  if (Epi::kMirror) {  // also store the transpose of the strictly-lower part (symmetric full storage)
+    for (int e = threadIdx.x; e < BM * BN; e += kGemmThreads) {
+      const int i = e / BN, j = e - i * BN;
+      double* dst = epi.cout_mirror(m0 + i, n0 + j);
+      if (dst) *dst = sm.c[j][i];
+    }
+  }
+}
+
+template <int BM, int BN, int STAGES>
+constexpr size_t gemm_smem_bytes() {
+  return sizeof(GemmSmem<BM, BN, STAGES>);
 }
 
 // ------------------------------------------------------------------ tile maps
@@ -150,7 +195,6 @@ struct RectMap {
 struct LowerMap {
   int bt;  // tile size (BM == BN)
   RCP_D bool operator()(int bid, int64_t& m0, int64_t& n0) const {
-    // I = floor((sqrt(8 bid + 1) - 1) / 2), fixed up for rounding.
     long long x = bid;
     long long I = static_cast<long long>((sqrt(8.0 * (double)x + 1.0) - 1.0) * 0.5);
     while (I * (I + 1) / 2 > x) --I;

@@ -12,11 +12,12 @@
 // rows).  The permutation is applied later by the gather-fused trailing update.
 //
 // Every pivot search / QRCP step is ONE all-to-all exchange: each CTA publishes its
-// local best candidate (plus the data the decision needs) and a release flag; every
-// CTA then reads all G records and reduces them identically, so all CTAs take the
-// same decision without a second barrier.  Values a CTA needs from rows it does not
-// own (the next pivot's W row entries of the columns produced in this step) are
-// recomputed redundantly with the same bitwise-deterministic dot routine.
+// local best candidate (plus the data the decision needs) behind a release flag;
+// every CTA polls all G flags, loads all G records and reduces them identically, so
+// all CTAs take the same decision without a second barrier.  Values a CTA needs from
+// rows it does not own (the next pivot's W-row entries of the columns produced in
+// this step) are recomputed redundantly with the same bitwise-deterministic dot
+// routine the owner used.
 #include <cfloat>
 #include <climits>
 #include "panel.cuh"
@@ -28,6 +29,8 @@ namespace {
 
 constexpr int kPanelThreads = 256;
 constexpr int kWarps = kPanelThreads / 32;
+constexpr int kRegRows = 32;  // QRCP register mode: sketch rows [0, 32) of each column live in registers
+constexpr long long kWatchdogCycles = 8000000000LL;
 
 struct BlockBest {
   double key;
@@ -35,24 +38,27 @@ struct BlockBest {
   int slot;
 };
 
-// Block-wide argmax with numpy first-index semantics; result broadcast to all threads.
-__device__ BlockBest block_argmax(double key, long long idx, int slot) {
+RCP_D void argmax_step(double& key, long long& idx, int& slot, int off) {
+  double k2 = __shfl_down_sync(0xffffffffu, key, off);
+  long long i2 = __shfl_down_sync(0xffffffffu, idx, off);
+  int s2 = __shfl_down_sync(0xffffffffu, slot, off);
+  if (better(k2, i2, key, idx)) {
+    key = k2;
+    idx = i2;
+    slot = s2;
+  }
+}
+
+// Block-wide argmax (numpy first-index semantics), broadcast to all threads; two
+// barriers.  `parity` alternates between consecutive calls (double-buffered result).
+__device__ BlockBest block_argmax(double key, long long idx, int slot, int parity) {
   __shared__ double sk[kWarps];
   __shared__ long long si[kWarps];
   __shared__ int ss[kWarps];
-  __shared__ BlockBest res;
+  __shared__ BlockBest res[2];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
-  for (int off = 16; off > 0; off >>= 1) {
-    double k2 = __shfl_down_sync(0xffffffffu, key, off);
-    long long i2 = __shfl_down_sync(0xffffffffu, idx, off);
-    int s2 = __shfl_down_sync(0xffffffffu, slot, off);
-    if (better(k2, i2, key, idx)) {
-      key = k2;
-      idx = i2;
-      slot = s2;
-    }
-  }
+  for (int off = 16; off > 0; off >>= 1) argmax_step(key, idx, slot, off);
   if (lane == 0) {
     sk[warp] = key;
     si[warp] = idx;
@@ -64,26 +70,15 @@ __device__ BlockBest block_argmax(double key, long long idx, int slot) {
     idx = lane < kWarps ? si[lane] : LLONG_MAX;
     slot = lane < kWarps ? ss[lane] : -1;
 #pragma unroll
-    for (int off = 16; off > 0; off >>= 1) {
-      double k2 = __shfl_down_sync(0xffffffffu, key, off);
-      long long i2 = __shfl_down_sync(0xffffffffu, idx, off);
-      int s2 = __shfl_down_sync(0xffffffffu, slot, off);
-      if (better(k2, i2, key, idx)) {
-        key = k2;
-        idx = i2;
-        slot = s2;
-      }
-    }
-    if (lane == 0) res = BlockBest{key, idx, slot};
+    for (int off = 16; off > 0; off >>= 1) argmax_step(key, idx, slot, off);
+    if (lane == 0) res[parity] = BlockBest{key, idx, slot};
   }
   __syncthreads();
-  BlockBest out = res;
-  __syncthreads();
-  return out;
+  return res[parity];
 }
 
-// Deterministic sum over vals[lo, hi) by warp 0 (lane-strided partials + fixed tree);
-// every CTA obtains the same bits for the same input.  Returns the value in lane 0.
+// Deterministic sum of squares over vals[lo, hi) by warp 0 (lane-strided partials + fixed
+// tree): every CTA obtains the same bits.  Result valid in lane 0.
 __device__ double warp0_sum_sq(const double* vals, int lo, int hi) {
   const int lane = threadIdx.x & 31;
   double acc = 0.0;
@@ -93,37 +88,45 @@ __device__ double warp0_sum_sq(const double* vals, int lo, int hi) {
   return acc;
 }
 
-RCP_D void xpublish(long long* flags, int cta, long long seq) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    st_release(flags + cta, seq);
-  }
+// ---- LL exchange words: 32 data bits + 32-bit tag per 64-bit store (single-copy atomic),
+// so a reader validates arrival and data with the same load and no fences are needed.
+typedef unsigned long long u64;
+RCP_D void ll_put(u64* p, unsigned tag, unsigned data) {
+  const u64 v = (static_cast<u64>(tag) << 32) | data;
+  asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
-
-// Waits for all G flags to reach seq.  A watchdog (~4 s of SM clock) turns a lost
-// peer into an error instead of a hung GPU; returns false on timeout.
-__device__ bool xwait(const long long* flags, int G, long long seq, PanelState* st) {
-  __shared__ int s_timeout;
-  if (threadIdx.x == 0) s_timeout = 0;
-  __syncthreads();
-  for (int c = threadIdx.x; c < G; c += blockDim.x) {
-    long long t0 = clock64();
-    while (ld_acquire(flags + c) < seq) {
-      if (clock64() - t0 > 8000000000LL) {
-        s_timeout = 1;
-        atomicExch(&st->status, 99);
-        break;
-      }
+RCP_D u64 ll_get(const u64* p) {
+  u64 v;
+  asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+RCP_D void ll_put_d(u64* p, unsigned tag, double x) {
+  const u64 b = static_cast<u64>(__double_as_longlong(x));
+  ll_put(p, tag, static_cast<unsigned>(b));
+  ll_put(p + 1, tag, static_cast<unsigned>(b >> 32));
+}
+RCP_D double ll_d(unsigned lo, unsigned hi) {
+  return __longlong_as_double(static_cast<long long>((static_cast<u64>(hi) << 32) | lo));
+}
+// Spin until all NW words carry `tag`; false if the watchdog fired (a lost peer).
+template <int NW>
+RCP_D bool ll_read(const u64* p, unsigned tag, unsigned (&out)[NW]) {
+  const long long t0 = clock64();
+  while (true) {
+    bool ok = true;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) {
+      const u64 v = ll_get(p + w);
+      out[w] = static_cast<unsigned>(v);
+      ok &= static_cast<unsigned>(v >> 32) == tag;
     }
+    if (ok) return true;
+    if (clock64() - t0 > kWatchdogCycles) return false;
   }
-  __syncthreads();
-  return s_timeout == 0;
 }
 
-// Euclidean norm from a fused (sum of squares, max |x|) pass.  Falls back to the
-// reference's scaled formulation (core.py:122-142) when the plain sum could have
-// overflowed or underflowed.
+// Euclidean norm from a fused (sum of squares, max |x|) pass; falls back to the
+// reference's scaled formulation (core.py:122-142) when the plain sum could over/underflow.
 template <class Get>
 RCP_D double safe_norm(double sumsq, double amax, Get get, int lo, int hi) {
   if (amax == 0.0) return 0.0;
@@ -136,6 +139,9 @@ RCP_D double safe_norm(double sumsq, double amax, Get get, int lo, int hi) {
   return amax * sqrt(ss);
 }
 
+RCP_D long long prof_now() { return clock64(); }
+
+
 }  // namespace
 
 __global__ void __launch_bounds__(kPanelThreads, 1) panel_kernel(PanelParams p) {
@@ -146,6 +152,13 @@ __global__ void __launch_bounds__(kPanelThreads, 1) panel_kernel(PanelParams p) 
   const int m0 = static_cast<int>(n - k0);
   const int r0 = cta * R;
   const int rcnt = max(0, min(R, m0 - r0));
+  const bool prof = (cta == 0 && tid == 0);
+  const long long c_kernel0 = prof ? prof_now() : 0;
+  long long c_mark = 0;
+#define PROF_BEGIN() \
+  if (prof) c_mark = prof_now()
+#define PROF_END(slot) \
+  if (prof) atomicAdd(reinterpret_cast<unsigned long long*>(&p.st->cyc[slot]), (unsigned long long)(prof_now() - c_mark))
 
   // ---- shared memory carve-up
   unsigned char* sp = smem_raw;
@@ -159,171 +172,305 @@ __global__ void __launch_bounds__(kPanelThreads, 1) panel_kernel(PanelParams p) 
   double* vvec = reinterpret_cast<double*>(carve(sizeof(double) * P));
   double* wrow = reinterpret_cast<double*>(carve(sizeof(double) * Wn));
   double* wrrow = reinterpret_cast<double*>(carve(sizeof(double) * Wn));
+  double* lnext = reinterpret_cast<double*>(carve(sizeof(double) * Wn));
+  double* wnext = reinterpret_cast<double*>(carve(sizeof(double) * Wn));
   unsigned char* region = sp;  // QRCP and SBKP phases reuse the rest
 
-  __shared__ long long s_seq;
-  __shared__ int s_stop;
-  __shared__ double s_coef;
-  __shared__ int s_skip;
-  __shared__ double s_gakk;
-  __shared__ int s_gerr, s_lerr, s_wcta;
-  __shared__ double s_akk;
+  __shared__ int s_abort, s_gerr, s_lerr, s_skip, s_moved, s_wcol;
+  __shared__ double s_coef, s_gakk, s_akk;
+  __shared__ XRec s_win;
+  __shared__ unsigned s_qhdr[8], s_dhdr[12];
+  __shared__ int s_wpos, s_qflags, s_hascand;
 
   for (int x = tid; x < Wn; x += nthr) win[x] = x;
   for (int i = tid; i < rcnt; i += nthr) lpos[i] = r0 + i;
   if (tid == 0) {
-    s_seq = p.st->seq;
-    s_stop = 0;
+    s_abort = 0;
     s_lerr = 0;
   }
+  long long seq = p.st->seq;
+  int par = 0;  // block_argmax result buffer parity
   __syncthreads();
-  long long seq = s_seq;
 
   // =====================================================================
   // Phase 1: guard + partial QRCP on the sketch (q = b mode).
   // =====================================================================
+  const long long c_q0 = prof ? prof_now() : 0;
   if (p.qn > 0) {
-    const int Rs = p.Rs, Rg = R - Rs;
-    double* Bs = reinterpret_cast<double*>(region);
-    double* qnorm = Bs + (size_t)P * Rs;
+    // Register mode: one column per thread, rows [0, 32) in registers, the rest in smem.
+    // Generic mode: columns spread over threads; smem with a global spill.
+    const bool regmode = p.qmode == 1;
+    const int PRr = regmode ? min(P, kRegRows) : 0;
+    const int Ps = P - PRr;
+    const int Rs = regmode ? R : p.Rs;  // columns whose rows >= PRr live in smem
+    const int Rg = R - Rs;
+    double* Bs = reinterpret_cast<double*>(region);  // [Ps][Rs] row-major
+    double* qnorm = Bs + (size_t)Ps * Rs;             // generic mode only
     int* qsel = reinterpret_cast<int*>(qnorm + R);
-    double* qg = p.qscr + (size_t)cta * P * (Rg > 0 ? Rg : 0);
-    auto bel = [&](int r, int c) -> double& {
-      return c < Rs ? Bs[r * Rs + c] : qg[(size_t)r * Rg + (c - Rs)];
+    double* qg = p.qscr + (size_t)cta * Ps * (Rg > 0 ? Rg : 0);
+    auto bsm = [&](int r, int c) -> double& {  // row r >= PRr of column c
+      return c < Rs ? Bs[(r - PRr) * Rs + c] : qg[(size_t)(r - PRr) * Rg + (c - Rs)];
     };
-    for (int f = tid; f < P * rcnt; f += nthr) {
-      int c = f / P, r = f - c * P;
-      bel(r, c) = p.B[(size_t)(k0 + r0 + c) * P + r];
+    double rg[kRegRows];
+    const bool own = regmode && tid < rcnt;
+    bool mysel = !own;
+    double myn = -1.0, myn2 = 0.0, myn2x = 0.0;
+    bool exact_only = false;
+    int mypos = own ? r0 + tid : INT_MAX;
+
+    // ---- load
+    if (own) {
+      const double* src = p.B + (size_t)(k0 + r0 + tid) * P;
+#pragma unroll
+      for (int r = 0; r < kRegRows; ++r) rg[r] = (r < PRr) ? src[r] : 0.0;
     }
-    for (int c = tid; c < rcnt; c += nthr) qsel[c] = 0;
+    for (int f = tid; f < Ps * rcnt; f += nthr) {
+      int c = f / Ps, r = f - c * Ps;
+      bsm(PRr + r, c) = p.B[(size_t)(k0 + r0 + c) * P + PRr + r];
+    }
+    if (!regmode)
+      for (int c = tid; c < rcnt; c += nthr) qsel[c] = 0;
     __syncthreads();
-    for (int c = tid; c < rcnt; c += nthr) {
-      double ss = 0.0, am = 0.0;
-      for (int r = 0; r < P; ++r) {
-        double x = bel(r, c);
-        am = fmax(am, fabs(x));
-        ss = __fma_rn(x, x, ss);
+    // exact residual norm of the own column over rows [lo, P): sets myn, myn2, myn2x, exact_only
+    auto exact_norm = [&](int lo) {
+      double ss0 = 0.0, ss1 = 0.0, am = 0.0;
+#pragma unroll
+      for (int r = 0; r < kRegRows; ++r) {
+        if (r >= lo && r < PRr) {
+          am = fmax(am, fabs(rg[r]));
+          if (r & 1) ss1 = __fma_rn(rg[r], rg[r], ss1); else ss0 = __fma_rn(rg[r], rg[r], ss0);
+        }
       }
-      qnorm[c] = safe_norm(ss, am, [&](int r) { return bel(r, c); }, 0, P);
+      for (int r = max(lo, PRr); r < P; ++r) {
+        const double x = Bs[(r - PRr) * Rs + tid];
+        am = fmax(am, fabs(x));
+        if (r & 1) ss1 = __fma_rn(x, x, ss1); else ss0 = __fma_rn(x, x, ss0);
+      }
+      const double ss = __dadd_rn(ss0, ss1);
+      if (am == 0.0) {
+        myn = 0.0;
+        myn2 = 0.0;
+      } else if (am > 1e-140 && am < 1e140) {
+        myn2 = ss;
+        myn = sqrt(ss);
+      } else {
+        double s2 = 0.0;
+#pragma unroll
+        for (int r = 0; r < kRegRows; ++r)
+          if (r >= lo && r < PRr) {
+            const double x = fabs(rg[r]) / am;
+            s2 = __fma_rn(x, x, s2);
+          }
+        for (int r = max(lo, PRr); r < P; ++r) {
+          const double x = fabs(Bs[(r - PRr) * Rs + tid]) / am;
+          s2 = __fma_rn(x, x, s2);
+        }
+        myn = am * sqrt(s2);
+        myn2 = myn * myn;
+        exact_only = true;  // out of the safe range for squared downdates
+      }
+      myn2x = myn2;
+    };
+    if (own) exact_norm(0);
+    if (!regmode) {
+      for (int c = tid; c < rcnt; c += nthr) {
+        double ss = 0.0, am = 0.0;
+        for (int r = 0; r < P; ++r) {
+          double x = bsm(r, c);
+          am = fmax(am, fabs(x));
+          ss = __fma_rn(x, x, ss);
+        }
+        qnorm[c] = safe_norm(ss, am, [&](int r) { return bsm(r, c); }, 0, P);
+      }
     }
     __syncthreads();
 
     for (int j = 0; j < p.qn; ++j) {
       // ---- local candidate: largest residual norm, ties to the lowest position
+      PROF_BEGIN();
       double bk = -1.0;
       long long bi = LLONG_MAX;
       int bs = -1;
-      for (int c = tid; c < rcnt; c += nthr) {
-        if (qsel[c]) continue;
-        double v = qnorm[c];
-        long long ix = lpos[c];
-        if (better(v, ix, bk, bi)) {
-          bk = v;
-          bi = ix;
-          bs = c;
+      if (regmode) {
+        if (own && !mysel) {
+          bk = myn;
+          bi = mypos;
+          bs = tid;
+        }
+      } else {
+        for (int c = tid; c < rcnt; c += nthr) {
+          if (qsel[c]) continue;
+          double v = qnorm[c];
+          long long ix = lpos[c];
+          if (better(v, ix, bk, bi)) {
+            bk = v;
+            bi = ix;
+            bs = c;
+          }
         }
       }
-      BlockBest lb = block_argmax(bk, bi, bs);
+      BlockBest lb = block_argmax(bk, bi, bs, par);
+      par ^= 1;
       const long long nseq = seq + 1;
-      const int par = static_cast<int>(nseq & 1);
+      const int pb = static_cast<int>(nseq & 1);
+      const unsigned tag = static_cast<unsigned>(nseq);
       if (lb.slot >= 0) {
-        double* dst = p.qcol + ((size_t)par * G + cta) * P;
-        for (int r = j + tid; r < P; r += nthr) dst[r] = bel(r, lb.slot);
+        u64* dst = p.qcll + ((size_t)pb * G + cta) * 2 * P;
+        if (regmode) {
+          if (tid == lb.slot) {
+#pragma unroll
+            for (int r = 0; r < kRegRows; ++r)
+              if (r >= j && r < PRr) ll_put_d(dst + 2 * r, tag, rg[r]);
+          }
+          for (int r = max(j, PRr) + tid; r < P; r += nthr) ll_put_d(dst + 2 * r, tag, Bs[(r - PRr) * Rs + lb.slot]);
+        } else {
+          for (int r = j + tid; r < P; r += nthr) ll_put_d(dst + 2 * r, tag, bsm(r, lb.slot));
+        }
       }
       if (tid == 0) {
-        QRec rec;
-        rec.norm = lb.slot >= 0 ? lb.key : -1.0;
-        rec.pos = lb.slot >= 0 ? static_cast<int>(lb.idx) : INT_MAX;
-        rec.col = lb.slot >= 0 ? r0 + lb.slot : -1;
-        p.qrec[(size_t)par * G + cta] = rec;
+        u64* q = p.qll + ((size_t)pb * G + cta) * kQWords;
+        ll_put_d(q, tag, lb.slot >= 0 ? lb.key : -1.0);
+        ll_put(q + 2, tag, lb.slot >= 0 ? static_cast<unsigned>(lb.idx) : 0x7fffffffu);
+        ll_put(q + 3, tag, lb.slot >= 0 ? static_cast<unsigned>(r0 + lb.slot) : 0xffffffffu);
       }
       seq = nseq;
-      xpublish(p.flags, cta, seq);
-      if (!xwait(p.flags, G, seq, p.st)) {
-        s_stop = 1;
-        break;
-      }
-
-      // ---- global winner (every CTA reduces the same records identically)
-      double gk = -1.0;
-      long long gi = LLONG_MAX;
-      int gs = -1;
-      for (int c = tid; c < G; c += nthr) {
-        const QRec* rc = p.qrec + (size_t)par * G + c;
-        double v = __ldcg(&rc->norm);
-        int ps = __ldcg(&rc->pos);
-        if (v >= 0.0 || v != v) {
-          if (better(v, ps, gk, gi)) {
+      PROF_END(9);
+      PROF_BEGIN();
+      // ---- reducer CTA 0: winner over all records, winner column, Householder vector;
+      //      broadcast as one LL decision (header + v) that every other CTA reads.
+      u64* dec = p.qdll + (size_t)pb * (8 + 2 * (size_t)P);
+      if (cta == 0) {
+        if (tid == 0) s_qflags = 0;
+        double gk = -1.0;
+        long long gi = LLONG_MAX;
+        int gs = -1, gcol = -1;
+        for (int c = tid; c < G; c += nthr) {
+          unsigned w[kQWords];
+          if (!ll_read<kQWords>(p.qll + ((size_t)pb * G + c) * kQWords, tag, w)) {
+            s_abort = 1;
+            continue;
+          }
+          const double v = ll_d(w[0], w[1]);
+          const int ps = static_cast<int>(w[2]);
+          const int cl = static_cast<int>(w[3]);
+          if ((v >= 0.0 || v != v) && better(v, ps, gk, gi)) {
             gk = v;
             gi = ps;
             gs = c;
+            gcol = cl;
           }
         }
-      }
-      BlockBest gb = block_argmax(gk, gi, gs);
-      const int wcta = gb.slot;
-      const int wpos = static_cast<int>(gb.idx);
-      const int wcol = __ldcg(&p.qrec[(size_t)par * G + wcta].col);
-
-      if (j == 0 && p.guard_mode != 0) {
-        // tsel = max column norm of B[:, k:] (factor.py:576-583 / 405-408)
-        bool below = gb.key < p.guard_limit;
-        if (below) {
-          if (cta == 0 && tid == 0) p.st->status = p.guard_mode == 1 ? 1 : 2;
-          s_stop = 1;
-          break;
+        BlockBest gb = block_argmax(gk, gi, gs, par);
+        if (gs >= 0 && gs == gb.slot) s_wcol = gcol;  // the thread that loaded the winning record
+        const int wcta = gb.slot;
+        // guard: tsel = max column norm of B[:, k:] (factor.py:576-583 / 405-408)
+        const bool gstop = (j == 0 && p.guard_mode != 0 && gb.key < p.guard_limit);
+        if (!gstop && !s_abort) {
+          const u64* src = p.qcll + ((size_t)pb * G + wcta) * 2 * P;
+          for (int r = j + tid; r < P; r += nthr) {
+            unsigned w[2];
+            if (!ll_read<2>(src + 2 * r, tag, w)) s_abort = 1;
+            vvec[r] = ll_d(w[0], w[1]);
+          }
         }
-      }
-
-      // ---- Householder vector from the winner column (sketch.py:159-168)
-      const double* src = p.qcol + ((size_t)par * G + wcta) * P;
-      for (int r = j + tid; r < P; r += nthr) vvec[r] = __ldcg(src + r);
-      __syncthreads();
-      if (tid < 32) {
-        double xn2 = warp0_sum_sq(vvec, j, P);
-        double xn = sqrt(xn2);
-        double x0 = vvec[j];
-        double v0 = x0;
-        int skip = 0;
-        if (tid == 0) {
+        __syncthreads();
+        if (!gstop && !s_abort && tid < 32) {
+          // Householder vector (sketch.py:159-168)
+          double xn = sqrt(warp0_sum_sq(vvec, j, P));
+          xn = __shfl_sync(0xffffffffu, xn, 0);
           if (xn == 0.0) {
-            skip = 1;
+            if (tid == 0) s_skip = 1;
           } else {
-            v0 = __dadd_rn(x0, copysign(xn, x0 != 0.0 ? x0 : 1.0));
-          }
-        }
-        skip = __shfl_sync(0xffffffffu, skip, 0);
-        v0 = __shfl_sync(0xffffffffu, v0, 0);
-        if (!skip) {
-          if (tid == 0) vvec[j] = v0;
-          __syncwarp();
-          double vn2 = warp0_sum_sq(vvec, j, P);
-          if (tid == 0) {
-            if (vn2 == 0.0) {
-              s_skip = 1;
-            } else {
-              s_skip = 0;
+            if (tid == 0) {
+              const double x0 = vvec[j];
+              vvec[j] = __dadd_rn(x0, copysign(xn, x0 != 0.0 ? x0 : 1.0));
+            }
+            __syncwarp();
+            double vn2 = warp0_sum_sq(vvec, j, P);
+            if (tid == 0) {
+              s_skip = (vn2 == 0.0) ? 1 : 0;
               s_coef = 2.0 / vn2;
             }
           }
-        } else if (tid == 0) {
-          s_skip = 1;
         }
-        // ---- replay bookkeeping (factor.py:586-599): position j <-> wpos
-        if (tid == 0 && wpos != j) {
-          int cj = win[j];
+        __syncthreads();
+        // v first, header last: readers spin only on the header, then find v already visible
+        if (!gstop)
+          for (int r = j + tid; r < P; r += nthr) ll_put_d(dec + 8 + 2 * r, tag, vvec[r]);
+        __syncthreads();
+        if (tid == 0) {
+          s_wpos = static_cast<int>(gb.idx);
+          s_qflags = (s_skip ? 1 : 0) | (gstop ? 2 : 0) | (s_abort ? 4 : 0);
+          ll_put_d(dec + 0, tag, gb.key);
+          ll_put(dec + 2, tag, static_cast<unsigned>(s_wpos));
+          ll_put(dec + 3, tag, static_cast<unsigned>(s_wcol));
+          ll_put(dec + 4, tag, static_cast<unsigned>(s_qflags));
+          ll_put_d(dec + 5, tag, s_coef);
+        }
+      } else {
+        if (tid < 7) {
+          unsigned w[1];
+          if (!ll_read<1>(dec + tid, tag, w)) {
+            s_abort = 1;
+            w[0] = 0;
+          }
+          s_qhdr[tid] = w[0];
+        }
+        __syncthreads();
+        if (!s_abort) {
+          const unsigned fl = s_qhdr[4];
+          if (tid == 0) {
+            s_wpos = static_cast<int>(s_qhdr[2]);
+            s_wcol = static_cast<int>(s_qhdr[3]);
+            s_qflags = static_cast<int>(fl);
+            s_skip = fl & 1;
+            s_coef = ll_d(s_qhdr[5], s_qhdr[6]);
+          }
+          if (!(fl & 2)) {
+            for (int r = j + tid; r < P; r += nthr) {
+              unsigned w[2];
+              if (!ll_read<2>(dec + 8 + 2 * r, tag, w)) s_abort = 1;
+              vvec[r] = ll_d(w[0], w[1]);
+            }
+          }
+        }
+      }
+      par ^= 1;
+      __syncthreads();
+      PROF_END(1);
+      PROF_BEGIN();
+      if (s_abort || (s_qflags & 4)) {
+        if (tid == 0) atomicExch(&p.st->status, 99);
+        s_abort = 1;
+        break;
+      }
+      if (s_qflags & 2) {
+        if (cta == 0 && tid == 0) p.st->status = p.guard_mode == 1 ? 1 : 2;
+        s_abort = 2;
+        break;
+      }
+      const int wpos = s_wpos;
+      const int wcol = s_wcol;
+      // ---- replay bookkeeping (factor.py:586-599): position j <-> wpos
+      if (tid == 0) {
+        int moved = -1;
+        if (wpos != j) {
+          moved = win[j];
           win[j] = wcol;
-          if (wpos < Wn) win[wpos] = cj;
-          // owner updates of lpos are done below by all CTAs (cj owner)
-          s_wcta = cj;  // reuse as scratch: column that moves to wpos
-        } else if (tid == 0) {
-          s_wcta = -1;
+          if (wpos < Wn) win[wpos] = moved;
         }
+        s_moved = moved;
       }
       __syncthreads();
       {
-        const int moved = s_wcta;
-        if (tid == 0) {
+        const int moved = s_moved;
+        if (regmode) {
+          if (own && r0 + tid == wcol) {
+            mypos = j;
+            mysel = true;
+          }
+          if (own && moved >= 0 && r0 + tid == moved) mypos = wpos;
+        } else if (tid == 0) {
           if (wcol >= r0 && wcol < r0 + rcnt) {
             lpos[wcol - r0] = j;
             qsel[wcol - r0] = 1;
@@ -331,54 +478,129 @@ __global__ void __launch_bounds__(kPanelThreads, 1) panel_kernel(PanelParams p) 
           if (moved >= 0 && moved >= r0 && moved < r0 + rcnt) lpos[moved - r0] = wpos;
         }
       }
-      __syncthreads();
-
       // ---- reflect the remaining columns and refresh their residual norms
+      PROF_END(10);
+      PROF_BEGIN();
       if (j + 1 < p.qn) {
+        if (!regmode) __syncthreads();
         const int skip = s_skip;
         const double coef = s_coef;
-        for (int c = tid; c < rcnt; c += nthr) {
-          if (qsel[c]) continue;
-          double ss = 0.0, am = 0.0;
-          if (!skip) {
-            double d0 = 0.0, d1 = 0.0, d2 = 0.0, d3 = 0.0;
-            int r = j;
-            for (; r + 4 <= P; r += 4) {
-              d0 = __fma_rn(vvec[r], bel(r, c), d0);
-              d1 = __fma_rn(vvec[r + 1], bel(r + 1, c), d1);
-              d2 = __fma_rn(vvec[r + 2], bel(r + 2, c), d2);
-              d3 = __fma_rn(vvec[r + 3], bel(r + 3, c), d3);
+        if (regmode) {
+          if (own && !mysel) {
+            // Residual norms are downdated (|r|^2 -= y_j^2) and recomputed exactly whenever
+            // cancellation could cost more than ~1e-10 relative accuracy (LAPACK xLAQP2 policy).
+            double yj;
+            if (!skip) {
+              double d0 = 0.0, d1 = 0.0, d2 = 0.0, d3 = 0.0;
+#pragma unroll
+              for (int r = 0; r < kRegRows; r += 4) {
+                if (r >= j && r < PRr) d0 = __fma_rn(vvec[r], rg[r], d0);
+                if (r + 1 >= j && r + 1 < PRr) d1 = __fma_rn(vvec[r + 1], rg[r + 1], d1);
+                if (r + 2 >= j && r + 2 < PRr) d2 = __fma_rn(vvec[r + 2], rg[r + 2], d2);
+                if (r + 3 >= j && r + 3 < PRr) d3 = __fma_rn(vvec[r + 3], rg[r + 3], d3);
+              }
+              int r = max(j, PRr);
+              const double* bc = Bs + (size_t)(r - PRr) * Rs + tid;
+#pragma unroll 2
+              for (; r + 4 <= P; r += 4, bc += 4 * Rs) {
+                d0 = __fma_rn(vvec[r], bc[0], d0);
+                d1 = __fma_rn(vvec[r + 1], bc[Rs], d1);
+                d2 = __fma_rn(vvec[r + 2], bc[2 * Rs], d2);
+                d3 = __fma_rn(vvec[r + 3], bc[3 * Rs], d3);
+              }
+              for (; r < P; ++r, bc += Rs) d0 = __fma_rn(vvec[r], bc[0], d0);
+              const double wv = __dmul_rn(coef, __dadd_rn(__dadd_rn(d0, d1), __dadd_rn(d2, d3)));
+#pragma unroll
+              for (int r2 = 0; r2 < kRegRows; ++r2)
+                if (r2 >= j && r2 < PRr) rg[r2] = __fma_rn(-vvec[r2], wv, rg[r2]);
+              r = max(j, PRr);
+              double* bw = Bs + (size_t)(r - PRr) * Rs + tid;
+              // batched: all loads of a group before its stores (smem aliasing would
+              // otherwise serialise every element on the load latency)
+              for (; r + 8 <= P; r += 8, bw += 8 * Rs) {
+                double x[8], vv[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                  x[u] = bw[u * Rs];
+                  vv[u] = vvec[r + u];
+                }
+#pragma unroll
+                for (int u = 0; u < 8; ++u) bw[u * Rs] = __fma_rn(-vv[u], wv, x[u]);
+              }
+              for (; r < P; ++r, bw += Rs) *bw = __fma_rn(-vvec[r], wv, *bw);
             }
-            for (; r < P; ++r) d0 = __fma_rn(vvec[r], bel(r, c), d0);
-            const double wv = __dmul_rn(coef, __dadd_rn(__dadd_rn(d0, d1), __dadd_rn(d2, d3)));
-            {
-              double& x = bel(j, c);
-              x = __dsub_rn(x, __dmul_rn(vvec[j], wv));
+            if (j < PRr) {
+              yj = 0.0;
+#pragma unroll
+              for (int r2 = 0; r2 < kRegRows; ++r2)
+                if (r2 == j) yj = rg[r2];
+            } else {
+              yj = Bs[(j - PRr) * Rs + tid];
             }
-            for (r = j + 1; r < P; ++r) {
-              double& x = bel(r, c);
-              double y = __dsub_rn(x, __dmul_rn(vvec[r], wv));
-              x = y;
-              am = fmax(am, fabs(y));
-              ss = __fma_rn(y, y, ss);
-            }
-          } else {
-            for (int r = j + 1; r < P; ++r) {
-              double y = bel(r, c);
-              am = fmax(am, fabs(y));
-              ss = __fma_rn(y, y, ss);
+            const double n2 = __fma_rn(-yj, yj, myn2);
+            if (exact_only || !(n2 > 1e-6 * myn2x) || !(n2 > 1e-280)) {
+              exact_norm(j + 1);
+            } else {
+              myn2 = n2;
+              myn = sqrt(n2);
             }
           }
-          qnorm[c] = safe_norm(ss, am, [&](int r) { return bel(r, c); }, j + 1, P);
+        } else {
+          for (int c = tid; c < rcnt; c += nthr) {
+            if (qsel[c]) continue;
+            double ss = 0.0, am = 0.0;
+            if (!skip) {
+              double d0 = 0.0, d1 = 0.0, d2 = 0.0, d3 = 0.0;
+              int r = j;
+              for (; r + 4 <= P; r += 4) {
+                d0 = __fma_rn(vvec[r], bsm(r, c), d0);
+                d1 = __fma_rn(vvec[r + 1], bsm(r + 1, c), d1);
+                d2 = __fma_rn(vvec[r + 2], bsm(r + 2, c), d2);
+                d3 = __fma_rn(vvec[r + 3], bsm(r + 3, c), d3);
+              }
+              for (; r < P; ++r) d0 = __fma_rn(vvec[r], bsm(r, c), d0);
+              const double wv = __dmul_rn(coef, __dadd_rn(__dadd_rn(d0, d1), __dadd_rn(d2, d3)));
+              for (r = j; r < P; ++r) {
+                double& x = bsm(r, c);
+                const double y = __dsub_rn(x, __dmul_rn(vvec[r], wv));
+                x = y;
+                if (r > j) {
+                  am = fmax(am, fabs(y));
+                  ss = __fma_rn(y, y, ss);
+                }
+              }
+            } else {
+              for (int r = j + 1; r < P; ++r) {
+                const double y = bsm(r, c);
+                am = fmax(am, fabs(y));
+                ss = __fma_rn(y, y, ss);
+              }
+            }
+            qnorm[c] = safe_norm(ss, am, [&](int r) { return bsm(r, c); }, j + 1, P);
+          }
         }
-        __syncthreads();
       }
+      __syncthreads();
+      PROF_END(6);
     }
+    if (regmode && own) lpos[tid] = mypos;
   }
-
-  if (s_stop) {
+  if (prof) atomicAdd(reinterpret_cast<unsigned long long*>(&p.st->cyc[0]), (unsigned long long)(prof_now() - c_q0));
+  __syncthreads();
+  if (s_abort) {
     if (cta == 0 && tid == 0) p.st->seq = seq;
     return;
+  }
+  {
+    // Prefetch this CTA's row slice of the panel's candidate pivot columns (the QRCP
+    // selection, positions [0, Wn)) into L2: most SBKP pivot columns come from here.
+    const int nl = (rcnt + 15) / 16;
+    const int wx = min(Wn, m0);
+    for (int f = tid; f < wx * nl; f += nthr) {
+      const int x = f / nl, line = f - x * nl;
+      const double* ptr = p.A + (k0 + r0 + 16 * line) + (int64_t)(k0 + win[x]) * n;
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(ptr));
+    }
   }
 
   // =====================================================================
@@ -389,7 +611,6 @@ __global__ void __launch_bounds__(kPanelThreads, 1) panel_kernel(PanelParams p) 
   double* ck = Lsm + (size_t)Ls * R;
   double* cr = ck + R;
   double* dg = cr + R;
-  double* acol = dg + R;
   const double* A = p.A;
   const double alpha = p.alpha;
   const int width = p.width;
@@ -398,15 +619,17 @@ __global__ void __launch_bounds__(kPanelThreads, 1) panel_kernel(PanelParams p) 
     int64_t x = k0 + r0 + i;
     dg[i] = A[x * (n + 1)];
   }
-  __syncthreads();
   int pk = win[0];
-  for (int i = tid; i < rcnt; i += nthr) acol[i] = sym_lower(A, n, k0 + r0 + i, k0 + pk);
   __syncthreads();
 
   int t = 0;
   while (t < width && k0 + t < n) {
     // ---- phase A: pivot column (rows of the active block owned here)
-    if (tid == 0) s_akk = 0.0;
+    PROF_BEGIN();
+    if (tid == 0) {
+      s_akk = 0.0;
+      s_gerr = 0;
+    }
     __syncthreads();
     double bk = -1.0;
     long long bi = LLONG_MAX;
@@ -415,10 +638,9 @@ __global__ void __launch_bounds__(kPanelThreads, 1) panel_kernel(PanelParams p) 
       const int lp = lpos[i];
       if (lp < t) continue;
       const int64_t row = k0 + r0 + i;
-      double dot = chain_dot4(
-          [&](int s) { return s < Ls ? Lsm[(size_t)s * R + i] : __ldcg(p.Lbuf + row + (int64_t)(k0 + s) * n); },
-          wrow, t);
-      double c = __dsub_rn(acol[i], dot);
+      const double av = sym_at(A, n, row, k0 + pk);  // issued before the dot: latency overlaps it
+      const double dot = row_dot4(Lsm + i, R, Ls, p.Lbuf + row + (int64_t)k0 * n, n, wrow, t);
+      double c = __dsub_rn(av, dot);
       ck[i] = c;
       if (lp > t) {
         double key = fabs(c);
@@ -430,58 +652,114 @@ __global__ void __launch_bounds__(kPanelThreads, 1) panel_kernel(PanelParams p) 
       }
       if (r0 + i == pk) s_akk = c;
     }
-    BlockBest lb = block_argmax(bk, bi, bs);
+    PROF_END(2);
+    PROF_BEGIN();
+    BlockBest lb = block_argmax(bk, bi, bs, par);
+    par ^= 1;
     const long long nseq = seq + 1;
-    const int par = static_cast<int>(nseq & 1);
+    const int pb = static_cast<int>(nseq & 1);
+    const unsigned tag = static_cast<unsigned>(nseq);
     if (tid == 0) {
-      XRec rec;
-      rec.key = lb.slot >= 0 ? lb.key : -1.0;
-      rec.val = lb.slot >= 0 ? ck[lb.slot] : 0.0;
-      rec.diag = lb.slot >= 0 ? dg[lb.slot] : 0.0;
-      rec.lidx = lb.slot >= 0 ? static_cast<int>(lb.idx) : INT_MAX;
-      rec.phys = lb.slot >= 0 ? r0 + lb.slot : -1;
-      rec.has_akk = (pk >= r0 && pk < r0 + rcnt) ? 1 : 0;
-      rec.akk = s_akk;
-      rec.err = s_lerr;
-      p.xrec[(size_t)par * G + cta] = rec;
+      u64* q = p.xll + ((size_t)pb * G + cta) * kXWords;
+      const bool has = lb.slot >= 0;
+      ll_put_d(q + 0, tag, has ? lb.key : -1.0);
+      ll_put_d(q + 2, tag, has ? ck[lb.slot] : 0.0);
+      ll_put_d(q + 4, tag, has ? dg[lb.slot] : 0.0);
+      ll_put_d(q + 6, tag, s_akk);
+      ll_put(q + 8, tag, has ? static_cast<unsigned>(lb.idx) : 0x7fffffffu);
+      ll_put(q + 9, tag, has ? static_cast<unsigned>(r0 + lb.slot) : 0xffffffffu);
+      ll_put(q + 10, tag, ((pk >= r0 && pk < r0 + rcnt) ? 1u : 0u) | (s_lerr ? 2u : 0u));
     }
     seq = nseq;
-    xpublish(p.flags, cta, seq);
-    if (!xwait(p.flags, G, seq, p.st)) break;
+    PROF_END(8);
+    PROF_BEGIN();
 
-    // ---- identical reduction of all records in every CTA
-    if (tid == 0) s_gerr = 0;
-    __syncthreads();
-    double gk = -1.0;
-    long long gi = LLONG_MAX;
-    int gs = -1;
-    for (int c = tid; c < G; c += nthr) {
-      const XRec* rc = p.xrec + (size_t)par * G + c;
-      double v = __ldcg(&rc->key);
-      int li = __ldcg(&rc->lidx);
-      if (v >= 0.0 || v != v) {
-        if (better(v, li, gk, gi)) {
-          gk = v;
-          gi = li;
+    // ---- reducer CTA 0 reads all records and broadcasts the decision inputs (one LL record)
+    u64* dec = p.sdll + (size_t)pb * kXWords;
+    if (cta == 0) {
+      double gk = -1.0;
+      long long gi = LLONG_MAX;
+      int gs = -1;
+      XRec mine;
+      mine.key = -1.0;
+      for (int c = tid; c < G; c += nthr) {
+        unsigned w[11];
+        if (!ll_read<11>(p.xll + ((size_t)pb * G + c) * kXWords, tag, w)) {
+          s_abort = 1;
+          continue;
+        }
+        XRec r;
+        r.key = ll_d(w[0], w[1]);
+        r.val = ll_d(w[2], w[3]);
+        r.diag = ll_d(w[4], w[5]);
+        r.akk = ll_d(w[6], w[7]);
+        r.lidx = static_cast<int>(w[8]);
+        r.phys = static_cast<int>(w[9]);
+        r.has_akk = w[10] & 1u;
+        r.err = (w[10] >> 1) & 1u;
+        if (r.has_akk) s_gakk = r.akk;
+        if (r.err) s_gerr = 1;
+        if ((r.key >= 0.0 || r.key != r.key) && better(r.key, r.lidx, gk, gi)) {
+          gk = r.key;
+          gi = r.lidx;
           gs = c;
+          mine = r;
         }
       }
-      if (__ldcg(&rc->has_akk)) s_gakk = __ldcg(&rc->akk);
-      if (__ldcg(&rc->err)) s_gerr = 1;
+      BlockBest gb = block_argmax(gk, gi, gs, par);
+      if (gb.slot >= 0 && gs == gb.slot) s_win = mine;  // the thread holding the winning record
+      if (tid == 0) s_hascand = gb.slot >= 0 ? 1 : 0;
+      __syncthreads();
+      if (tid == 0) {
+        ll_put_d(dec + 0, tag, s_win.key);
+        ll_put_d(dec + 2, tag, s_win.val);
+        ll_put_d(dec + 4, tag, s_win.diag);
+        ll_put_d(dec + 6, tag, s_gakk);
+        ll_put(dec + 8, tag, static_cast<unsigned>(s_win.lidx));
+        ll_put(dec + 9, tag, static_cast<unsigned>(s_win.phys));
+        ll_put(dec + 10, tag, (s_hascand ? 1u : 0u) | (s_gerr ? 2u : 0u) | (s_abort ? 4u : 0u));
+      }
+    } else {
+      if (tid < 11) {
+        unsigned w[1];
+        if (!ll_read<1>(dec + tid, tag, w)) {
+          s_abort = 1;
+          w[0] = 0;
+        }
+        s_dhdr[tid] = w[0];
+      }
+      __syncthreads();
+      if (tid == 0) {
+        s_win.key = ll_d(s_dhdr[0], s_dhdr[1]);
+        s_win.val = ll_d(s_dhdr[2], s_dhdr[3]);
+        s_win.diag = ll_d(s_dhdr[4], s_dhdr[5]);
+        s_gakk = ll_d(s_dhdr[6], s_dhdr[7]);
+        s_win.lidx = static_cast<int>(s_dhdr[8]);
+        s_win.phys = static_cast<int>(s_dhdr[9]);
+        s_hascand = s_dhdr[10] & 1u;
+        if (s_dhdr[10] & 2u) s_gerr = 1;
+        if (s_dhdr[10] & 4u) s_abort = 1;
+      }
     }
-    BlockBest gb = block_argmax(gk, gi, gs);
+    par ^= 1;
+    __syncthreads();
+    PROF_END(3);
+    PROF_BEGIN();
+    if (s_abort) {
+      if (cta == 0 && tid == 0) atomicExch(&p.st->status, 99);
+      break;
+    }
     if (s_gerr) break;
     const double akk = s_gakk;
-    const bool has_cand = gb.slot >= 0;
+    const bool has_cand = s_hascand != 0;
     double lam = 0.0, ckr = 0.0, dr = 0.0;
     int r_rel = -1, pr = -1;
     if (has_cand) {
-      const XRec* rc = p.xrec + (size_t)par * G + gb.slot;
-      lam = __ldcg(&rc->key);
-      ckr = __ldcg(&rc->val);
-      dr = __ldcg(&rc->diag);
-      r_rel = __ldcg(&rc->lidx);
-      pr = __ldcg(&rc->phys);
+      lam = s_win.key;
+      ckr = s_win.val;
+      dr = s_win.diag;
+      r_rel = s_win.lidx;
+      pr = s_win.phys;
     }
 
     // ---- SBKP decision (pivot.py:111-128): 0 skip, 1 1x1, 2 1x1-swap, 3 2x2
@@ -504,43 +782,37 @@ __global__ void __launch_bounds__(kPanelThreads, 1) panel_kernel(PanelParams p) 
 
     // ---- symmetric swaps as permutation bookkeeping (factor.py:624-630)
     int p_t = pk, p_t1 = -1;
-    if (kind == 2) {
-      // swap(k, r)
+    if (kind == 2) {  // swap(k, r)
       if (tid == 0) {
         win[t] = pr;
         if (r_rel < Wn) win[r_rel] = pk;
-      }
-      if (tid == 0) {
         if (pr >= r0 && pr < r0 + rcnt) lpos[pr - r0] = t;
         if (pk >= r0 && pk < r0 + rcnt) lpos[pk - r0] = r_rel;
       }
       p_t = pr;
-    } else if (kind == 3) {
-      if (r_rel != t + 1) {
-        if (tid == 0) {
-          const int p1 = win[t + 1];
-          win[t + 1] = pr;
-          if (r_rel < Wn) win[r_rel] = p1;
-          if (pr >= r0 && pr < r0 + rcnt) lpos[pr - r0] = t + 1;
-          if (p1 >= r0 && p1 < r0 + rcnt) lpos[p1 - r0] = r_rel;
-        }
+    } else if (kind == 3) {  // swap(k+1, r)
+      if (r_rel != t + 1 && tid == 0) {
+        const int p1 = win[t + 1];
+        win[t + 1] = pr;
+        if (r_rel < Wn) win[r_rel] = p1;
+        if (pr >= r0 && pr < r0 + rcnt) lpos[pr - r0] = t + 1;
+        if (p1 >= r0 && p1 < r0 + rcnt) lpos[p1 - r0] = r_rel;
       }
       p_t1 = pr;
     }
-    __syncthreads();
 
     // ---- phase B: partner column when needed, multipliers, writes
     const int64_t kglob = k0 + t;
     if (kind >= 2) {
       for (int s2 = tid; s2 < t; s2 += nthr) wrrow[s2] = __ldcg(p.W + (k0 + pr) + (int64_t)s2 * n);
-      __syncthreads();
+      const double av0 = (tid < rcnt) ? sym_at(A, n, k0 + r0 + tid, k0 + pr) : 0.0;
+      __syncthreads();  // wrrow ready, swaps (lpos) visible
       for (int i = tid; i < rcnt; i += nthr) {
+        const double a_ip = (i == tid) ? av0 : sym_at(A, n, k0 + r0 + i, k0 + pr);
         if (lpos[i] < t) continue;
         const int64_t row = k0 + r0 + i;
-        double dot = chain_dot4(
-            [&](int s3) { return s3 < Ls ? Lsm[(size_t)s3 * R + i] : __ldcg(p.Lbuf + row + (int64_t)(k0 + s3) * n); },
-            wrrow, t);
-        cr[i] = __dsub_rn(sym_lower(A, n, row, k0 + pr), dot);
+        const double dot = row_dot4(Lsm + i, R, Ls, p.Lbuf + row + (int64_t)k0 * n, n, wrrow, t);
+        cr[i] = __dsub_rn(a_ip, dot);
       }
     }
     // D block and its checks (factor.py:202-226, 455-466) — identical in every CTA
@@ -573,7 +845,7 @@ __global__ void __launch_bounds__(kPanelThreads, 1) panel_kernel(PanelParams p) 
       if (cta == 0 && tid == 0) atomicMin(&p.st->err, (kglob << 8) | num_kind);
       break;
     }
-    __syncthreads();  // cr complete before use; lpos updates visible
+    __syncthreads();  // cr complete; lpos / win updates visible
     bool lerr = false;
     for (int i = tid; i < rcnt; i += nthr) {
       const int lp = lpos[i];
@@ -641,46 +913,35 @@ __global__ void __launch_bounds__(kPanelThreads, 1) panel_kernel(PanelParams p) 
       p.st->n_steps += 1;
       if (kind == 3) p.st->n_2x2 += 1;
     }
+    PROF_END(4);
 
-    // ---- next pivot: its W row (older entries from memory, this step's entries
-    //      recomputed redundantly with the owner's exact arithmetic) + A column prefetch
+    // ---- next pivot: its W row (older entries from memory, this step's entries recomputed
+    //      redundantly with the owner's exact arithmetic from an smem copy of its L row)
+    PROF_BEGIN();
     const int tn = t + s;
-    __syncthreads();
     if (tn < width && k0 + tn < n) {
-      const int pn = win[tn];
+      const int pn = win[tn];  // win updated by tid 0 before the barrier above
+      const int64_t rown = k0 + pn;
+      for (int s3 = tid; s3 < t; s3 += nthr) {
+        lnext[s3] = __ldcg(p.Lbuf + rown + (int64_t)(k0 + s3) * n);
+        wnext[s3] = __ldcg(p.W + rown + (int64_t)s3 * n);
+      }
+      const double an0 = (tid == 0) ? sym_at(A, n, rown, k0 + (kind == 2 ? pr : pk)) : 0.0;
+      const double an1 = (tid == 0 && kind == 3) ? sym_at(A, n, rown, k0 + pr) : 0.0;
+      __syncthreads();
       if (tid == 0) {
-        const int64_t rown = k0 + pn;
-        auto lrow = [&](int s3) { return __ldcg(p.Lbuf + rown + (int64_t)(k0 + s3) * n); };
-        double v0, v1 = 0.0;
-        if (kind <= 1) {
-          v0 = __dsub_rn(sym_lower(A, n, rown, k0 + pk), chain_dot4(lrow, wrow, t));
-        } else if (kind == 2) {
-          v0 = __dsub_rn(sym_lower(A, n, rown, k0 + pr), chain_dot4(lrow, wrrow, t));
-        } else {
-          v0 = __dsub_rn(sym_lower(A, n, rown, k0 + pk), chain_dot4(lrow, wrow, t));
-          v1 = __dsub_rn(sym_lower(A, n, rown, k0 + pr), chain_dot4(lrow, wrrow, t));
-        }
-        s_coef = v0;  // scratch broadcast
-        s_gakk = v1;
+        auto lrow = [&](int s3) { return lnext[s3]; };
+        const double v0 = __dsub_rn(an0, chain_dot4(lrow, kind == 2 ? wrrow : wrow, t));
+        wnext[t] = v0;
+        if (kind == 3) wnext[t + 1] = __dsub_rn(an1, chain_dot4(lrow, wrrow, t));
       }
       __syncthreads();
-      const double v0 = s_coef, v1 = s_gakk;
-      for (int s3 = tid; s3 < tn; s3 += nthr) {
-        double w;
-        if (s3 < t) {
-          w = __ldcg(p.W + (k0 + pn) + (int64_t)s3 * n);
-        } else {
-          w = (s3 == t) ? v0 : v1;
-        }
-        wrow[s3] = w;
-      }
-      for (int i = tid; i < rcnt; i += nthr) {
-        if (lpos[i] >= tn) acol[i] = sym_lower(A, n, k0 + r0 + i, k0 + pn);
-      }
+      for (int s3 = tid; s3 < tn; s3 += nthr) wrow[s3] = wnext[s3];
       pk = pn;
     }
     t = tn;
     __syncthreads();
+    PROF_END(5);
   }
 
   // ---- publish the panel's permutation and outcome
@@ -694,6 +955,9 @@ __global__ void __launch_bounds__(kPanelThreads, 1) panel_kernel(PanelParams p) 
     p.st->k_end = k0 + t;
     p.st->t_end = t;
   }
+  if (prof) atomicAdd(reinterpret_cast<unsigned long long*>(&p.st->cyc[7]), (unsigned long long)(prof_now() - c_kernel0));
+#undef PROF_BEGIN
+#undef PROF_END
 }
 
 cudaError_t panel_init_attributes(int max_dyn_smem) {

@@ -15,7 +15,13 @@ struct PanelState {
   int n_steps;         // decisions taken (cumulative)
   int n_2x2;           // 2x2 blocks (cumulative)
   int pad;
+  long long pad2;
+  // SM-cycle profile of CTA 0 (cumulative), see kProfNames in capi.cu
+  long long cyc[16];
 };
+
+constexpr int kXWords = 16;  // 11 used, padded to 128 B per record
+constexpr int kQWords = 4;
 
 // One CTA's contribution to a pivot-search exchange (SBKP step).
 struct XRec {
@@ -27,6 +33,7 @@ struct XRec {
   int phys;     // physical (panel-relative) row of the candidate
   int has_akk;
   int err;
+  double pad[2];  // 64-byte records
 };
 
 // One CTA's contribution to a QRCP exchange.
@@ -43,6 +50,7 @@ struct PanelParams {
   double guard_limit;  // thr * beta
   double alpha;
   int G, R, Rs, Ls, Wn;
+  int qmode;           // QRCP: 1 = register mode (one column per thread), 0 = generic
   const double* A;     // trailing matrix at panel start, col-major ld n, lower triangle valid
   const double* B;     // sketch, P x n col-major (ld P), panel-start order
   double* qscr;        // spill for sketch columns that do not fit in smem
@@ -57,10 +65,13 @@ struct PanelParams {
   int8_t* pattern;
   int8_t* trace_kind;
   int32_t* trace_r;
-  long long* flags;    // [G]
-  XRec* xrec;          // [2][G]
-  QRec* qrec;          // [2][G]
-  double* qcol;        // [2][G][P]
+  // Exchange buffers in LL format (NCCL-style): every 64-bit word carries 32 data bits and
+  // the 32-bit exchange tag, so a reader validates data and arrival with one load.
+  unsigned long long* xll;   // SBKP records  [2][G][kXWords]
+  unsigned long long* qll;   // QRCP records  [2][G][kQWords]
+  unsigned long long* qcll;  // QRCP candidate columns [2][G][2P]
+  unsigned long long* sdll;  // SBKP decision broadcast by the reducer CTA [2][kXWords]
+  unsigned long long* qdll;  // QRCP decision (header + Householder vector) [2][8 + 2P]
   PanelState* st;
 };
 

@@ -25,10 +25,9 @@ RCP_D void st_release(long long* p, long long v) {
 }
 
 // ---------------------------------------------------------------- symmetric access
-// Trailing blocks keep only the LOWER triangle valid (column-major, ld = n).
-RCP_D double sym_lower(const double* a, int64_t ld, int64_t i, int64_t j) {
-  return (i >= j) ? a[i + j * ld] : a[j + i * ld];
-}
+// Trailing blocks are stored in FULL symmetric form (column-major, ld = n): element (i, j)
+// is read from column j, so a pivot column is one contiguous read.
+RCP_D double sym_at(const double* a, int64_t ld, int64_t i, int64_t j) { return a[i + j * ld]; }
 
 // ---------------------------------------------------------------- pivot-column dot
 // Dot product of row i of the panel L (Lrow(s)) with the pivot's W row w[s], s < t,
@@ -48,6 +47,35 @@ RCP_D double chain_dot4(F lrow, const double* w, int t) {
   if (s < t) c0 = __fma_rn(lrow(s), w[s], c0);
   if (s + 1 < t) c1 = __fma_rn(lrow(s + 1), w[s + 1], c1);
   if (s + 2 < t) c2 = __fma_rn(lrow(s + 2), w[s + 2], c2);
+  return __dadd_rn(__dadd_rn(c0, c1), __dadd_rn(c2, c3));
+}
+
+// Same chain arithmetic for a row of the panel L held partly in shared memory (columns
+// s < ls, at lsm[s * ldsm]) and partly in global memory (s >= ls, at lg[s * ldg]).
+// Chain q accumulates the terms s = q (mod 4) in increasing s, exactly like chain_dot4.
+RCP_D double row_dot4(const double* __restrict__ lsm, int ldsm, int ls, const double* __restrict__ lg, int64_t ldg,
+                      const double* __restrict__ w, int t) {
+  double c0 = 0.0, c1 = 0.0, c2 = 0.0, c3 = 0.0;
+  const int ts = t < ls ? t : ls;
+  int s = 0;
+  const double* lp = lsm;
+  const int st4 = 4 * ldsm;
+#pragma unroll 2
+  for (; s + 4 <= ts; s += 4, lp += st4) {
+    c0 = __fma_rn(lp[0], w[s], c0);
+    c1 = __fma_rn(lp[ldsm], w[s + 1], c1);
+    c2 = __fma_rn(lp[2 * ldsm], w[s + 2], c2);
+    c3 = __fma_rn(lp[3 * ldsm], w[s + 3], c3);
+  }
+  for (; s < t; ++s) {
+    const double x = (s < ls) ? lsm[s * ldsm] : __ldcg(lg + (int64_t)s * ldg);
+    switch (s & 3) {
+      case 0: c0 = __fma_rn(x, w[s], c0); break;
+      case 1: c1 = __fma_rn(x, w[s], c1); break;
+      case 2: c2 = __fma_rn(x, w[s], c2); break;
+      default: c3 = __fma_rn(x, w[s], c3); break;
+    }
+  }
   return __dadd_rn(__dadd_rn(c0, c1), __dadd_rn(c2, c3));
 }
 

@@ -2,57 +2,43 @@
 // sketch projection and sketch correction.
 #include "gemm_dmma.cuh"
 #include "misc.cuh"
+#include "schur_kernel.cuh"
 
 namespace rcp {
 
 namespace {
 
-// A22 <- A22 - L21 W21^T on the lower triangle, reading the previous matrix through the
-// panel permutation (factor.py:369-379 + core.py:115-119: the stored value of (i, j),
-// i > j, is the lower-computed one).
-struct SchurEpi {
-  static constexpr bool kNeedInit = true;
-  const double* ain;
-  double* aout;
-  const int* phys;
-  int64_t n, k, mp;
-  RCP_D double init(int64_t i, int64_t j) const {
-    if (i >= mp || j >= mp || i < j) return 0.0;
-    return sym_lower(ain, n, phys[i], phys[j]);
-  }
-  RCP_D void store(int64_t i, int64_t j, double v) const {
-    if (i < mp && j < mp && i >= j) aout[(k + i) + (k + j) * n] = v;
-  }
-};
-
 struct SketchEpi {
-  static constexpr bool kNeedInit = false;
+  static constexpr bool kHasInput = false;
+  static constexpr bool kMirror = false;
+  RCP_D double* cout_mirror(int64_t, int64_t) const { return nullptr; }
   double* b;
   int64_t P, ncols, col0;
-  RCP_D double init(int64_t, int64_t) const { return 0.0; }
-  RCP_D void store(int64_t r, int64_t j, double v) const {
-    if (r < P && j < ncols) b[r + (col0 + j) * P] = v;
-  }
+  RCP_D int map_row(int64_t) const { return 0; }
+  RCP_D int map_col(int64_t) const { return 0; }
+  RCP_D const double* dummy() const { return b; }
+  RCP_D const double* cin(int64_t, int64_t, int, int) const { return nullptr; }
+  RCP_D double* cout(int64_t r, int64_t j) const { return (r < P && j < ncols) ? b + r + (col0 + j) * P : nullptr; }
 };
 
 struct SketchCorrEpi {
-  static constexpr bool kNeedInit = true;
+  static constexpr bool kHasInput = true;
+  static constexpr bool kMirror = false;
+  RCP_D double* cout_mirror(int64_t, int64_t) const { return nullptr; }
   const double* bin;
   double* bout;
   const int* phys;
   int64_t P, mp, k;
-  RCP_D double init(int64_t r, int64_t j) const {
-    return (r < P && j < mp) ? bin[r + (int64_t)phys[j] * P] : 0.0;
+  RCP_D int map_row(int64_t) const { return 0; }
+  RCP_D int map_col(int64_t j) const { return j < mp ? phys[j] : -1; }
+  RCP_D const double* dummy() const { return bin; }
+  RCP_D const double* cin(int64_t r, int64_t j, int, int pj) const {
+    return (r < P && j < mp) ? bin + r + (int64_t)pj * P : nullptr;
   }
-  RCP_D void store(int64_t r, int64_t j, double v) const {
-    if (r < P && j < mp) bout[r + (k + j) * P] = v;
-  }
+  RCP_D double* cout(int64_t r, int64_t j) const { return (r < P && j < mp) ? bout + r + (k + j) * P : nullptr; }
 };
 
-template <int BM, int BN>
-constexpr size_t smem_bytes() {
-  return sizeof(GemmSmem<BM, BN>);
-}
+constexpr int kRectStages = 3;
 
 bool aligned16(const void* p, int64_t ld) {
   return (reinterpret_cast<uintptr_t>(p) % 16 == 0) && (ld % 2 == 0);
@@ -62,32 +48,28 @@ bool aligned16(const void* p, int64_t ld) {
 
 cudaError_t gemm_init_attributes() {
   cudaError_t e;
-  e = cudaFuncSetAttribute(dmma_gemm_kernel<128, 128, 2, LowerMap, SchurEpi>,
-                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes<128, 128>());
+  e = cudaFuncSetAttribute(schur_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)schur_smem_bytes());
   if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(dmma_gemm_kernel<64, 128, 2, RectMap, SketchEpi>,
-                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes<64, 128>());
+  e = cudaFuncSetAttribute(dmma_gemm_kernel<64, 128, kRectStages, 2, RectMap, SketchEpi>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gemm_smem_bytes<64, 128, kRectStages>());
   if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(dmma_gemm_kernel<64, 128, 1, RectMap, SketchEpi>,
-                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes<64, 128>());
+  e = cudaFuncSetAttribute(dmma_gemm_kernel<64, 128, kRectStages, 1, RectMap, SketchEpi>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gemm_smem_bytes<64, 128, kRectStages>());
   if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(dmma_gemm_kernel<64, 128, 2, RectMap, SketchCorrEpi>,
-                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes<64, 128>());
+  e = cudaFuncSetAttribute(dmma_gemm_kernel<64, 128, kRectStages, 2, RectMap, SketchCorrEpi>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gemm_smem_bytes<64, 128, kRectStages>());
   return e;
 }
 
 cudaError_t launch_schur_update(int64_t n, int64_t k, int64_t mp, const double* Lneg, const double* Wg, int tpad,
                                 int K, const double* A_in, const int* phys, double* A_out, cudaStream_t st) {
   if (mp <= 0 || K <= 0) return cudaSuccess;
-  const int64_t nb = (mp + 127) / 128;
-  const int64_t tiles = nb * (nb + 1) / 2;
-  // operands are zero padded to tpad (a multiple of kBK) along K
-  const int Kl = ((K + kBK - 1) / kBK) * kBK;
-  OperandDesc a{Lneg, tpad, mp, tpad};
-  OperandDesc b{Wg, tpad, mp, tpad};
-  SchurEpi epi{A_in, A_out, phys, n, k, mp};
-  dmma_gemm_kernel<128, 128, 2, LowerMap, SchurEpi>
-      <<<(unsigned)tiles, kGemmThreads, smem_bytes<128, 128>(), st>>>(a, b, Kl, LowerMap{128}, epi);
+  const int64_t nbi = (mp + kSchurBM - 1) / kSchurBM;
+  const int64_t tiles = nbi * (nbi + 1);  // row block I has 2I+2 column blocks of 64
+  const int Kl = ((K + kBK - 1) / kBK) * kBK;  // operands are zero padded to tpad along K
+  schur_update_kernel<<<(unsigned)tiles, kSchurThreads, schur_smem_bytes(), st>>>(Lneg, Wg, tpad, Kl, A_in, A_out,
+                                                                                 phys, n, k, mp);
   return cudaGetLastError();
 }
 
@@ -99,12 +81,13 @@ cudaError_t launch_sketch_gemm(int P, int64_t m, const double* omega, int64_t ld
   OperandDesc b{A, lda, m, m};
   SketchEpi epi{B, P, m, col0};
   RectMap map{tn, 64, 128};
+  const size_t smem = gemm_smem_bytes<64, 128, kRectStages>();
   if (aligned16(omega, ldo) && aligned16(A, lda) && (m % 2 == 0)) {
-    dmma_gemm_kernel<64, 128, 2, RectMap, SketchEpi>
-        <<<(unsigned)(tm * tn), kGemmThreads, smem_bytes<64, 128>(), st>>>(a, b, m, map, epi);
+    dmma_gemm_kernel<64, 128, kRectStages, 2, RectMap, SketchEpi>
+        <<<(unsigned)(tm * tn), kGemmThreads, smem, st>>>(a, b, m, map, epi);
   } else {
-    dmma_gemm_kernel<64, 128, 1, RectMap, SketchEpi>
-        <<<(unsigned)(tm * tn), kGemmThreads, smem_bytes<64, 128>(), st>>>(a, b, m, map, epi);
+    dmma_gemm_kernel<64, 128, kRectStages, 1, RectMap, SketchEpi>
+        <<<(unsigned)(tm * tn), kGemmThreads, smem, st>>>(a, b, m, map, epi);
   }
   return cudaGetLastError();
 }
@@ -119,8 +102,8 @@ cudaError_t launch_sketch_correction(int P, int64_t mp, int64_t k, const double*
   OperandDesc b{Lneg, tpad, mp, tpad};
   SketchCorrEpi epi{B_in, B_out, phys, P, mp, k};
   RectMap map{tn, 64, 128};
-  dmma_gemm_kernel<64, 128, 2, RectMap, SketchCorrEpi>
-      <<<(unsigned)(tm * tn), kGemmThreads, smem_bytes<64, 128>(), st>>>(a, b, Kl, map, epi);
+  dmma_gemm_kernel<64, 128, kRectStages, 2, RectMap, SketchCorrEpi>
+      <<<(unsigned)(tm * tn), kGemmThreads, gemm_smem_bytes<64, 128, kRectStages>(), st>>>(a, b, Kl, map, epi);
   return cudaGetLastError();
 }
 

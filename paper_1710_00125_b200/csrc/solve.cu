@@ -180,13 +180,17 @@ __global__ void scale_ld_kernel(int64_t n, const double* __restrict__ L, const d
 }
 
 struct ReconEpi {
-  static constexpr bool kNeedInit = false;
+  static constexpr bool kHasInput = false;
+  static constexpr bool kMirror = false;
+  RCP_D double* cout_mirror(int64_t, int64_t) const { return nullptr; }
   double* out;
   int64_t n;
-  RCP_D double init(int64_t, int64_t) const { return 0.0; }
-  RCP_D void store(int64_t i, int64_t j, double v) const {
-    if (i < n && j < n) out[i * n + j] = v;
-  }
+  RCP_D int map_row(int64_t) const { return 0; }
+  RCP_D int map_col(int64_t) const { return 0; }
+  RCP_D const double* dummy() const { return out; }
+  RCP_D const double* cin(int64_t, int64_t, int, int) const { return nullptr; }
+  // tile element (i, j) of L D L^T, stored row-major
+  RCP_D double* cout(int64_t i, int64_t j) const { return (i < n && j < n) ? out + i * n + j : nullptr; }
 };
 
 }  // namespace
@@ -224,11 +228,11 @@ cudaError_t reconstruct_device(int64_t n, const double* L, const double* dd, con
   OperandDesc b{L, n, n, n};
   ReconEpi epi{out, n};
   RectMap map{tn, 64, 128};
-  size_t smem = sizeof(GemmSmem<64, 128>);
-  cudaError_t e = cudaFuncSetAttribute(dmma_gemm_kernel<64, 128, 1, RectMap, ReconEpi>,
+  size_t smem = gemm_smem_bytes<64, 128, 3>();
+  cudaError_t e = cudaFuncSetAttribute(dmma_gemm_kernel<64, 128, 3, 1, RectMap, ReconEpi>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  dmma_gemm_kernel<64, 128, 1, RectMap, ReconEpi><<<(unsigned)(tm * tn), kGemmThreads, smem, st>>>(a, b, n, map, epi);
+  dmma_gemm_kernel<64, 128, 3, 1, RectMap, ReconEpi><<<(unsigned)(tm * tn), kGemmThreads, smem, st>>>(a, b, n, map, epi);
   return cudaGetLastError();
 }
 
