@@ -32,20 +32,32 @@ struct SchurSmem {
   int colmap[kSchurBN];
 };
 
+// Operand stage loader: thread t copies 16-byte chunks (rows r0 + 16u, columns kk..kk+1) of
+// a ROWS x kBK tile; the per-thread row base is computed once per launch.
 template <int ROWS>
-RCP_D void schur_load_tile(double (*dst)[kBK + kPad], const double* base, int64_t ld, int64_t rows, int64_t row0,
-                           int64_t k0) {
-  constexpr int kChunksPerRow = kBK / 2;
-  constexpr int kChunks = ROWS * kChunksPerRow;
-#pragma unroll
-  for (int c = threadIdx.x; c < kChunks; c += kSchurThreads) {
-    const int r = c / kChunksPerRow;
-    const int kk = (c % kChunksPerRow) * 2;
-    const int64_t gr = row0 + r;
-    const bool ok = gr < rows;
-    cp_async16(&dst[r][kk], ok ? base + gr * ld + k0 + kk : base, ok);
+struct StageLoader {
+  const double* base;  // row (row0 + tid/8) of the operand, column (tid%8)*2
+  int64_t step;        // 16 rows
+  int nvalid;          // rows r0 + 16u valid for u < nvalid
+  int soff;            // smem column offset
+  int srow;            // first smem row
+  RCP_D void init(const double* op, int64_t ld, int64_t rows, int64_t row0) {
+    srow = threadIdx.x / 8;
+    soff = (threadIdx.x % 8) * 2;
+    base = op + (row0 + srow) * ld + soff;
+    step = 16 * ld;
+    const int64_t left = rows - (row0 + srow);
+    nvalid = left <= 0 ? 0 : (left + 15) / 16;
   }
-}
+  RCP_D void load(double (*dst)[kBK + kPad], int64_t k0) const {
+    const double* src = base + k0;
+#pragma unroll
+    for (int u = 0; u < ROWS / 16; ++u) {
+      const bool ok = u < nvalid;
+      cp_async16(&dst[srow + 16 * u][soff], ok ? src + u * step : base, ok);
+    }
+  }
+};
 
 // Lneg, Wg: (rows x tpad) K-contiguous, zero padded in [t, tpad).  A_in / A_out: n x n
 // column-major full symmetric.  phys[j]: physical row (panel-start order) of new logical k+j.
@@ -72,11 +84,15 @@ schur_update_kernel(const double* __restrict__ Lneg, const double* __restrict__ 
   for (int j = tid; j < kSchurBN; j += kSchurThreads) sm.colmap[j] = (n0 + j < mp) ? phys[n0 + j] : 0;
 
   const int KT = Kl / kBK;
+  StageLoader<kSchurBM> la;
+  StageLoader<kSchurBN> lb;
+  la.init(Lneg, tpad, mp, m0);
+  lb.init(Wg, tpad, mp, n0);
 #pragma unroll
   for (int s = 0; s < kSchurStages - 1; ++s) {
     if (s < KT) {
-      schur_load_tile<kSchurBM>(sm.op.a[s], Lneg, tpad, mp, m0, (int64_t)s * kBK);
-      schur_load_tile<kSchurBN>(sm.op.b[s], Wg, tpad, mp, n0, (int64_t)s * kBK);
+      la.load(sm.op.a[s], (int64_t)s * kBK);
+      lb.load(sm.op.b[s], (int64_t)s * kBK);
     }
     cp_async_commit();
   }
@@ -103,23 +119,31 @@ schur_update_kernel(const double* __restrict__ Lneg, const double* __restrict__ 
       const int nk = kt + kSchurStages - 1;
       if (nk < KT) {
         const int st = nk % kSchurStages;
-        schur_load_tile<kSchurBM>(sm.op.a[st], Lneg, tpad, mp, m0, (int64_t)nk * kBK);
-        schur_load_tile<kSchurBN>(sm.op.b[st], Wg, tpad, mp, n0, (int64_t)nk * kBK);
+        la.load(sm.op.a[st], (int64_t)nk * kBK);
+        lb.load(sm.op.b[st], (int64_t)nk * kBK);
       }
       cp_async_commit();
     }
     const int st = kt % kSchurStages;
+    // fragments double-buffered: the loads for k-step kk+4 are issued before the MMAs of kk
+    double af[2][MF], bf[2][NF];
+#pragma unroll
+    for (int i = 0; i < MF; ++i) af[0][i] = sm.op.a[st][wm0 + 8 * i + g][q];
+#pragma unroll
+    for (int j = 0; j < NF; ++j) bf[0][j] = sm.op.b[st][wn0 + 8 * j + g][q];
 #pragma unroll
     for (int kk = 0; kk < kBK; kk += 4) {
-      double af[MF], bf[NF];
+      const int cb = (kk / 4) & 1;
+      if (kk + 4 < kBK) {
 #pragma unroll
-      for (int i = 0; i < MF; ++i) af[i] = sm.op.a[st][wm0 + 8 * i + g][kk + q];
+        for (int i = 0; i < MF; ++i) af[cb ^ 1][i] = sm.op.a[st][wm0 + 8 * i + g][kk + 4 + q];
 #pragma unroll
-      for (int j = 0; j < NF; ++j) bf[j] = sm.op.b[st][wn0 + 8 * j + g][kk + q];
+        for (int j = 0; j < NF; ++j) bf[cb ^ 1][j] = sm.op.b[st][wn0 + 8 * j + g][kk + 4 + q];
+      }
 #pragma unroll
       for (int i = 0; i < MF; ++i)
 #pragma unroll
-        for (int j = 0; j < NF; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+        for (int j = 0; j < NF; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[cb][i], bf[cb][j]);
     }
   }
   cp_async_wait<0>();
@@ -127,11 +151,19 @@ schur_update_kernel(const double* __restrict__ Lneg, const double* __restrict__ 
 
   // ---- epilogue: C-in gather -> smem (cp.async, L2-prefetched), += acc, then store the
   //      lower part column-wise and its mirror row-wise, both coalesced from smem.
-  for (int e = tid; e < kSchurBM * kSchurBN; e += kSchurThreads) {
-    const int j = e / kSchurBM, i = e - j * kSchurBM;
-    const bool ok = (m0 + i < mp) && (n0 + j < mp) && (m0 + i >= n0 + j);
-    const double* src = ok ? ain + (int64_t)sm.rowmap[i] + (int64_t)sm.colmap[j] * n : ain;
-    cp_async8(&sm.c[j][i], src, ok);
+  // thread tid owns tile row i = tid for the gather and the column-wise store
+  static_assert(kSchurThreads == kSchurBM, "one thread per tile row");
+  const int64_t gi_row = m0 + tid;
+  const bool row_ok = gi_row < mp;
+  // j < jmax: element (gi_row, n0 + j) is in range and on/below the diagonal
+  const int64_t jlim = (mp < gi_row + 1 ? mp : gi_row + 1) - n0;
+  const int jmax = (int)(jlim < kSchurBN ? (jlim > 0 ? jlim : 0) : kSchurBN);
+  {
+    const double* src = ain + (int64_t)sm.rowmap[tid];
+    for (int j = 0; j < kSchurBN; ++j) {
+      const bool ok = row_ok && j < jmax;
+      cp_async8(&sm.c[j][tid], ok ? src + (int64_t)sm.colmap[j] * n : ain, ok);
+    }
   }
   cp_async_commit();
   cp_async_wait<0>();
@@ -145,16 +177,18 @@ schur_update_kernel(const double* __restrict__ Lneg, const double* __restrict__ 
       sm.c[lj + 1][li] = __dadd_rn(sm.c[lj + 1][li], acc[i][j][1]);
     }
   __syncthreads();
-  for (int e = tid; e < kSchurBM * kSchurBN; e += kSchurThreads) {
-    const int j = e / kSchurBM, i = e - j * kSchurBM;
-    const int64_t gi = m0 + i, gj = n0 + j;
-    if (gi < mp && gj < mp && gi >= gj) aout[(k + gi) + (k + gj) * n] = sm.c[j][i];
+  if (row_ok) {  // lower part: column j, rows m0..m0+127 (coalesced along the threads)
+    double* dst = aout + (k + gi_row) + (k + n0) * n;
+    for (int j = 0; j < jmax; ++j, dst += n) *dst = sm.c[j][tid];
   }
-  if (m0 + kSchurBM - 1 > n0) {  // mirror of the strictly-lower part (full symmetric storage)
-    for (int e = tid; e < kSchurBM * kSchurBN; e += kSchurThreads) {
-      const int i = e / kSchurBN, j = e - i * kSchurBN;
-      const int64_t gi = m0 + i, gj = n0 + j;
-      if (gi < mp && gj < mp && gi > gj) aout[(k + gj) + (k + gi) * n] = sm.c[j][i];
+  if (m0 + kSchurBM - 1 > n0) {  // mirror of the strictly-lower part: row (k+n0+j), columns k+m0+i
+    const int j = tid & 63, i0 = tid >> 6;
+    const int64_t gj = n0 + j;
+    if (gj < mp) {
+      double* dst = aout + (k + gj) + (k + m0 + i0) * n;
+      const int imax = (int)(mp - m0 < kSchurBM ? mp - m0 : kSchurBM);
+      for (int i = i0; i < imax; i += 2, dst += 2 * n)
+        if (m0 + i > gj) *dst = sm.c[j][i];
     }
   }
 }
