@@ -180,7 +180,7 @@ __global__ void __launch_bounds__(kPanelThreads, 1) panel_kernel(PanelParams p) 
   __shared__ double s_coef, s_gakk, s_akk;
   __shared__ XRec s_win;
   __shared__ unsigned s_qhdr[8], s_dhdr[12];
-  __shared__ int s_wpos, s_qflags, s_hascand;
+  __shared__ int s_wpos, s_qflags, s_hascand, s_wcta;
 
   for (int x = tid; x < Wn; x += nthr) win[x] = x;
   for (int i = tid; i < rcnt; i += nthr) lpos[i] = r0 + i;
@@ -314,101 +314,106 @@ __global__ void __launch_bounds__(kPanelThreads, 1) panel_kernel(PanelParams p) 
       const long long nseq = seq + 1;
       const int pb = static_cast<int>(nseq & 1);
       const unsigned tag = static_cast<unsigned>(nseq);
+      // ---- speculative Householder vector of this CTA's candidate (sketch.py:159-168):
+      //      only the global winner's v is used, so every CTA prepares its own and the
+      //      reducer broadcasts just a small header.
       if (lb.slot >= 0) {
-        u64* dst = p.qcll + ((size_t)pb * G + cta) * 2 * P;
         if (regmode) {
           if (tid == lb.slot) {
 #pragma unroll
             for (int r = 0; r < kRegRows; ++r)
-              if (r >= j && r < PRr) ll_put_d(dst + 2 * r, tag, rg[r]);
+              if (r >= j && r < PRr) vvec[r] = rg[r];
           }
-          for (int r = max(j, PRr) + tid; r < P; r += nthr) ll_put_d(dst + 2 * r, tag, Bs[(r - PRr) * Rs + lb.slot]);
+          for (int r = max(j, PRr) + tid; r < P; r += nthr) vvec[r] = Bs[(r - PRr) * Rs + lb.slot];
         } else {
-          for (int r = j + tid; r < P; r += nthr) ll_put_d(dst + 2 * r, tag, bsm(r, lb.slot));
+          for (int r = j + tid; r < P; r += nthr) vvec[r] = bsm(r, lb.slot);
         }
+      }
+      __syncthreads();
+      if (lb.slot >= 0 && tid < 32) {
+        double xn = sqrt(warp0_sum_sq(vvec, j, P));
+        xn = __shfl_sync(0xffffffffu, xn, 0);
+        if (xn == 0.0) {
+          if (tid == 0) {
+            s_skip = 1;
+            s_coef = 0.0;
+          }
+        } else {
+          if (tid == 0) {
+            const double x0 = vvec[j];
+            vvec[j] = __dadd_rn(x0, copysign(xn, x0 != 0.0 ? x0 : 1.0));
+          }
+          __syncwarp();
+          const double vn2 = warp0_sum_sq(vvec, j, P);
+          if (tid == 0) {
+            s_skip = (vn2 == 0.0) ? 1 : 0;
+            s_coef = (vn2 == 0.0) ? 0.0 : 2.0 / vn2;
+          }
+        }
+      }
+      __syncthreads();
+      if (lb.slot >= 0) {
+        u64* dst = p.qcll + ((size_t)pb * G + cta) * 2 * P;
+        for (int r = j + tid; r < P; r += nthr) ll_put_d(dst + 2 * r, tag, vvec[r]);
       }
       if (tid == 0) {
         u64* q = p.qll + ((size_t)pb * G + cta) * kQWords;
-        ll_put_d(q, tag, lb.slot >= 0 ? lb.key : -1.0);
-        ll_put(q + 2, tag, lb.slot >= 0 ? static_cast<unsigned>(lb.idx) : 0x7fffffffu);
-        ll_put(q + 3, tag, lb.slot >= 0 ? static_cast<unsigned>(r0 + lb.slot) : 0xffffffffu);
+        const bool has = lb.slot >= 0;
+        ll_put_d(q, tag, has ? lb.key : -1.0);
+        ll_put(q + 2, tag, has ? static_cast<unsigned>(lb.idx) : 0x7fffffffu);
+        ll_put(q + 3, tag, has ? static_cast<unsigned>(r0 + lb.slot) : 0xffffffffu);
+        ll_put_d(q + 4, tag, has ? s_coef : 0.0);
+        ll_put(q + 6, tag, has ? static_cast<unsigned>(s_skip) : 1u);
       }
       seq = nseq;
       PROF_END(9);
       PROF_BEGIN();
-      // ---- reducer CTA 0: winner over all records, winner column, Householder vector;
-      //      broadcast as one LL decision (header + v) that every other CTA reads.
-      u64* dec = p.qdll + (size_t)pb * (8 + 2 * (size_t)P);
+      // ---- reducer CTA 0: winner over all records -> small LL header (winner CTA, position,
+      //      column, norm, coef, skip); every CTA then reads v from the winner's buffer.
+      u64* dec = p.qdll + (size_t)pb * 8;
       if (cta == 0) {
-        if (tid == 0) s_qflags = 0;
         double gk = -1.0;
         long long gi = LLONG_MAX;
-        int gs = -1, gcol = -1;
+        int gs = -1;
+        unsigned gw[7] = {0, 0, 0, 0, 0, 0, 0};
         for (int c = tid; c < G; c += nthr) {
-          unsigned w[kQWords];
-          if (!ll_read<kQWords>(p.qll + ((size_t)pb * G + c) * kQWords, tag, w)) {
+          unsigned w[7];
+          if (!ll_read<7>(p.qll + ((size_t)pb * G + c) * kQWords, tag, w)) {
             s_abort = 1;
             continue;
           }
           const double v = ll_d(w[0], w[1]);
           const int ps = static_cast<int>(w[2]);
-          const int cl = static_cast<int>(w[3]);
           if ((v >= 0.0 || v != v) && better(v, ps, gk, gi)) {
             gk = v;
             gi = ps;
             gs = c;
-            gcol = cl;
+#pragma unroll
+            for (int u = 0; u < 7; ++u) gw[u] = w[u];
           }
         }
         BlockBest gb = block_argmax(gk, gi, gs, par);
-        if (gs >= 0 && gs == gb.slot) s_wcol = gcol;  // the thread that loaded the winning record
-        const int wcta = gb.slot;
-        // guard: tsel = max column norm of B[:, k:] (factor.py:576-583 / 405-408)
-        const bool gstop = (j == 0 && p.guard_mode != 0 && gb.key < p.guard_limit);
-        if (!gstop && !s_abort) {
-          const u64* src = p.qcll + ((size_t)pb * G + wcta) * 2 * P;
-          for (int r = j + tid; r < P; r += nthr) {
-            unsigned w[2];
-            if (!ll_read<2>(src + 2 * r, tag, w)) s_abort = 1;
-            vvec[r] = ll_d(w[0], w[1]);
-          }
+        if (gs >= 0 && gs == gb.slot) {  // the thread that loaded the winning record
+          const bool gstop = (j == 0 && p.guard_mode != 0 && gb.key < p.guard_limit);
+          s_wcta = gs;
+          s_wpos = static_cast<int>(gw[2]);
+          s_wcol = static_cast<int>(gw[3]);
+          s_coef = ll_d(gw[4], gw[5]);
+          s_skip = static_cast<int>(gw[6]);
+          s_qflags = (gw[6] ? 1 : 0) | (gstop ? 2 : 0) | (s_abort ? 4 : 0);
+          ll_put(dec + 0, tag, static_cast<unsigned>(gs));
+          ll_put(dec + 1, tag, gw[2]);
+          ll_put(dec + 2, tag, gw[3]);
+          ll_put(dec + 3, tag, gw[4]);
+          ll_put(dec + 4, tag, gw[5]);
+          ll_put(dec + 5, tag, static_cast<unsigned>(s_qflags));
         }
-        __syncthreads();
-        if (!gstop && !s_abort && tid < 32) {
-          // Householder vector (sketch.py:159-168)
-          double xn = sqrt(warp0_sum_sq(vvec, j, P));
-          xn = __shfl_sync(0xffffffffu, xn, 0);
-          if (xn == 0.0) {
-            if (tid == 0) s_skip = 1;
-          } else {
-            if (tid == 0) {
-              const double x0 = vvec[j];
-              vvec[j] = __dadd_rn(x0, copysign(xn, x0 != 0.0 ? x0 : 1.0));
-            }
-            __syncwarp();
-            double vn2 = warp0_sum_sq(vvec, j, P);
-            if (tid == 0) {
-              s_skip = (vn2 == 0.0) ? 1 : 0;
-              s_coef = 2.0 / vn2;
-            }
-          }
-        }
-        __syncthreads();
-        // v first, header last: readers spin only on the header, then find v already visible
-        if (!gstop)
-          for (int r = j + tid; r < P; r += nthr) ll_put_d(dec + 8 + 2 * r, tag, vvec[r]);
-        __syncthreads();
-        if (tid == 0) {
-          s_wpos = static_cast<int>(gb.idx);
-          s_qflags = (s_skip ? 1 : 0) | (gstop ? 2 : 0) | (s_abort ? 4 : 0);
-          ll_put_d(dec + 0, tag, gb.key);
-          ll_put(dec + 2, tag, static_cast<unsigned>(s_wpos));
-          ll_put(dec + 3, tag, static_cast<unsigned>(s_wcol));
-          ll_put(dec + 4, tag, static_cast<unsigned>(s_qflags));
-          ll_put_d(dec + 5, tag, s_coef);
+        if (s_abort && tid == 0) {
+          s_qflags = 4;
+          ll_put(dec + 5, tag, 4u);
         }
       } else {
-        if (tid < 7) {
+        if (tid < 6) {
           unsigned w[1];
           if (!ll_read<1>(dec + tid, tag, w)) {
             s_abort = 1;
@@ -417,25 +422,26 @@ __global__ void __launch_bounds__(kPanelThreads, 1) panel_kernel(PanelParams p) 
           s_qhdr[tid] = w[0];
         }
         __syncthreads();
-        if (!s_abort) {
-          const unsigned fl = s_qhdr[4];
-          if (tid == 0) {
-            s_wpos = static_cast<int>(s_qhdr[2]);
-            s_wcol = static_cast<int>(s_qhdr[3]);
-            s_qflags = static_cast<int>(fl);
-            s_skip = fl & 1;
-            s_coef = ll_d(s_qhdr[5], s_qhdr[6]);
-          }
-          if (!(fl & 2)) {
-            for (int r = j + tid; r < P; r += nthr) {
-              unsigned w[2];
-              if (!ll_read<2>(dec + 8 + 2 * r, tag, w)) s_abort = 1;
-              vvec[r] = ll_d(w[0], w[1]);
-            }
-          }
+        if (tid == 0) {
+          s_wcta = static_cast<int>(s_qhdr[0]);
+          s_wpos = static_cast<int>(s_qhdr[1]);
+          s_wcol = static_cast<int>(s_qhdr[2]);
+          s_coef = ll_d(s_qhdr[3], s_qhdr[4]);
+          s_qflags = static_cast<int>(s_qhdr[5]);
+          s_skip = s_qflags & 1;
+          if (s_abort) s_qflags |= 4;
         }
       }
       par ^= 1;
+      __syncthreads();
+      if (!(s_qflags & 6)) {  // fetch the winner's Householder vector
+        const u64* src = p.qcll + ((size_t)pb * G + s_wcta) * 2 * P;
+        for (int r = j + tid; r < P; r += nthr) {
+          unsigned w[2];
+          if (!ll_read<2>(src + 2 * r, tag, w)) s_abort = 1;
+          vvec[r] = ll_d(w[0], w[1]);
+        }
+      }
       __syncthreads();
       PROF_END(1);
       PROF_BEGIN();

@@ -21,7 +21,7 @@ struct PanelState {
 };
 
 constexpr int kXWords = 16;  // 11 used, padded to 128 B per record
-constexpr int kQWords = 4;
+constexpr int kQWords = 8;  // norm(2) pos col coef(2) skip, padded
 
 // One CTA's contribution to a pivot-search exchange (SBKP step).
 struct XRec {
@@ -71,7 +71,7 @@ struct PanelParams {
   unsigned long long* qll;   // QRCP records  [2][G][kQWords]
   unsigned long long* qcll;  // QRCP candidate columns [2][G][2P]
   unsigned long long* sdll;  // SBKP decision broadcast by the reducer CTA [2][kXWords]
-  unsigned long long* qdll;  // QRCP decision (header + Householder vector) [2][8 + 2P]
+  unsigned long long* qdll;  // QRCP decision header [2][8]
   PanelState* st;
 };
 
