@@ -12,6 +12,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include <vector>
 
 #include "../../include/rcp_b200.h"
@@ -30,7 +31,7 @@ constexpr int kRowsMin = 32;
 size_t align_up(size_t x) { return (x + kAlign - 1) & ~(kAlign - 1); }
 
 struct Layout {
-  size_t A0, A1, Lbuf, W, Lneg, Wg, B0, B1, qscr, Y, omega, phys, lop, pol, perm0, perm1, poso, snap, flags, xrec, qrec,
+  size_t A0, A1, Lbuf, W, Lneg, Wg, B0, B1, qscr, Y, L11, omega, phys, lop, pol, perm0, perm1, poso, snap, flags, xrec, qrec,
       qcol, sdec, qdec, state, scal, total;
   int64_t rows_pad, snap_cap;
   int tpad;
@@ -61,6 +62,7 @@ Layout make_layout(int64_t n, const rcp_config& c) {
   L.B1 = take((size_t)P * n * 8);
   L.qscr = take((size_t)P * n * 8);
   L.Y = take((size_t)P * L.tpad * 8);
+  L.L11 = take((size_t)L.tpad * L.tpad * 8);
   L.omega = take((size_t)P * n * 8);
   L.phys = take((size_t)n * 4);
   L.lop = take((size_t)n * 4);
@@ -162,6 +164,7 @@ int rcp_factor(const rcp_config* cfg, int64_t n, const double* a, int64_t lda, c
   double* Lneg = dptr(Lay.Lneg);
   double* Wg = dptr(Lay.Wg);
   double* Y = dptr(Lay.Y);
+  double* L11c = dptr(Lay.L11);
   double* omg = dptr(Lay.omega);
   int* phys = iptr(Lay.phys);
   int* lop = iptr(Lay.lop);
@@ -367,6 +370,9 @@ int rcp_factor(const rcp_config* cfg, int64_t n, const double* a, int64_t lda, c
       draw_buf.resize((size_t)P * m0);
       if (draw(draw_ctx, P, m0, draw_buf.data()) != 0) return RCP_ERR_NEED_NORMALS;
       RCP_CHECK(cudaMemcpyAsync(omg, draw_buf.data(), sizeof(double) * (size_t)P * m0, cudaMemcpyHostToDevice, st));
+#if !RCP_FULL_STORAGE
+      RCP_LAUNCH(launch_mirror_lower(n, k0, A[cur], st));  // the projection reads full columns
+#endif
       RCP_LAUNCH(launch_sketch_gemm(P, m0, omg, m0, A[cur] + k0 + (int64_t)k0 * n, n, B[cur], k0, st));
       recomputes += 1;
       delta += 1.0 / c.robust_r;
@@ -397,7 +403,7 @@ int rcp_factor(const rcp_config* cfg, int64_t n, const double* a, int64_t lda, c
       return RCP_ERR_WORKSPACE;
     }
     RCP_LAUNCH(launch_gather(n, k0, k_end, t, tpad, ((mp + 127) / 128) * 128, pol, Lbuf, W, permb[pcur],
-                            permb[pcur ^ 1], snap + snap_off, phys, Lneg, Wg, st));
+                            permb[pcur ^ 1], snap + snap_off, phys, Lneg, Wg, L11c, st));
     panels.push_back(PanelRecord{k0, k_end, snap_off});
     snap_off += m0;
     if (mp > 0 && t > 0) {
@@ -407,7 +413,7 @@ int rcp_factor(const rcp_config* cfg, int64_t n, const double* a, int64_t lda, c
       RCP_CHECK(cudaEventRecord(es.b, st));
       schur_flops += (double)t * (double)mp * (double)(mp + 1);
       // sketch correction (factor.py:554-565)
-      RCP_LAUNCH(launch_ysolve(n, P, k0, t, tpad, pol, B[cur], Lbuf, Y, st));
+      RCP_LAUNCH(launch_ysolve(n, P, k0, t, tpad, pol, B[cur], L11c, Y, st));
       RCP_LAUNCH(launch_sketch_correction(P, mp, k_end, Y, tpad, t, Lneg, B[cur], phys, B[cur ^ 1], st));
       cur ^= 1;
     }

@@ -90,7 +90,17 @@ __global__ void gather_kernel(int64_t n, int k0, int k_end, int t, int tpad, int
                               const int* __restrict__ phys_of_log, const double* __restrict__ Lbuf,
                               const double* __restrict__ W, const int* __restrict__ perm_cur,
                               int* __restrict__ perm_next, int* __restrict__ snap,
-                              int* __restrict__ phys, double* __restrict__ Lneg, double* __restrict__ Wg) {
+                              int* __restrict__ phys, double* __restrict__ Lneg, double* __restrict__ Wg,
+                              double* __restrict__ L11) {
+  // compact unit-lower panel block L11 (t x t, row-major ld t) in logical order, for ysolve
+  {
+    const int64_t nthreads = (int64_t)gridDim.x * blockDim.x * blockDim.y;
+    const int64_t tflat = ((int64_t)blockIdx.x * blockDim.y + threadIdx.y) * blockDim.x + threadIdx.x;
+    for (int64_t f = tflat; f < (int64_t)t * t; f += nthreads) {
+      const int a = (int)(f / t), c = (int)(f - (int64_t)a * t);
+      L11[f] = (c < a) ? Lbuf[phys_of_log[k0 + a] + (int64_t)(k0 + c) * n] : 0.0;
+    }
+  }
   const int64_t mp = n - k_end;
   const int64_t m0 = n - k0;
   const int64_t stride = (int64_t)gridDim.x * blockDim.y;
@@ -122,18 +132,13 @@ __global__ void gather_kernel(int64_t n, int k0, int k_end, int t, int tpad, int
 // B1 @ solve_triangular(L11, L21^T, trans='T') (factor.py:554-561).  16 sketch rows per
 // CTA, 16 lanes per row.
 __global__ void ysolve_kernel(int64_t n, int P, int k0, int t, int tpad, const int* __restrict__ phys_of_log,
-                              const double* __restrict__ Bin, const double* __restrict__ Lbuf,
+                              const double* __restrict__ Bin, const double* __restrict__ L11g,
                               double* __restrict__ Y) {
   extern __shared__ double sm[];
   double* L11 = sm;                 // [t][t]
   double* yv = sm + (size_t)t * t;  // [16][tpad]
   const int tid = threadIdx.x;
-  for (int f = tid; f < t * t; f += blockDim.x) {
-    int a = f / t, c = f - a * t;
-    double v = 0.0;
-    if (c < a) v = Lbuf[phys_of_log[k0 + a] + (int64_t)(k0 + c) * n];
-    L11[f] = v;
-  }
+  for (int f = tid; f < t * t; f += blockDim.x) L11[f] = L11g[f];  // compact copy made by gather_kernel
   const int rr = tid >> 4, l16 = tid & 15;
   const int r = blockIdx.x * 16 + rr;
   for (int a = l16; a < tpad; a += 16) yv[rr * tpad + a] = 0.0;
@@ -245,21 +250,21 @@ cudaError_t launch_sketch_norm_max(const double* B, int P, int64_t ncols, double
 
 cudaError_t launch_gather(int64_t n, int k0, int k_end, int t, int tpad, int64_t rows_pad, const int* phys_of_log,
                           const double* Lbuf, const double* W, const int* perm_cur, int* perm_next, int* snap,
-                          int* phys, double* Lneg, double* Wg, cudaStream_t st) {
+                          int* phys, double* Lneg, double* Wg, double* L11, cudaStream_t st) {
   dim3 block(32, 8);
   int64_t rows = rows_pad > (n - k0) ? rows_pad : (n - k0);
   unsigned grid = (unsigned)std::min<int64_t>((rows + 7) / 8, 148 * 16);
   gather_kernel<<<grid, block, 0, st>>>(n, k0, k_end, t, tpad, rows_pad, phys_of_log, Lbuf, W, perm_cur,
-                                        perm_next, snap, phys, Lneg, Wg);
+                                        perm_next, snap, phys, Lneg, Wg, L11);
   return cudaGetLastError();
 }
 
 cudaError_t launch_ysolve(int64_t n, int P, int k0, int t, int tpad, const int* phys_of_log, const double* Bin,
-                          const double* Lbuf, double* Y, cudaStream_t st) {
+                          const double* L11, double* Y, cudaStream_t st) {
   size_t smem = sizeof(double) * ((size_t)t * t + 16 * (size_t)tpad);
   cudaError_t e = cudaFuncSetAttribute(ysolve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  ysolve_kernel<<<(unsigned)((P + 15) / 16), 256, smem, st>>>(n, P, k0, t, tpad, phys_of_log, Bin, Lbuf, Y);
+  ysolve_kernel<<<(unsigned)((P + 15) / 16), 256, smem, st>>>(n, P, k0, t, tpad, phys_of_log, Bin, L11, Y);
   return cudaGetLastError();
 }
 

@@ -10,9 +10,9 @@ cudaError_t launch_validate_copy(const double* a, int64_t lda, int64_t n, double
 cudaError_t launch_sketch_norm_max(const double* B, int P, int64_t ncols, double* out, cudaStream_t st);
 cudaError_t launch_gather(int64_t n, int k0, int k_end, int t, int tpad, int64_t rows_pad, const int* phys_of_log,
                           const double* Lbuf, const double* W, const int* perm_cur, int* perm_next, int* snap,
-                          int* phys, double* Lneg, double* Wg, cudaStream_t st);
+                          int* phys, double* Lneg, double* Wg, double* L11, cudaStream_t st);
 cudaError_t launch_ysolve(int64_t n, int P, int k0, int t, int tpad, const int* phys_of_log, const double* Bin,
-                          const double* Lbuf, double* Y, cudaStream_t st);
+                          const double* L11, double* Y, cudaStream_t st);
 cudaError_t launch_assemble_panel(int64_t n, int k0, int k_end, const int* snap, int* pos_of_orig,
                                   const int64_t* perm, const double* Lbuf, double* L, double* maxmult,
                                   cudaStream_t st);

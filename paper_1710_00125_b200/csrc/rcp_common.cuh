@@ -25,9 +25,20 @@ RCP_D void st_release(long long* p, long long v) {
 }
 
 // ---------------------------------------------------------------- symmetric access
-// Trailing blocks are stored in FULL symmetric form (column-major, ld = n): element (i, j)
-// is read from column j, so a pivot column is one contiguous read.
-RCP_D double sym_at(const double* a, int64_t ld, int64_t i, int64_t j) { return a[i + j * ld]; }
+// Trailing blocks are column-major (ld = n).  With RCP_FULL_STORAGE both triangles are kept
+// (a pivot column is one contiguous read; the Schur update also writes the mirror); otherwise
+// only the lower triangle is valid and (i, j), i < j, is read from (j, i).
+#ifndef RCP_FULL_STORAGE
+#define RCP_FULL_STORAGE 1
+#endif
+RCP_HD int64_t sym_index(int64_t ld, int64_t i, int64_t j) {
+#if RCP_FULL_STORAGE
+  return i + j * ld;
+#else
+  return (i >= j) ? i + j * ld : j + i * ld;
+#endif
+}
+RCP_D double sym_at(const double* a, int64_t ld, int64_t i, int64_t j) { return a[sym_index(ld, i, j)]; }
 
 // ---------------------------------------------------------------- pivot-column dot
 // Dot product of row i of the panel L (Lrow(s)) with the pivot's W row w[s], s < t,
@@ -107,6 +118,19 @@ RCP_D void cp_async16(void* smem, const void* gmem, bool pred) {
   int n = pred ? 16 : 0;
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(n));
 }
+// Same with an L2 cache-policy hint (e.g. evict_first for streamed data).
+RCP_D void cp_async8_hint(void* smem, const void* gmem, bool pred, unsigned long long policy) {
+  unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  int n = pred ? 8 : 0;
+  asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 8, %2, %3;\n" ::"r"(s), "l"(gmem), "r"(n),
+               "l"(policy));
+}
+RCP_D unsigned long long policy_evict_first() {
+  unsigned long long p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+RCP_D void st_stream(double* p, double v) { __stcs(p, v); }
 RCP_D void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int N>
 RCP_D void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
