@@ -45,7 +45,8 @@ def needs_build() -> bool:
 def build(force: bool = False, verbose: bool = False) -> Path:
     if not force and not needs_build():
         return OUT
-    cmd = [_nvcc(), *NVCC_FLAGS, "-o", str(OUT) + ".tmp", *map(str, sources())]
+    extra = ["-DRCP_PANEL_PROF=1"] if os.environ.get("RCP_PANEL_PROF") == "1" else []
+    cmd = [_nvcc(), *NVCC_FLAGS, *extra, "-o", str(OUT) + ".tmp", *map(str, sources())]
     if verbose:
         print(" ".join(cmd), flush=True)
     subprocess.run(cmd, check=True, cwd=str(ROOT))
