@@ -84,6 +84,8 @@ def load(path: str | os.PathLike | None = None):
     global _lib
     if _lib is not None and path is None:
         return _lib
+    if path is None and os.environ.get("RCP_B200_LIB"):
+        path = os.environ["RCP_B200_LIB"]  # alternative build (experiments)
     p = Path(path) if path is not None else LIB_PATH
     if not p.exists():
         raise NativeUnavailable(
@@ -107,6 +109,5 @@ def load(path: str | os.PathLike | None = None):
     lib.rcp_reconstruct.restype = ctypes.c_int
     lib.rcp_version.argtypes = []
     lib.rcp_version.restype = ctypes.c_char_p
-    if path is None:
-        _lib = lib
+    _lib = lib
     return lib

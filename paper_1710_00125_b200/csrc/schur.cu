@@ -3,6 +3,8 @@
 #include "gemm_dmma.cuh"
 #include "misc.cuh"
 #include "schur_kernel.cuh"
+#include "schur_ws.cuh"
+#include <algorithm>
 
 namespace rcp {
 
@@ -51,6 +53,8 @@ cudaError_t gemm_init_attributes() {
   e = cudaFuncSetAttribute(schur_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)schur_smem_bytes());
   if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(schur_ws_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)schur_ws_smem_bytes());
+  if (e != cudaSuccess) return e;
   e = cudaFuncSetAttribute(dmma_gemm_kernel<64, 128, kRectStages, 2, RectMap, SketchEpi>,
                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gemm_smem_bytes<64, 128, kRectStages>());
   if (e != cudaSuccess) return e;
@@ -66,10 +70,14 @@ cudaError_t launch_schur_update(int64_t n, int64_t k, int64_t mp, const double* 
                                 int K, const double* A_in, const int* phys, double* A_out, cudaStream_t st) {
   if (mp <= 0 || K <= 0) return cudaSuccess;
   const int64_t nbi = (mp + kSchurBM - 1) / kSchurBM;
-  const int64_t tiles = nbi * (nbi + 1);  // row block I has 2I+2 column blocks of 64
+  const long long tiles = nbi * (nbi + 1);  // row block I has 2I+2 column blocks of 64
   const int Kl = ((K + kBK - 1) / kBK) * kBK;  // operands are zero padded to tpad along K
-  schur_update_kernel<<<(unsigned)tiles, kSchurThreads, schur_smem_bytes(), st>>>(Lneg, Wg, tpad, Kl, A_in, A_out,
-                                                                                 phys, n, k, mp);
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const long long grid = std::min<long long>(tiles, sms);
+  schur_ws_kernel<<<(unsigned)grid, ws::kThreads, schur_ws_smem_bytes(), st>>>(Lneg, Wg, tpad, Kl, A_in, A_out, phys,
+                                                                               n, k, mp, tiles);
   return cudaGetLastError();
 }
 
