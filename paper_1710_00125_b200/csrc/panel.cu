@@ -728,6 +728,12 @@ __global__ void __launch_bounds__(kPanelThreads, 1) panel_kernel(PanelParams p) 
         ll_put(dec + 9, tag, static_cast<unsigned>(s_win.phys));
         ll_put(dec + 10, tag, (s_hascand ? 1u : 0u) | (s_gerr ? 2u : 0u) | (s_abort ? 4u : 0u));
       }
+      // The decision will need the partner column r unless the 1x1 test passes: start pulling it
+      // into L2 now, while the workers are still waiting for this broadcast.
+      if (s_hascand && !(fabs(s_gakk) >= __dmul_rn(alpha, s_win.key))) {
+        const double* colr = p.A + (int64_t)(k0 + s_win.phys) * n;
+        for (int64_t r = k0 + 16 * tid; r < n; r += 16 * nthr) asm volatile("prefetch.global.L2 [%0];" ::"l"(colr + r));
+      }
     } else {
       if (tid < 11) {
         unsigned w[1];

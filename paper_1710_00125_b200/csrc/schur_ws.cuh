@@ -27,7 +27,11 @@ namespace ws {
 #endif
 constexpr int BM = 128, BN = 64, STAGES = RCP_WS_STAGES;
 constexpr int NBUF = RCP_WS_NBUF;  // C tile buffers (1: the epilogue drains tile t during mainloop t+1)
-constexpr int kThreads = 256;
+#ifndef RCP_WS_MMA_WARPS
+#define RCP_WS_MMA_WARPS 4
+#endif
+constexpr int kMmaWarps = RCP_WS_MMA_WARPS;  // 4: 64x32 warp tiles, 8: 32x32 warp tiles
+constexpr int kThreads = 32 * kMmaWarps + 128;
 constexpr int kProdThreads = 64, kEpiThreads = 64;
 constexpr int kCStride = BM + 1;
 
@@ -104,20 +108,21 @@ schur_ws_kernel(const double* __restrict__ Lneg, const double* __restrict__ Wg, 
   if (tid == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&sm.full[s], kProdThreads);
-      mbar_init(&sm.empty[s], 4);
+      mbar_init(&sm.empty[s], kMmaWarps);
     }
     for (int b = 0; b < NBUF; ++b) {
       mbar_init(&sm.cin[b], kEpiThreads);
-      mbar_init(&sm.accd[b], 4);
+      mbar_init(&sm.accd[b], kMmaWarps);
     }
   }
   __syncthreads();
 
-  if (warp < 4) {
+  if (warp < kMmaWarps) {
     // ======================= MMA warps =======================
     const int g = lane >> 2, q = lane & 3;
-    const int wm0 = (warp >> 1) * 64, wn0 = (warp & 1) * 32;
-    constexpr int MF = 8, NF = 4;
+    constexpr int WM = BM / (kMmaWarps / 2);  // warps tile 2 (N) x kMmaWarps/2 (M)
+    const int wm0 = (warp >> 1) * WM, wn0 = (warp & 1) * 32;
+    constexpr int MF = WM / 8, NF = 4;
     unsigned stage = 0, sphase = 0;
     int it = 0;
     for (long long x = blockIdx.x; x < tiles; x += gridDim.x, ++it) {
@@ -168,9 +173,9 @@ schur_ws_kernel(const double* __restrict__ Lneg, const double* __restrict__ Wg, 
       __syncwarp();
       if (lane == 0) mbar_arrive(&sm.accd[b]);
     }
-  } else if (warp < 6) {
+  } else if (warp < kMmaWarps + 2) {
     // ======================= producer warps =======================
-    const int pt = tid - 128;  // 0..63
+    const int pt = tid - 32 * kMmaWarps;  // 0..63
     const int srow = pt / 8, soff = (pt % 8) * 2;
     unsigned stage = 0, ephase = 1;  // fresh "empty" barriers count as released
     for (long long x = blockIdx.x; x < tiles; x += gridDim.x) {
@@ -201,7 +206,7 @@ schur_ws_kernel(const double* __restrict__ Lneg, const double* __restrict__ Wg, 
     }
   } else {
     // ======================= epilogue warps =======================
-    const int et = tid - 192;  // 0..63
+    const int et = tid - 32 * kMmaWarps - 64;  // 0..63
     auto gather = [&](long long x, int b) {
       int64_t m0, n0;
       tile_of(x, m0, n0);
