@@ -8,8 +8,8 @@
  * maintainer adds to `randldl`):
  *
  *   rcp_factor          <- randldl.factor / factor_robust   (factor.py:637-660)
- *                          with strategy="rcp", q in {b} (q == 1 reported as
- *                          RCP_ERR_UNSUPPORTED in this build)
+ *                          with strategy="rcp", q = b (panel QRCP preselect) or
+ *                          q = 1 (per-step sketch pivot + per-step sketch downdate)
  *   rcp_solve           <- randldl.solve / solve_many        (solve.py:79-107)
  *   rcp_reconstruct     <- randldl.reconstruct               (factor.py:663-665)
  *   rcp_workspace_bytes    workspace query (no reference counterpart)
@@ -52,7 +52,7 @@ enum {
   RCP_ERR_NEED_NORMALS = 5,     /* guard recompute needed but no `draw` callback                  */
   RCP_ERR_CUDA = 6,             /* CUDA runtime failure; message in rcp_stats                     */
   RCP_ERR_WORKSPACE = 7,        /* workspace smaller than rcp_workspace_bytes()                   */
-  RCP_ERR_UNSUPPORTED = 8       /* e.g. q == 1 mode in this build                                 */
+  RCP_ERR_UNSUPPORTED = 8       /* configuration beyond the on-chip panel capacity (message says) */
 };
 
 /* NumericalError kinds (factor.py:214, 222, 456, 464-466). */

@@ -145,10 +145,6 @@ int rcp_factor(const rcp_config* cfg, int64_t n, const double* a, int64_t lda, c
   if (vc != RCP_OK) return vc;
   if (lda < n || !a || !omega_dev || !perm || !Lout || !d_diag || !d_off || !pattern) return RCP_ERR_INVALID_ARG;
   const rcp_config c = *cfg;
-  if (c.q == 1) {
-    if (stats) snprintf(stats->message, sizeof(stats->message), "q == 1 (per-step sketch pivoting) not built");
-    return RCP_ERR_UNSUPPORTED;
-  }
   const Layout Lay = make_layout(n, c);
   if (!workspace || workspace_bytes < Lay.total) return RCP_ERR_WORKSPACE;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(cuda_stream);
@@ -259,7 +255,7 @@ int rcp_factor(const rcp_config* cfg, int64_t n, const double* a, int64_t lda, c
   }
   RCP_LAUNCH(launch_iota(n, permb[0], st));
 
-  int cur = 0;       // A / B buffer holding the current trailing block
+  int curA = 0, curB = 0;  // ping-pong buffers holding the current trailing block / sketch
   int pcur = 0;      // perm buffer for the current order
   int64_t k = 0;
   int64_t snap_off = 0;
@@ -304,8 +300,11 @@ int rcp_factor(const rcp_config* cfg, int64_t n, const double* a, int64_t lda, c
       }
     }
     long long ls = (avail - 24LL * R - 64) / (8LL * R);
-    int Ls = (int)std::max(0LL, std::min<long long>(Wn, ls));
-    size_t need_s = (size_t)8 * Ls * R + 24 * (size_t)R + 64;
+    int Ls = 0;
+    const bool q1 = (c.q == 1);
+    if (q1) ls = (avail - 24LL * R - 8LL * P * R - 8LL * P - 128) / (8LL * R);
+    Ls = (int)std::max(0LL, std::min<long long>(Wn, ls));
+    size_t need_s = (size_t)8 * Ls * R + 24 * (size_t)R + (q1 ? (size_t)8 * P * R + 8 * (size_t)P : 0) + 128;
     size_t smem = fixed + std::max(need_q, need_s);
 
     PanelParams prm{};
@@ -314,7 +313,7 @@ int rcp_factor(const rcp_config* cfg, int64_t n, const double* a, int64_t lda, c
     prm.width = width;
     prm.P = P;
     prm.qn = qn;
-    prm.guard_mode = (armed && qn > 0) ? 1 : 0;
+    prm.guard_mode = (armed && (qn > 0 || q1)) ? 1 : 0;
     prm.guard_limit = thr * beta;
     prm.alpha = std::sqrt(2.0) / 2.0;
     prm.G = G;
@@ -323,8 +322,10 @@ int rcp_factor(const rcp_config* cfg, int64_t n, const double* a, int64_t lda, c
     prm.Ls = Ls;
     prm.Wn = Wn;
     prm.qmode = qmode;
-    prm.A = A[cur];
-    prm.B = B[cur];
+    prm.A = A[curA];
+    prm.B = B[curB];
+    prm.Bout = B[curB ^ 1];
+    prm.q1 = q1 ? 1 : 0;
     prm.qscr = dptr(Lay.qscr);
     prm.Lbuf = Lbuf;
     prm.W = W;
@@ -371,9 +372,9 @@ int rcp_factor(const rcp_config* cfg, int64_t n, const double* a, int64_t lda, c
       if (draw(draw_ctx, P, m0, draw_buf.data()) != 0) return RCP_ERR_NEED_NORMALS;
       RCP_CHECK(cudaMemcpyAsync(omg, draw_buf.data(), sizeof(double) * (size_t)P * m0, cudaMemcpyHostToDevice, st));
 #if !RCP_FULL_STORAGE
-      RCP_LAUNCH(launch_mirror_lower(n, k0, A[cur], st));  // the projection reads full columns
+      RCP_LAUNCH(launch_mirror_lower(n, k0, A[curA], st));  // the projection reads full columns
 #endif
-      RCP_LAUNCH(launch_sketch_gemm(P, m0, omg, m0, A[cur] + k0 + (int64_t)k0 * n, n, B[cur], k0, st));
+      RCP_LAUNCH(launch_sketch_gemm(P, m0, omg, m0, A[curA] + k0 + (int64_t)k0 * n, n, B[curB], k0, st));
       recomputes += 1;
       delta += 1.0 / c.robust_r;
       thr = std::pow(DBL_EPSILON, delta);
@@ -409,13 +410,16 @@ int rcp_factor(const rcp_config* cfg, int64_t n, const double* a, int64_t lda, c
     if (mp > 0 && t > 0) {
       EventPair& es = new_pair(ev_schur);
       RCP_CHECK(cudaEventRecord(es.a, st));
-      RCP_LAUNCH(launch_schur_update(n, k_end, mp, Lneg, Wg, tpad, t, A[cur], phys, A[cur ^ 1], st));
+      RCP_LAUNCH(launch_schur_update(n, k_end, mp, Lneg, Wg, tpad, t, A[curA], phys, A[curA ^ 1], st));
       RCP_CHECK(cudaEventRecord(es.b, st));
       schur_flops += (double)t * (double)mp * (double)(mp + 1);
-      // sketch correction (factor.py:554-565)
-      RCP_LAUNCH(launch_ysolve(n, P, k0, t, tpad, pol, B[cur], L11c, Y, st));
-      RCP_LAUNCH(launch_sketch_correction(P, mp, k_end, Y, tpad, t, Lneg, B[cur], phys, B[cur ^ 1], st));
-      cur ^= 1;
+      curA ^= 1;
+      if (!q1) {
+        // sketch correction once per panel (factor.py:554-565)
+        RCP_LAUNCH(launch_ysolve(n, P, k0, t, tpad, pol, B[curB], L11c, Y, st));
+        RCP_LAUNCH(launch_sketch_correction(P, mp, k_end, Y, tpad, t, Lneg, B[curB], phys, B[curB ^ 1], st));
+      }
+      curB ^= 1;  // q = 1: the panel kernel already wrote the per-step-updated sketch
     }
     pcur ^= 1;
     k = k_end;

@@ -183,7 +183,7 @@ __global__ void __launch_bounds__(kPanelThreads, 1) panel_kernel(PanelParams p) 
   __shared__ double s_coef, s_gakk, s_akk;
   __shared__ XRec s_win;
   __shared__ unsigned s_qhdr[8], s_dhdr[12];
-  __shared__ int s_wpos, s_qflags, s_hascand, s_wcta;
+  __shared__ int s_wpos, s_qflags, s_hascand, s_wcta, s_gs1, s_gs2;
 
   for (int x = tid; x < Wn; x += nthr) win[x] = x;
   for (int i = tid; i < rcnt; i += nthr) lpos[i] = r0 + i;
@@ -620,6 +620,11 @@ __global__ void __launch_bounds__(kPanelThreads, 1) panel_kernel(PanelParams p) 
   double* ck = Lsm + (size_t)Ls * R;
   double* cr = ck + R;
   double* dg = cr + R;
+  // q = 1 mode (factor.py:607-620, 486-489): own sketch columns [P][R] + the two pivot columns
+  double* Bq = dg + R;
+  double* skr = Bq + (size_t)P * R;
+  double* skp0 = vvec;
+  const bool q1 = p.q1 != 0;
   const double* A = p.A;
   const double alpha = p.alpha;
   const int width = p.width;
@@ -628,11 +633,154 @@ __global__ void __launch_bounds__(kPanelThreads, 1) panel_kernel(PanelParams p) 
     int64_t x = k0 + r0 + i;
     dg[i] = A[x * (n + 1)];
   }
+  if (q1)
+    for (int f = tid; f < P * rcnt; f += nthr) {
+      const int i = f / P, r = f - i * P;
+      Bq[r * R + i] = p.B[(size_t)(k0 + r0 + i) * P + r];
+    }
   int pk = win[0];
+  bool first_guard = true;
   __syncthreads();
 
   int t = 0;
   while (t < width && k0 + t < n) {
+    if (q1) {
+      // ---- q = 1: sketch column argmax (factor.py:607-620), then swap(k, k + jl)
+      if (n - (k0 + t) > 1) {
+        double bk1 = -1.0;
+        long long bi1 = LLONG_MAX;
+        int bs1 = -1;
+        for (int i = tid; i < rcnt; i += nthr) {
+          const int lp = lpos[i];
+          if (lp < t) continue;
+          double am = 0.0;
+          for (int r = 0; r < P; ++r) am = fmax(am, fabs(Bq[r * R + i]));
+          double nv = 0.0;
+          if (am > 0.0) {
+            double ss = 0.0;
+            for (int r = 0; r < P; ++r) {
+              const double x = fabs(Bq[r * R + i]) / am;
+              ss = __fma_rn(x, x, ss);
+            }
+            nv = am * sqrt(ss);
+          }
+          if (better(nv, lp, bk1, bi1)) {
+            bk1 = nv;
+            bi1 = lp;
+            bs1 = i;
+          }
+        }
+        BlockBest lb1 = block_argmax(bk1, bi1, bs1, par);
+        par ^= 1;
+        const long long nseq1 = seq + 1;
+        const int pb1 = static_cast<int>(nseq1 & 1);
+        const unsigned tag1 = static_cast<unsigned>(nseq1);
+        if (lb1.slot >= 0) {
+          u64* dst = p.qcll + ((size_t)pb1 * G + cta) * 2 * P;
+          for (int r = tid; r < P; r += nthr) ll_put_d(dst + 2 * r, tag1, Bq[r * R + lb1.slot]);
+        }
+        if (tid == 0) {
+          u64* q = p.qll + ((size_t)pb1 * G + cta) * kQWords;
+          const bool has = lb1.slot >= 0;
+          ll_put_d(q, tag1, has ? lb1.key : -1.0);
+          ll_put(q + 2, tag1, has ? static_cast<unsigned>(lb1.idx) : 0x7fffffffu);
+          ll_put(q + 3, tag1, has ? static_cast<unsigned>(r0 + lb1.slot) : 0xffffffffu);
+        }
+        seq = nseq1;
+        u64* dec1 = p.qdll + (size_t)pb1 * 8;
+        if (cta == 0) {
+          double gk = -1.0;
+          long long gi = LLONG_MAX;
+          int gs = -1, gph = -1;
+          for (int c = tid; c < G; c += nthr) {
+            unsigned w[4];
+            if (!ll_read<4>(p.qll + ((size_t)pb1 * G + c) * kQWords, tag1, w)) {
+              s_abort = 1;
+              continue;
+            }
+            const double v = ll_d(w[0], w[1]);
+            const int ps = static_cast<int>(w[2]);
+            if ((v >= 0.0 || v != v) && better(v, ps, gk, gi)) {
+              gk = v;
+              gi = ps;
+              gs = c;
+              gph = static_cast<int>(w[3]);
+            }
+          }
+          BlockBest gb = block_argmax(gk, gi, gs, par);
+          if (gs >= 0 && gs == gb.slot) {
+            // guard (factor.py:613-619): trip -> defer (t > 0) or recompute (t == 0); after a
+            // recompute the first check decides "stop"
+            unsigned fl = 0;
+            if (p.guard_mode != 0 && gb.key < p.guard_limit) {
+              if (p.guard_mode == 2 && first_guard) fl = 2;  // stop
+              else if (t > 0) fl = 8;                        // defer
+              else fl = 1;                                   // trip: recompute
+            }
+            s_qflags = fl | (s_abort ? 4u : 0u);
+            s_wpos = static_cast<int>(gb.idx);
+            s_wcol = gph;
+            s_gs1 = gs;
+            ll_put(dec1 + 0, tag1, static_cast<unsigned>(gs));
+            ll_put(dec1 + 1, tag1, static_cast<unsigned>(s_wpos));
+            ll_put(dec1 + 2, tag1, static_cast<unsigned>(gph));
+            ll_put(dec1 + 3, tag1, static_cast<unsigned>(s_qflags));
+          }
+        } else {
+          if (tid < 4) {
+            unsigned w[1];
+            if (!ll_read<1>(dec1 + tid, tag1, w)) {
+              s_abort = 1;
+              w[0] = 4;
+            }
+            s_qhdr[tid] = w[0];
+          }
+          __syncthreads();
+          if (tid == 0) {
+            s_gs1 = static_cast<int>(s_qhdr[0]);
+            s_wpos = static_cast<int>(s_qhdr[1]);
+            s_wcol = static_cast<int>(s_qhdr[2]);
+            s_qflags = static_cast<int>(s_qhdr[3]) | (s_abort ? 4 : 0);
+          }
+        }
+        par ^= 1;
+        __syncthreads();
+        first_guard = false;
+        if (s_abort || (s_qflags & 4)) {
+          if (tid == 0) atomicExch(&p.st->status, 99);
+          break;
+        }
+        if (s_qflags & 8) break;  // defer: flush this panel, retest at t == 0
+        if (s_qflags & 3) {
+          if (cta == 0 && tid == 0) p.st->status = (s_qflags & 2) ? 2 : 1;
+          s_abort = 2;
+          break;
+        }
+        // pivot sketch column (for the per-step downdate) from the winner's LL buffer
+        {
+          const u64* src = p.qcll + ((size_t)pb1 * G + s_gs1) * 2 * P;
+          for (int r = tid; r < P; r += nthr) {
+            unsigned w[2];
+            ll_read<2>(src + 2 * r, tag1, w);
+            skp0[r] = ll_d(w[0], w[1]);
+          }
+        }
+        // swap(k, k + jl) as bookkeeping
+        const int jl = s_wpos, pw = s_wcol;
+        if (tid == 0 && jl != t) {
+          const int pold = win[t];
+          win[t] = pw;
+          if (jl < Wn) win[jl] = pold;
+          if (pw >= r0 && pw < r0 + rcnt) lpos[pw - r0] = t;
+          if (pold >= r0 && pold < r0 + rcnt) lpos[pold - r0] = jl;
+        }
+        __syncthreads();
+      }
+      // pivot and its W row: all entries were written before the exchange(s) of this step
+      pk = win[t];
+      for (int s3 = tid; s3 < t; s3 += nthr) wrow[s3] = __ldcg(p.W + (k0 + pk) + (int64_t)s3 * n);
+      __syncthreads();
+    }
     // ---- phase A: pivot column (rows of the active block owned here)
     PROF_BEGIN();
     if (tid == 0) {
@@ -668,6 +816,10 @@ __global__ void __launch_bounds__(kPanelThreads, 1) panel_kernel(PanelParams p) 
     const long long nseq = seq + 1;
     const int pb = static_cast<int>(nseq & 1);
     const unsigned tag = static_cast<unsigned>(nseq);
+    if (q1 && lb.slot >= 0) {
+      u64* dst = p.qcll + ((size_t)pb * G + cta) * 2 * P;
+      for (int r = tid; r < P; r += nthr) ll_put_d(dst + 2 * r, tag, Bq[r * R + lb.slot]);
+    }
     if (tid == 0) {
       u64* q = p.xll + ((size_t)pb * G + cta) * kXWords;
       const bool has = lb.slot >= 0;
@@ -727,6 +879,8 @@ __global__ void __launch_bounds__(kPanelThreads, 1) panel_kernel(PanelParams p) 
         ll_put(dec + 8, tag, static_cast<unsigned>(s_win.lidx));
         ll_put(dec + 9, tag, static_cast<unsigned>(s_win.phys));
         ll_put(dec + 10, tag, (s_hascand ? 1u : 0u) | (s_gerr ? 2u : 0u) | (s_abort ? 4u : 0u));
+        ll_put(dec + 11, tag, static_cast<unsigned>(gb.slot));
+        s_gs2 = gb.slot;
       }
       // The decision will need the partner column r unless the 1x1 test passes: start pulling it
       // into L2 now, while the workers are still waiting for this broadcast.
@@ -735,7 +889,7 @@ __global__ void __launch_bounds__(kPanelThreads, 1) panel_kernel(PanelParams p) 
         for (int64_t r = k0 + 16 * tid; r < n; r += 16 * nthr) asm volatile("prefetch.global.L2 [%0];" ::"l"(colr + r));
       }
     } else {
-      if (tid < 11) {
+      if (tid < 12) {
         unsigned w[1];
         if (!ll_read<1>(dec + tid, tag, w)) {
           s_abort = 1;
@@ -752,6 +906,7 @@ __global__ void __launch_bounds__(kPanelThreads, 1) panel_kernel(PanelParams p) 
         s_win.lidx = static_cast<int>(s_dhdr[8]);
         s_win.phys = static_cast<int>(s_dhdr[9]);
         s_hascand = s_dhdr[10] & 1u;
+        s_gs2 = static_cast<int>(s_dhdr[11]);
         if (s_dhdr[10] & 2u) s_gerr = 1;
         if (s_dhdr[10] & 4u) s_abort = 1;
       }
@@ -820,6 +975,14 @@ __global__ void __launch_bounds__(kPanelThreads, 1) panel_kernel(PanelParams p) 
     const int64_t kglob = k0 + t;
     if (kind >= 2) {
       for (int s2 = tid; s2 < t; s2 += nthr) wrrow[s2] = __ldcg(p.W + (k0 + pr) + (int64_t)s2 * n);
+      if (q1) {  // partner's sketch column (per-step downdate, factor.py:486-489)
+        const u64* src = p.qcll + ((size_t)pb * G + s_gs2) * 2 * P;
+        for (int r = tid; r < P; r += nthr) {
+          unsigned w[2];
+          ll_read<2>(src + 2 * r, tag, w);
+          skr[r] = ll_d(w[0], w[1]);
+        }
+      }
       const double av0 = (tid < rcnt) ? sym_at(A, n, k0 + r0 + tid, k0 + pr) : 0.0;
       __syncthreads();  // wrrow ready, swaps (lpos) visible
       for (int i = tid; i < rcnt; i += nthr) {
@@ -875,6 +1038,8 @@ __global__ void __launch_bounds__(kPanelThreads, 1) panel_kernel(PanelParams p) 
           p.Lbuf[row + kglob * n] = l;
           if (t < Ls) Lsm[(size_t)t * R + i] = l;
           dg[i] = __fma_rn(-l, c, dg[i]);
+          if (q1)
+            for (int r = 0; r < P; ++r) Bq[r * R + i] = __dsub_rn(Bq[r * R + i], __dmul_rn(skp0[r], l));
         }
       } else if (kind == 2) {
         const double c = cr[i];
@@ -885,6 +1050,8 @@ __global__ void __launch_bounds__(kPanelThreads, 1) panel_kernel(PanelParams p) 
           p.Lbuf[row + kglob * n] = l;
           if (t < Ls) Lsm[(size_t)t * R + i] = l;
           dg[i] = __fma_rn(-l, c, dg[i]);
+          if (q1)
+            for (int r = 0; r < P; ++r) Bq[r * R + i] = __dsub_rn(Bq[r * R + i], __dmul_rn(skr[r], l));
         }
       } else {
         const double c0 = ck[i], c1 = cr[i];
@@ -899,6 +1066,9 @@ __global__ void __launch_bounds__(kPanelThreads, 1) panel_kernel(PanelParams p) 
           if (t < Ls) Lsm[(size_t)t * R + i] = l1;
           if (t + 1 < Ls) Lsm[(size_t)(t + 1) * R + i] = l2;
           dg[i] = __fma_rn(-l2, c1, __fma_rn(-l1, c0, dg[i]));
+          if (q1)
+            for (int r = 0; r < P; ++r)
+              Bq[r * R + i] = __dsub_rn(Bq[r * R + i], __dadd_rn(__dmul_rn(skp0[r], l1), __dmul_rn(skr[r], l2)));
         } else if (lp == t + 1) {
           // partner row of the 2x2 block: L[k+1, k] is exactly zero
           p.Lbuf[row + kglob * n] = 0.0;
@@ -934,7 +1104,7 @@ __global__ void __launch_bounds__(kPanelThreads, 1) panel_kernel(PanelParams p) 
     //      redundantly with the owner's exact arithmetic from an smem copy of its L row)
     PROF_BEGIN();
     const int tn = t + s;
-    if (tn < width && k0 + tn < n) {
+    if (!q1 && tn < width && k0 + tn < n) {
       const int pn = win[tn];  // win updated by tid 0 before the barrier above
       const int64_t rown = k0 + pn;
       for (int s3 = tid; s3 < t; s3 += nthr) {
@@ -959,6 +1129,12 @@ __global__ void __launch_bounds__(kPanelThreads, 1) panel_kernel(PanelParams p) 
     PROF_END(5);
   }
 
+  // ---- q = 1: the updated sketch of the rows still active, in the new logical order
+  if (q1 && s_abort == 0)
+    for (int f = tid; f < P * rcnt; f += nthr) {
+      const int i = f / P, r = f - i * P;
+      if (lpos[i] >= t) p.Bout[(size_t)(k0 + lpos[i]) * P + r] = Bq[r * R + i];
+    }
   // ---- publish the panel's permutation and outcome
   for (int i = tid; i < rcnt; i += nthr) {
     const int lp = lpos[i];

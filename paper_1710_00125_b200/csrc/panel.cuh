@@ -51,6 +51,8 @@ struct PanelParams {
   double alpha;
   int G, R, Rs, Ls, Wn;
   int qmode;           // QRCP: 1 = register mode (one column per thread), 0 = generic
+  int q1;              // 1: q = 1 mode (per-step sketch pivot + per-step sketch downdate)
+  double* Bout;        // q = 1: updated sketch written in the new logical order
   const double* A;     // trailing matrix at panel start, col-major ld n, lower triangle valid
   const double* B;     // sketch, P x n col-major (ld P), panel-start order
   double* qscr;        // spill for sketch columns that do not fit in smem

@@ -13,7 +13,7 @@ from conftest import golden_names, l_tol, load_golden
 
 pytestmark = pytest.mark.gpu
 
-Q_B_CASES = [n for n in golden_names() if "_q1_" not in n]
+ALL_CASES = golden_names()
 
 
 def _gpu_factor(a, cfg, robust=False, trace=False):
@@ -42,7 +42,7 @@ def _assert_factor_parity(g, f, n):
     assert np.abs(f.L.sum(axis=1) - g["L_rowsum"]).max() <= tol * n
 
 
-@pytest.mark.parametrize("name", Q_B_CASES)
+@pytest.mark.parametrize("name", ALL_CASES)
 def test_factor_matches_reference_fixture(cuda_ok, name):
     from paper_1710_00125_b200 import api
     g = load_golden(name)
@@ -147,3 +147,48 @@ def test_deficient_solve_flags_singular(cuda_ok):
     rep = api.solve(f, g["a"] @ np.ones(65), g["a"])
     assert rep.singular
     assert rep.backward_error <= 1e-12
+
+
+@pytest.mark.parametrize("n,b,p,seed", [(96, 64, 5, 0), (200, 16, 8, 3), (333, 32, 5, 1), (130, 1, 5, 2)])
+def test_q1_mode_matches_oracle_live(cuda_ok, n, b, p, seed):
+    """q = 1 (per-step sketch pivoting, the reference's default FactorConfig mode)."""
+    from oracle.rcp_oracle import OracleConfig, oracle_factor
+    from paper_1710_00125_b200 import gallery
+    a = gallery.type6(n, 2000 + seed)
+    o = oracle_factor(a, OracleConfig(b=b, q=1, p=p, seed=seed))
+    df = _gpu_factor(a, dict(strategy="rcp", b=b, q=1, p=p, seed=seed))
+    hf = df.to_host()
+    assert np.array_equal(hf.perm, o.perm)
+    assert np.array_equal(hf.pattern, o.pattern)
+    assert np.abs(hf.L - o.L).max() <= l_tol(n)
+    dref = o.d_dense()
+    assert np.abs(hf.D.to_dense() - dref).max() <= l_tol(n) * max(1.0, np.abs(dref).max())
+
+
+def test_default_config_is_supported(cuda_ok):
+    """factor(a) with the reference's default FactorConfig (rcp, p=5, b=64, q=1)."""
+    from oracle.rcp_oracle import OracleConfig, oracle_factor
+    from paper_1710_00125_b200 import api, gallery
+    a = gallery.type6(150, 77)
+    f = api.factor(a)
+    o = oracle_factor(a, OracleConfig())
+    assert np.array_equal(f.perm, o.perm)
+    assert np.abs(f.L - o.L).max() <= l_tol(150)
+
+
+def test_q1_guard_detects_zero_tail(cuda_ok):
+    """Reference test_factor.py:157-166 in the reference's own configuration (b=64, q=1, p=6)."""
+    from oracle.rcp_oracle import OracleConfig, oracle_factor
+    from paper_1710_00125_b200 import api, gallery
+    a = np.zeros((65, 65))
+    a[:40, :40] = gallery.type6(40, 5)
+    f = api.factor_robust(a, strategy="rcp", p=6, seed=2)
+    o = oracle_factor(a, OracleConfig(p=6, seed=2))
+    assert f.deficient_from == 40
+    assert np.all(f.pattern[40:] == api.PAT_DEFICIENT)
+    assert f.stats.recompute_count == o.recompute_count == 1
+    assert np.array_equal(f.perm, o.perm)
+    assert np.array_equal(f.pattern, o.pattern)
+    den = float(np.abs(a).max())
+    rec = f.L @ f.D.to_dense() @ f.L.T
+    assert float(np.abs(rec - a[np.ix_(f.perm, f.perm)]).max()) / den <= 1e-12
