@@ -91,6 +91,7 @@ typedef struct rcp_stats {
   double t_panel_ms;         /* device time inside the panel kernels              */
   double schur_flops;        /* algorithmic flops of the trailing updates: sum t*m*(m+1) */
   int64_t n_launches;        /* kernels launched by this call                     */
+  int64_t mults, adds, divs, comps; /* the reference's OpCounters (metrics.py:28-43), exact */
   double panel_prof_ms[16];  /* CTA-0 cycle profile of the panel kernels (ms at the max SM clock):
                                 0 qrcp, 1 qrcp-exchange, 2 sbkp-gemv, 3 sbkp-exchange, 4 sbkp-eliminate,
                                 5 next-pivot, 6 qrcp-reflect, 7 total, 8 sbkp-local-argmax,

@@ -68,6 +68,10 @@ class RcpStats(ctypes.Structure):
         ("t_panel_ms", ctypes.c_double),
         ("schur_flops", ctypes.c_double),
         ("n_launches", ctypes.c_int64),
+        ("mults", ctypes.c_int64),
+        ("adds", ctypes.c_int64),
+        ("divs", ctypes.c_int64),
+        ("comps", ctypes.c_int64),
         ("panel_prof_ms", ctypes.c_double * 16),
         ("message", ctypes.c_char * 160),
     ]

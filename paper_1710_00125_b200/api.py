@@ -246,7 +246,7 @@ class DeviceFactorization:
         blocks = _blocks_from_arrays(self.d_diag.cpu().numpy(), self.d_off.cpu().numpy(), pattern)
         s = self.stats
         stats = GrowthStats(rho_cheap=s["rho_cheap"], max_multiplier=s["max_multiplier"],
-                            counters=OpCounters(), recompute_count=s["recompute_count"])
+                            counters=OpCounters(*s["counters"]), recompute_count=s["recompute_count"])
         if self.n >= 2048:  # D2H into (cached) pinned memory: full PCIe bandwidth for the dense L
             lh = torch.empty(tuple(self.L.shape), dtype=torch.float64, pin_memory=True)
             lh.copy_(self.L)
@@ -367,6 +367,7 @@ def factor_device(a: torch.Tensor, cfg: FactorConfig | None = None, *, omega: to
         "deficient_from": int(st.deficient_from), "t_factor_ms": float(st.t_factor_ms),
         "t_schur_ms": float(st.t_schur_ms), "t_panel_ms": float(st.t_panel_ms),
         "schur_flops": float(st.schur_flops), "n_launches": int(st.n_launches),
+        "counters": (int(st.mults), int(st.adds), int(st.divs), int(st.comps)),
         "panel_prof_ms": dict(zip(("qrcp", "qrcp_exchange", "sbkp_gemv", "sbkp_exchange", "sbkp_eliminate",
                                    "next_pivot", "qrcp_reflect", "total", "sbkp_local_argmax",
                                    "qrcp_local_argmax", "qrcp_householder"),

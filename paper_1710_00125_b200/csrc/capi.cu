@@ -260,6 +260,8 @@ int rcp_factor(const rcp_config* cfg, int64_t n, const double* a, int64_t lda, c
   int64_t k = 0;
   int64_t snap_off = 0;
   int64_t recomputes = 0;
+  // panel-level op counters (factor.py:377-378, 564-565, 577-599); step-level ones come from the kernel
+  long long h_mul = 0, h_add = 0, h_div = 0, h_cmp = 0;
   int64_t deficient_from = -1;
   std::vector<PanelRecord> panels;
   std::vector<double> draw_buf;
@@ -382,6 +384,23 @@ int rcp_factor(const rcp_config* cfg, int64_t n, const double* a, int64_t lda, c
       prm.guard_limit = thr * beta;
       (void)attempt;
     }
+    if (!q1 && m0 > 1) {  // preselect norms (factor.py:576-577)
+      h_mul += (long long)P * (m0 - 1);
+      h_add += (long long)P * (m0 - 1);
+      h_cmp += m0 - 1;
+    }
+    if (stopped && q1) {  // the stopping step charged its sketch norms (factor.py:608-610)
+      h_mul += (long long)P * (m0 - 1);
+      h_add += (long long)P * (m0 - 1);
+      h_cmp += m0 - 1;
+    }
+    if (!stopped) {
+      for (int j = 0; j < qn; ++j) {  // QRCP slots (sketch.py:135-169 via factor.py:586-599)
+        h_cmp += m0 - 1 - j;
+        h_mul += 2LL * P * (m0 - j);
+        h_add += 2LL * P * (m0 - j);
+      }
+    }
     if (stopped) {
       RCP_LAUNCH(launch_deficient_fill(n, k0, permb[pcur], perm, d_diag, d_off, pattern, st));
       deficient_from = k0;
@@ -413,9 +432,13 @@ int rcp_factor(const rcp_config* cfg, int64_t n, const double* a, int64_t lda, c
       RCP_LAUNCH(launch_schur_update(n, k_end, mp, Lneg, Wg, tpad, t, A[curA], phys, A[curA ^ 1], st));
       RCP_CHECK(cudaEventRecord(es.b, st));
       schur_flops += (double)t * (double)mp * (double)(mp + 1);
+      h_mul += (long long)t * (mp * (mp + 1) / 2);  // _apply_trailing (factor.py:377-378)
+      h_add += (long long)t * (mp * (mp + 1) / 2);
       curA ^= 1;
       if (!q1) {
         // sketch correction once per panel (factor.py:554-565)
+        h_mul += (long long)t * P * mp + (long long)(t * (t - 1) / 2) * mp;
+        h_add += (long long)t * P * mp + (long long)(t * (t - 1) / 2) * mp;
         RCP_LAUNCH(launch_ysolve(n, P, k0, t, tpad, pol, B[curB], L11c, Y, st));
         RCP_LAUNCH(launch_sketch_correction(P, mp, k_end, Y, tpad, t, Lneg, B[curB], phys, B[curB ^ 1], st));
       }
@@ -474,6 +497,10 @@ int rcp_factor(const rcp_config* cfg, int64_t n, const double* a, int64_t lda, c
     cudaDeviceGetAttribute(&clk_khz, cudaDevAttrClockRate, dev);
     for (int i = 0; i < 16; ++i) stats->panel_prof_ms[i] = clk_khz > 0 ? (double)hstate->cyc[i] / clk_khz : 0.0;
     stats->n_launches = launches;
+    stats->mults = h_mul + hstate->cnt[0];
+    stats->adds = h_add + hstate->cnt[1];
+    stats->divs = h_div + hstate->cnt[2];
+    stats->comps = h_cmp + hstate->cnt[3];
   }
   return RCP_OK;
 }

@@ -643,10 +643,20 @@ __global__ void __launch_bounds__(kPanelThreads, 1) panel_kernel(PanelParams p) 
   __syncthreads();
 
   int t = 0;
+  int end_reason = 0;  // 1: 2x2 defer, 2: q=1 guard defer (for the op counters)
+  // Operation counters of the steps (metrics.py:28-43), kept by CTA 0 / thread 0 and committed
+  // only when the panel completes (a tripped attempt is relaunched and recharged).
+  long long c_mul = 0, c_add = 0, c_div = 0, c_cmp = 0;
   while (t < width && k0 + t < n) {
     if (q1) {
       // ---- q = 1: sketch column argmax (factor.py:607-620), then swap(k, k + jl)
       if (n - (k0 + t) > 1) {
+        if (cta == 0 && tid == 0) {  // column_norms of the active sketch (factor.py:608-610)
+          const long long mm = n - (k0 + t);
+          c_mul += (long long)P * (mm - 1);
+          c_add += (long long)P * (mm - 1);
+          c_cmp += mm - 1;
+        }
         double bk1 = -1.0;
         long long bi1 = LLONG_MAX;
         int bs1 = -1;
@@ -750,7 +760,10 @@ __global__ void __launch_bounds__(kPanelThreads, 1) panel_kernel(PanelParams p) 
           if (tid == 0) atomicExch(&p.st->status, 99);
           break;
         }
-        if (s_qflags & 8) break;  // defer: flush this panel, retest at t == 0
+        if (s_qflags & 8) {  // defer: flush this panel, retest at t == 0
+          end_reason = 2;
+          break;
+        }
         if (s_qflags & 3) {
           if (cta == 0 && tid == 0) p.st->status = (s_qflags & 2) ? 2 : 1;
           s_abort = 2;
@@ -948,7 +961,41 @@ __global__ void __launch_bounds__(kPanelThreads, 1) panel_kernel(PanelParams p) 
       kind = 3;
       s = 2;
     }
-    if (s == 2 && t > 0 && t + 2 > width) break;  // defer (factor.py:622-623)
+    const bool deferred = s == 2 && t > 0 && t + 2 > width;
+    if (cta == 0 && tid == 0) {
+      // _decide: form column k, scan, diag of r (factor.py:350-367, 414-427)
+      const long long mm = n - (k0 + t);
+      const long long colc = t > 0 ? (long long)t * mm : 0;
+      c_mul += colc;
+      c_add += colc;
+      c_cmp += mm >= 2 ? mm - 2 : 0;
+      if (kind >= 2 && t > 0) {
+        c_mul += t;
+        c_add += t;
+      }
+      if (!deferred) {  // _eliminate re-forms the column(s) (factor.py:449-489)
+        c_mul += colc * s;
+        c_add += colc * s;
+        const long long w = mm - s;
+        if (kind != 0) {
+          if (s == 1) {
+            c_div += w;
+          } else {
+            c_div += 2 * w;
+            c_mul += 4 * w + 2;
+            c_add += 2 * w + 1;
+          }
+        }
+        if (q1 && w > 0) {
+          c_mul += (long long)s * P * w;
+          c_add += (long long)s * P * w;
+        }
+      }
+    }
+    if (deferred) {  // defer (factor.py:622-623)
+      end_reason = 1;
+      break;
+    }
 
     // ---- symmetric swaps as permutation bookkeeping (factor.py:624-630)
     int p_t = pk, p_t1 = -1;
@@ -1145,6 +1192,13 @@ __global__ void __launch_bounds__(kPanelThreads, 1) panel_kernel(PanelParams p) 
     p.st->seq = seq;
     p.st->k_end = k0 + t;
     p.st->t_end = t;
+    p.st->end_reason = end_reason;
+    if (s_abort == 0) {
+      p.st->cnt[0] += c_mul;
+      p.st->cnt[1] += c_add;
+      p.st->cnt[2] += c_div;
+      p.st->cnt[3] += c_cmp;
+    }
   }
   if (prof) atomicAdd(reinterpret_cast<unsigned long long*>(&p.st->cyc[7]), (unsigned long long)(prof_now() - c_kernel0));
 #undef PROF_BEGIN

@@ -14,8 +14,8 @@ struct PanelState {
   int status;          // 0 ok, 1 guard trip (recompute needed), 2 guard stop (deficient tail)
   int n_steps;         // decisions taken (cumulative)
   int n_2x2;           // 2x2 blocks (cumulative)
-  int pad;
-  long long pad2;
+  int end_reason;      // why the panel ended early: 0 none, 1 2x2 defer, 2 q=1 guard defer
+  long long cnt[4];    // step op counters (mults, adds, divs, comps), cumulative
   // SM-cycle profile of CTA 0 (cumulative), see kProfNames in capi.cu
   long long cyc[16];
 };

@@ -60,6 +60,8 @@ def test_factor_matches_reference_fixture(cuda_ok, name):
 
     _assert_factor_parity(g, F, n)
     assert hf.stats.recompute_count == int(g["recompute_count"])
+    c = hf.stats.counters  # exact OpCounters parity (metrics.py:28-43)
+    assert [c.mults, c.adds, c.divs, c.comps] == [int(x) for x in g["counters"]]
     rho_ref = float(g["rho_cheap"])
     assert abs(hf.stats.rho_cheap - rho_ref) <= l_tol(n) * max(1.0, rho_ref)
     assert abs(hf.stats.max_multiplier - float(g["max_multiplier"])) <= l_tol(n) * 10
@@ -98,6 +100,8 @@ def test_factor_matches_oracle_live(cuda_ok, n, b, p, seed):
     hf = df.to_host()
     assert np.array_equal(hf.perm, o.perm)
     assert np.array_equal(hf.pattern, o.pattern)
+    c, oc = hf.stats.counters, o.counters
+    assert [c.mults, c.adds, c.divs, c.comps] == [oc.mults, oc.adds, oc.divs, oc.comps]
     assert np.abs(hf.L - o.L).max() <= l_tol(n)
     dref = o.d_dense()
     assert np.abs(hf.D.to_dense() - dref).max() <= l_tol(n) * max(1.0, np.abs(dref).max())
@@ -160,6 +164,8 @@ def test_q1_mode_matches_oracle_live(cuda_ok, n, b, p, seed):
     hf = df.to_host()
     assert np.array_equal(hf.perm, o.perm)
     assert np.array_equal(hf.pattern, o.pattern)
+    c, oc = hf.stats.counters, o.counters
+    assert [c.mults, c.adds, c.divs, c.comps] == [oc.mults, oc.adds, oc.divs, oc.comps]
     assert np.abs(hf.L - o.L).max() <= l_tol(n)
     dref = o.d_dense()
     assert np.abs(hf.D.to_dense() - dref).max() <= l_tol(n) * max(1.0, np.abs(dref).max())
