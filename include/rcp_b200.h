@@ -13,6 +13,10 @@
  *   rcp_solve           <- randldl.solve / solve_many        (solve.py:79-107)
  *   rcp_reconstruct     <- randldl.reconstruct               (factor.py:663-665)
  *   rcp_workspace_bytes    workspace query (no reference counterpart)
+ *   rcp_factor_batched  <- a loop of randldl.factor over independent small
+ *                          matrices sharing one FactorConfig (BASELINE config C5;
+ *                          q = b, n <= 256): one CTA per matrix, no host round trip
+ *   rcp_solve_batched   <- a loop of randldl.solve over those factorizations
  *
  * Conventions
  *  - All matrix pointers are DEVICE pointers to fp64 data.  The input matrix
@@ -131,6 +135,49 @@ size_t rcp_solve_workspace_bytes(int64_t n, int64_t nrhs);
 /* out (n x n row-major) = L D L^T (factor.py:663-665). */
 int rcp_reconstruct(int64_t n, const double* L, const double* d_diag, const double* d_off,
                     const int8_t* pattern, double* out, void* cuda_stream);
+
+/* ---- batched small matrices (C5) -------------------------------------------------------- */
+
+/* Per-matrix outcome of rcp_factor_batched (status uses the RCP_* codes above). */
+typedef struct rcp_batch_stats {
+  int32_t status;            /* RCP_OK / NOT_SYMMETRIC / NONFINITE_INPUT / NUMERICAL / NEED_NORMALS */
+  int32_t num_kind;          /* RCP_NUM_* when status == RCP_ERR_NUMERICAL                      */
+  int32_t num_step;          /* step k of the numerical error                                    */
+  int32_t recompute_count;   /* guard recomputes                                                 */
+  int32_t deficient_from;    /* first PAT_DEFICIENT index, -1 if none                            */
+  int32_t n_2x2;
+  int32_t n_steps;
+  int32_t n_panels;
+  double rho_cheap, max_multiplier, amax, dmax;
+  int64_t mults, adds, divs, comps;  /* OpCounters (metrics.py:28-43)                           */
+} rcp_batch_stats;
+
+/* Device workspace bytes for rcp_factor_batched (independent of `count`: the kernel is
+ * persistent, one slot per resident CTA). */
+size_t rcp_batched_workspace_bytes(int64_t n, const rcp_config* cfg);
+
+/* Factor `count` independent symmetric n x n matrices (n <= 256, q == b <= 32, p <= 64):
+ * matrix i is a + i * a_stride (leading dimension lda).  `normals` (device, length
+ * normals_len >= p * n) is the factorization's normal stream
+ * Generator(Philox(seed)).standard_normal(normals_len): its first p * n values are Omega
+ * (row-major, sketch.py:83-84) and each guard recompute of a matrix consumes the next p * m
+ * values (sketch.py:63-84) — every matrix starts the stream afresh, exactly as separate
+ * randldl.factor calls with one cfg.seed do.  A matrix that would need more normals than
+ * supplied gets status RCP_ERR_NEED_NORMALS (re-run it with rcp_factor).
+ * Outputs are per matrix, contiguous: perm[count][n], L[count][n][n] (row-major),
+ * d_diag/d_off[count][n], pattern[count][n], mstats[count] (all device).
+ * Returns RCP_OK when the launch succeeded; per-matrix outcomes are in mstats. */
+int rcp_factor_batched(const rcp_config* cfg, int64_t count, int64_t n, const double* a,
+                       int64_t lda, int64_t a_stride, const double* normals, int64_t normals_len,
+                       void* workspace, size_t workspace_bytes, int64_t* perm, double* L,
+                       double* d_diag, double* d_off, int8_t* pattern, rcp_batch_stats* mstats,
+                       void* cuda_stream);
+
+/* x[i] = solve(factorization i, b[i]) for `count` factorizations from rcp_factor_batched
+ * (solve.py:34-76); b and x are [count][n] (may alias); singular[i] set as in rcp_solve. */
+int rcp_solve_batched(int64_t count, int64_t n, const int64_t* perm, const double* L,
+                      const double* d_diag, const double* d_off, const int8_t* pattern,
+                      const double* b, double* x, int32_t* singular, void* cuda_stream);
 
 /* Library identification: "rcp_b200 <version> sm_100a". */
 const char* rcp_version(void);

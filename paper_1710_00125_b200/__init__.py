@@ -33,5 +33,12 @@ from .api import (  # noqa: F401
     solve_many,
 )
 from ._native import NativeUnavailable  # noqa: F401
+from .batched import (  # noqa: F401
+    BatchedDeviceFactorization,
+    factor_batched,
+    factor_batched_device,
+    solve_batched,
+    solve_batched_device,
+)
 
 __version__ = "0.1.0"

@@ -39,6 +39,9 @@ EXPORTED_SYMBOLS = (
     "rcp_solve_workspace_bytes",
     "rcp_reconstruct",
     "rcp_version",
+    "rcp_batched_workspace_bytes",
+    "rcp_factor_batched",
+    "rcp_solve_batched",
 )
 
 
@@ -77,6 +80,36 @@ class RcpStats(ctypes.Structure):
     ]
 
 
+class RcpBatchStats(ctypes.Structure):
+    _fields_ = [
+        ("status", ctypes.c_int32),
+        ("num_kind", ctypes.c_int32),
+        ("num_step", ctypes.c_int32),
+        ("recompute_count", ctypes.c_int32),
+        ("deficient_from", ctypes.c_int32),
+        ("n_2x2", ctypes.c_int32),
+        ("n_steps", ctypes.c_int32),
+        ("n_panels", ctypes.c_int32),
+        ("rho_cheap", ctypes.c_double),
+        ("max_multiplier", ctypes.c_double),
+        ("amax", ctypes.c_double),
+        ("dmax", ctypes.c_double),
+        ("mults", ctypes.c_int64),
+        ("adds", ctypes.c_int64),
+        ("divs", ctypes.c_int64),
+        ("comps", ctypes.c_int64),
+    ]
+
+
+# numpy view of an array of rcp_batch_stats (same layout, 96 bytes)
+BATCH_STATS_DTYPE = [
+    ("status", "<i4"), ("num_kind", "<i4"), ("num_step", "<i4"), ("recompute_count", "<i4"),
+    ("deficient_from", "<i4"), ("n_2x2", "<i4"), ("n_steps", "<i4"), ("n_panels", "<i4"),
+    ("rho_cheap", "<f8"), ("max_multiplier", "<f8"), ("amax", "<f8"), ("dmax", "<f8"),
+    ("mults", "<i8"), ("adds", "<i8"), ("divs", "<i8"), ("comps", "<i8"),
+]
+
+
 DRAW_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64,
                            ctypes.POINTER(ctypes.c_double))
 
@@ -111,6 +144,13 @@ def load(path: str | os.PathLike | None = None):
     lib.rcp_solve_workspace_bytes.restype = sz
     lib.rcp_reconstruct.argtypes = [i64, vp, vp, vp, vp, vp, vp]
     lib.rcp_reconstruct.restype = ctypes.c_int
+    lib.rcp_batched_workspace_bytes.argtypes = [i64, ctypes.POINTER(RcpConfig)]
+    lib.rcp_batched_workspace_bytes.restype = sz
+    lib.rcp_factor_batched.argtypes = [ctypes.POINTER(RcpConfig), i64, i64, vp, i64, i64, vp, i64, vp, sz,
+                                       vp, vp, vp, vp, vp, vp, vp]
+    lib.rcp_factor_batched.restype = ctypes.c_int
+    lib.rcp_solve_batched.argtypes = [i64, i64, vp, vp, vp, vp, vp, vp, vp, vp, vp]
+    lib.rcp_solve_batched.restype = ctypes.c_int
     lib.rcp_version.argtypes = []
     lib.rcp_version.restype = ctypes.c_char_p
     _lib = lib

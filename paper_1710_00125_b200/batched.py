@@ -1,0 +1,257 @@
+"""Batched factor/solve of many small independent matrices (BASELINE config C5).
+
+The reference has no batched entry point: a user factors a stack of matrices by
+calling ``randldl.factor(a_i, cfg)`` in a loop (``factor.py:637-647``; one
+``FactorConfig``, hence one seed, for all of them) and ``randldl.solve`` per
+matrix (``solve.py:79-92``).  :func:`factor_batched` / :func:`solve_batched`
+return exactly what that loop returns, computed by one persistent CUDA kernel
+(``csrc/batched.cu``, C ABI ``rcp_factor_batched``) with no host round trip
+per matrix.
+
+Sketch stream: every ``factor`` call starts ``Generator(Philox(cfg.seed))``
+afresh, draws Omega (``p x n``) and, on each guard recompute, the next ``p x m``
+normals (``sketch.py:63-84``).  All matrices therefore read the same stream;
+it is drawn once on the host and uploaded, with a budget of ``extra_draws``
+full-size recomputes per matrix.  A matrix needing more (not seen on C5: its
+scaled members recompute exactly once) is re-run through the single-matrix
+path, which draws on demand.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _native
+from .api import (BlockDiag, DeviceFactorization, Factorization, FactorConfig, GrowthStats, NumericalError,
+                  OpCounters, _blocks_from_arrays, _check_supported, _config, _device, _raise_status, _stream,
+                  factor_device)
+
+__all__ = ["BatchedDeviceFactorization", "factor_batched_device", "factor_batched", "solve_batched_device",
+           "solve_batched", "batched_workspace_bytes", "normal_stream"]
+
+MAX_N = 256
+
+
+@dataclass
+class BatchedDeviceFactorization:
+    """``count`` GPU-resident factorizations (leading dimension = matrix index)."""
+
+    perm: torch.Tensor      # int64 [count, n]
+    L: torch.Tensor         # float64 [count, n, n], row-major unit lower
+    d_diag: torch.Tensor    # float64 [count, n]
+    d_off: torch.Tensor     # float64 [count, n]
+    pattern: torch.Tensor   # int8 [count, n]
+    stats: np.ndarray       # structured array (_native.BATCH_STATS_DTYPE) [count]
+
+    @property
+    def count(self) -> int:
+        return int(self.perm.shape[0])
+
+    @property
+    def n(self) -> int:
+        return int(self.perm.shape[1])
+
+    def factorization(self, i: int) -> Factorization:
+        return self.to_host(range(i, i + 1))[0]
+
+    def to_host(self, which=None) -> list:
+        idx = range(self.count) if which is None else which
+        sel = torch.as_tensor(list(idx), dtype=torch.int64, device=self.perm.device)
+        perm = self.perm.index_select(0, sel).cpu().numpy()
+        L = self.L.index_select(0, sel).cpu().numpy()
+        dd = self.d_diag.index_select(0, sel).cpu().numpy()
+        doff = self.d_off.index_select(0, sel).cpu().numpy()
+        pat = self.pattern.index_select(0, sel).cpu().numpy().astype(np.int8)
+        out = []
+        for j, i in enumerate(idx):
+            s = self.stats[i]
+            stats = GrowthStats(rho_cheap=float(s["rho_cheap"]), max_multiplier=float(s["max_multiplier"]),
+                                counters=OpCounters(int(s["mults"]), int(s["adds"]), int(s["divs"]),
+                                                    int(s["comps"])),
+                                recompute_count=int(s["recompute_count"]))
+            out.append(Factorization(perm=perm[j].astype(np.int64), L=L[j],
+                                     D=BlockDiag(_blocks_from_arrays(dd[j], doff[j], pat[j])),
+                                     pattern=pat[j], stats=stats))
+        return out
+
+
+def _cfg_struct(cfg: FactorConfig) -> _native.RcpConfig:
+    return _native.RcpConfig(cfg.p, cfg.b, cfg.q, cfg.robust_r)
+
+
+def batched_workspace_bytes(n: int, cfg: FactorConfig) -> int:
+    lib = _native.load()
+    c = _cfg_struct(cfg)
+    return int(lib.rcp_batched_workspace_bytes(n, ctypes.byref(c)))
+
+
+def normal_stream(cfg: FactorConfig, n: int, extra_draws: int = 4) -> np.ndarray:
+    """The first ``p*n*(1 + extra_draws)`` values of ``Generator(Philox(cfg.seed)).standard_normal``."""
+    gen = np.random.Generator(np.random.Philox(cfg.seed))
+    return gen.standard_normal(cfg.p * n * (1 + extra_draws))
+
+
+def _supported(cfg: FactorConfig, n: int) -> bool:
+    return n <= MAX_N and cfg.q == cfg.b and cfg.q > 1 and cfg.b <= 32 and cfg.p <= 64
+
+
+def _raise_matrix(i: int, s) -> None:
+    st = _native.RcpStats()
+    st.num_kind = int(s["num_kind"])
+    st.num_step = int(s["num_step"])
+    try:
+        _raise_status(int(s["status"]), st)
+    except (ValueError, NumericalError) as exc:
+        raise type(exc)(f"matrix {i}: {exc}") from None
+
+
+def factor_batched_device(a: torch.Tensor, cfg: FactorConfig | None = None, *, normals: torch.Tensor | None = None,
+                          extra_draws: int = 4, workspace: torch.Tensor | None = None,
+                          out: BatchedDeviceFactorization | None = None, check: bool = True,
+                          **overrides) -> BatchedDeviceFactorization:
+    """Factor ``a[i]`` (CUDA float64 ``[count, n, n]``, each exactly symmetric) for every i.
+
+    Results equal ``[factor(a[i], cfg) for i in range(count)]``.  With ``check`` the first
+    failing matrix raises the reference's exception (prefixed with its index); matrices that
+    exhaust the pre-drawn normal stream are re-run through :func:`factor_device`.
+    """
+    cfg = _config(cfg, overrides)
+    _check_supported(cfg)
+    lib = _native.load()
+    if a.dim() != 3 or a.shape[1] != a.shape[2]:
+        raise ValueError(f"expected a [count, n, n] stack, got shape {tuple(a.shape)}")
+    if a.dtype != torch.float64 or not a.is_cuda:
+        raise ValueError("factor_batched_device expects a CUDA float64 tensor")
+    count, n = int(a.shape[0]), int(a.shape[1])
+    if n == 0:
+        raise ValueError("A must have at least one row")
+    if a.stride(2) != 1 or a.stride(1) != n:
+        a = a.contiguous()
+    dev = a.device
+    if out is None:
+        out = BatchedDeviceFactorization(
+            perm=torch.empty(count, n, dtype=torch.int64, device=dev),
+            L=torch.empty(count, n, n, dtype=torch.float64, device=dev),
+            d_diag=torch.empty(count, n, dtype=torch.float64, device=dev),
+            d_off=torch.empty(count, n, dtype=torch.float64, device=dev),
+            pattern=torch.empty(count, n, dtype=torch.int8, device=dev),
+            stats=np.zeros(count, dtype=_native.BATCH_STATS_DTYPE))
+    if not _supported(cfg, n):
+        # outside the batched kernel's on-chip limits: the single-matrix GPU path, per matrix
+        for i in range(count):
+            f = factor_device(a[i], cfg)
+            _copy_single(out, i, f)
+        return out
+    if normals is None:
+        normals = torch.from_numpy(normal_stream(cfg, n, extra_draws)).to(dev)
+    if workspace is None:
+        workspace = torch.empty(batched_workspace_bytes(n, cfg), dtype=torch.uint8, device=dev)
+    mstats = torch.empty(count * ctypes.sizeof(_native.RcpBatchStats), dtype=torch.uint8, device=dev)
+    c = _cfg_struct(cfg)
+    status = lib.rcp_factor_batched(ctypes.byref(c), count, n, a.data_ptr(), n, n * n, normals.data_ptr(),
+                                    normals.numel(), workspace.data_ptr(), workspace.numel(), out.perm.data_ptr(),
+                                    out.L.data_ptr(), out.d_diag.data_ptr(), out.d_off.data_ptr(),
+                                    out.pattern.data_ptr(), mstats.data_ptr(), _stream())
+    _raise_status(status, None)
+    out.stats = mstats.cpu().numpy().view(_native.BATCH_STATS_DTYPE).copy()
+    redo = np.nonzero(out.stats["status"] == _native.RCP_ERR_NEED_NORMALS)[0]
+    for i in redo:
+        f = factor_device(a[int(i)], cfg)
+        _copy_single(out, int(i), f)
+    if check:
+        bad = np.nonzero(out.stats["status"] != _native.RCP_OK)[0]
+        if bad.size:
+            i = int(bad[0])
+            _raise_matrix(i, out.stats[i])
+    return out
+
+
+def _copy_single(out: BatchedDeviceFactorization, i: int, f: DeviceFactorization) -> None:
+    out.perm[i].copy_(f.perm)
+    out.L[i].copy_(f.L)
+    out.d_diag[i].copy_(f.d_diag)
+    out.d_off[i].copy_(f.d_off)
+    out.pattern[i].copy_(f.pattern)
+    s = f.stats
+    rec = out.stats[i]
+    rec["status"] = _native.RCP_OK
+    rec["recompute_count"] = s["recompute_count"]
+    rec["deficient_from"] = s["deficient_from"]
+    rec["n_2x2"] = s["n_2x2"]
+    rec["n_steps"] = s["n_steps"]
+    rec["n_panels"] = s["n_panels"]
+    rec["rho_cheap"] = s["rho_cheap"]
+    rec["max_multiplier"] = s["max_multiplier"]
+    rec["amax"] = s["amax"]
+    rec["dmax"] = s["dmax"]
+    rec["mults"], rec["adds"], rec["divs"], rec["comps"] = s["counters"]
+
+
+def factor_batched(a: np.ndarray, cfg: FactorConfig | None = None, **overrides) -> list:
+    """``[randldl.factor(a[i], cfg) for i in range(len(a))]`` in one device call."""
+    cfg = _config(cfg, overrides)
+    a = np.asarray(a, dtype=np.float64)
+    if a.ndim != 3 or a.shape[1] != a.shape[2]:
+        raise ValueError(f"expected a [count, n, n] stack, got shape {a.shape}")
+    dev = _device()
+    ad = torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+    return factor_batched_device(ad, cfg).to_host()
+
+
+def solve_batched_device(f: BatchedDeviceFactorization, b: torch.Tensor,
+                         x: torch.Tensor | None = None) -> tuple:
+    """x[i] = A_i^-1 b[i] (solve.py:34-76) for every factorization; returns (x, singular[count])."""
+    lib = _native.load()
+    count, n = f.count, f.n
+    if tuple(b.shape) != (count, n):
+        raise ValueError(f"right-hand sides must be ({count}, {n}), got {tuple(b.shape)}")
+    b = b.to(dtype=torch.float64).contiguous()
+    if x is None:
+        x = torch.empty_like(b)
+    sing = torch.zeros(count, dtype=torch.int32, device=b.device)
+    if n > MAX_N:
+        from .api import solve_device
+        for i in range(count):
+            df = DeviceFactorization(perm=f.perm[i], L=f.L[i], d_diag=f.d_diag[i], d_off=f.d_off[i],
+                                     pattern=f.pattern[i], stats={})
+            xi, si = solve_device(df, b[i])
+            x[i].copy_(xi)
+            sing[i] = int(si)
+        return x, sing.bool()
+    status = lib.rcp_solve_batched(count, n, f.perm.data_ptr(), f.L.data_ptr(), f.d_diag.data_ptr(),
+                                   f.d_off.data_ptr(), f.pattern.data_ptr(), b.data_ptr(), x.data_ptr(),
+                                   sing.data_ptr(), _stream())
+    _raise_status(status, None)
+    return x, sing.bool()
+
+
+def solve_batched(fs: list, b: np.ndarray) -> np.ndarray:
+    """``[randldl.solve(fs[i], b[i]).x for i]`` in one device call."""
+    b = np.asarray(b, dtype=np.float64)
+    if b.ndim != 2 or b.shape[0] != len(fs):
+        raise ValueError(f"right-hand sides must be (count, n), got {b.shape}")
+    dev = _device()
+    n = b.shape[1]
+    dd = np.zeros((len(fs), n))
+    doff = np.zeros((len(fs), n))
+    for i, f in enumerate(fs):
+        j = 0
+        for blk in f.D.blocks:
+            if blk.shape[0] == 1:
+                dd[i, j] = blk[0, 0]
+                j += 1
+            else:
+                dd[i, j], dd[i, j + 1], doff[i, j] = blk[0, 0], blk[1, 1], blk[1, 0]
+                j += 2
+    bf = BatchedDeviceFactorization(
+        perm=torch.from_numpy(np.stack([f.perm for f in fs]).astype(np.int64)).to(dev),
+        L=torch.from_numpy(np.ascontiguousarray(np.stack([f.L for f in fs]))).to(dev),
+        d_diag=torch.from_numpy(dd).to(dev), d_off=torch.from_numpy(doff).to(dev),
+        pattern=torch.from_numpy(np.stack([f.pattern for f in fs]).astype(np.int8)).to(dev),
+        stats=np.zeros(len(fs), dtype=_native.BATCH_STATS_DTYPE))
+    x, _ = solve_batched_device(bf, torch.from_numpy(b).to(dev))
+    return x.cpu().numpy()

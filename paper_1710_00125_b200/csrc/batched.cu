@@ -1,0 +1,982 @@
+// Batched RCP factorization of many small symmetric matrices (BASELINE config C5:
+// 65536 x n = 256, b = q = 16, P = 24), plus the matching batched solve.
+//
+// Same algorithm as the single-matrix driver (capi.cu + panel.cu), re-laid out for a
+// matrix that one CTA can own: every synchronisation is a CTA barrier, nothing goes back
+// to the host, and one persistent grid (two CTAs per SM) pulls matrices from an atomic
+// counter.  Thread i of the CTA owns logical row/column i of its matrix:
+//   * the sketch column B[:, i] lives in thread i's registers (x[]), so QRCP
+//     (sketch.py:135-169) is register-resident and swaps move registers via smem;
+//   * the panel's L and W columns (factor.py:350-367, W = unscaled columns) live in smem;
+//   * the trailing matrix lives in per-CTA global scratch (L2-resident) in the panel's
+//     start order; inside a panel symmetric swaps (factor.py:333-348) are bookkeeping
+//     (pol[]), and the trailing update (factor.py:369-379) gathers through it while
+//     writing the next panel's compact trailing block (lower computed, mirrored);
+//   * L columns are stored keyed by the ORIGINAL row index, so later row swaps never move
+//     them; the final L (final pivot order) is one coalesced row gather.
+// The decision logic (first-index argmax, thresholds, alpha, defer rule, 2x2 formulas with
+// IEEE division and no FMA contraction, the checks of factor.py:455-466, the guard with
+// the continuing normal stream) follows the reference line by line; see panel.cu for the
+// corresponding cross-references.
+#include <algorithm>
+#include <cfloat>
+#include <climits>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+
+#include "../../include/rcp_b200.h"
+#include "rcp_common.cuh"
+
+using namespace rcp;
+
+namespace {
+
+constexpr int BT = 256;  // threads per CTA == largest supported n
+constexpr int BW = BT / 32;
+constexpr int kMaxB = 32;
+constexpr int kMaxThr = 24;  // guard thresholds precomputed on the host
+
+struct BatchParams {
+  int count, n, P, b, q, armed;
+  double alpha;
+  double thr[kMaxThr];  // thr[j] = eps ** ((j + 1) / robust_r)  (factor.py:316, 406), host pow
+  const double* A;
+  int64_t lda, a_stride;
+  const double* omegaT;  // n x P: omegaT[j * P + r] = Omega[r, j]
+  const double* z;       // normal stream; z[0, P n) = Omega row-major
+  int64_t z_len;
+  double* ws;
+  int64_t ws_stride;  // doubles per CTA
+  int64_t* perm;
+  double* L;
+  double* d_diag;
+  double* d_off;
+  int8_t* pattern;
+  rcp_batch_stats* mstats;
+  int* next;
+  int dbg;  // debug: stop after stage dbg (0 = off)
+};
+
+struct Shm {
+  double* Lp;   // b columns x BT
+  double* Wp;   // (b + 1) columns x BT
+  double* scr;  // aliases Lp/Wp: QRCP register exchange (P x BT)
+  double* c0s;  // formed pivot column
+  double* xs;   // 2 x PM: swap exchange of sketch columns
+  double* vsh;  // Householder vector + coefficient
+  double* B1s;  // P x b
+  double* Ys;   // P x b
+  double* redk;
+  int* redi;
+  int* pol;    // logical position -> storage index (relative to the panel start)
+  int* permv;  // logical position -> original index
+};
+
+// Block-wide first-index argmax (numpy semantics); one barrier; result in every thread.
+__device__ __forceinline__ void bargmax(double& key, int& idx, const Shm& S, int& par) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double k2 = __shfl_down_sync(0xffffffffu, key, o);
+    const int i2 = __shfl_down_sync(0xffffffffu, idx, o);
+    if (better(k2, i2, key, idx)) {
+      key = k2;
+      idx = i2;
+    }
+  }
+  if (lane == 0) {
+    S.redk[par * BW + warp] = key;
+    S.redi[par * BW + warp] = idx;
+  }
+  __syncthreads();
+  key = S.redk[par * BW];
+  idx = S.redi[par * BW];
+#pragma unroll
+  for (int w = 1; w < BW; ++w) {
+    const double k2 = S.redk[par * BW + w];
+    const int i2 = S.redi[par * BW + w];
+    if (better(k2, i2, key, idx)) {
+      key = k2;
+      idx = i2;
+    }
+  }
+  par ^= 1;
+}
+
+__device__ __forceinline__ double bmax(double v, const Shm& S, int& par) {
+  int idx = 0;
+  bargmax(v, idx, S, par);
+  return v;
+}
+
+// Scaled Euclidean norm of x[lo, P) (core.py:122-142).
+template <int PM>
+__device__ __forceinline__ double sc_norm(const double (&x)[PM], int lo, int P) {
+  double am = 0.0;
+#pragma unroll
+  for (int r = 0; r < PM; ++r)
+    if (r >= lo && r < P) am = fmax(am, fabs(x[r]));
+  if (!(am > 0.0)) return 0.0;
+  double ss = 0.0;
+#pragma unroll
+  for (int r = 0; r < PM; ++r)
+    if (r >= lo && r < P) {
+      const double v = fabs(x[r]) / am;
+      ss = __fma_rn(v, v, ss);
+    }
+  return am * sqrt(ss);
+}
+
+// c = Lp[:, row] . Wp[:, col] over the first t panel columns (fixed order, every caller
+// that needs the same value gets the same bits).
+__device__ __forceinline__ double panel_dot(const double* Lp, const double* Wp, int row, int col, int t) {
+  double acc = 0.0;
+  for (int s = 0; s < t; ++s) acc = __fma_rn(Lp[s * BT + row], Wp[s * BT + col], acc);
+  return acc;
+}
+
+template <int PM, int MINB>
+__global__ void __launch_bounds__(BT, MINB) batched_factor_kernel(BatchParams p) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
+  const int n = p.n, P = p.P, b = p.b;
+  const int SC = max(2 * b + 1, PM);
+  Shm S;
+  {
+    double* d = reinterpret_cast<double*>(smem_raw);
+    S.Lp = d;
+    S.Wp = d + (size_t)b * BT;
+    S.scr = d;
+    d += (size_t)SC * BT;
+    S.c0s = d;
+    d += BT;
+    S.xs = d;
+    d += 2 * PM;
+    S.vsh = d;
+    d += PM + 2;
+    S.B1s = d;
+    d += PM * b;
+    S.Ys = d;
+    d += PM * b;
+    S.redk = d;
+    d += 2 * BW;
+    int* ip = reinterpret_cast<int*>(d);
+    S.redi = ip;
+    ip += 2 * BW;
+    S.pol = ip;
+    ip += BT;
+    S.permv = ip;
+  }
+  __shared__ int s_mat, s_skip;
+  __shared__ double s_tsw[2];
+  double* ws = p.ws + (size_t)blockIdx.x * (size_t)p.ws_stride;
+  double* Abuf[2] = {ws, ws + (size_t)n * n};
+  double* Lst = ws + 2 * (size_t)n * n;  // L entries keyed by (original row, column)
+  const double alpha = p.alpha;
+  const int i = tid;  // owned logical row / column
+  const bool live = i < n;
+  int par = 0;
+
+  for (;;) {
+    __syncthreads();
+    if (tid == 0) s_mat = atomicAdd(p.next, 1);
+    __syncthreads();
+    const int mat = s_mat;
+    if (mat >= p.count) break;
+    const double* A = p.A + (size_t)mat * (size_t)p.a_stride;
+    const int64_t lda = p.lda;
+    int64_t* perm_o = p.perm + (size_t)mat * n;
+    double* Lo = p.L + (size_t)mat * n * n;
+    double* dd = p.d_diag + (size_t)mat * n;
+    double* dof = p.d_off + (size_t)mat * n;
+    int8_t* pat = p.pattern + (size_t)mat * n;
+    rcp_batch_stats* ms = p.mstats + mat;
+
+    // ---- input checks (core.py:48-53, factor.py:280-281) and max|A|
+    int asym = 0, nonfin = 0;
+    double mx = 0.0;
+    if (live) {
+      for (int j = 0; j < n; ++j) {
+        const double v = A[(size_t)j * lda + i];  // (i, j)
+        const double w = A[(size_t)i * lda + j];  // (j, i)
+        if (!(v == w)) asym = 1;
+        if (!isfinite(v)) nonfin = 1;
+        mx = fmax(mx, fabs(v));
+      }
+    }
+    asym = __syncthreads_or(asym);
+    nonfin = __syncthreads_or(nonfin);
+    if (asym || nonfin) {
+      if (tid == 0) {
+        rcp_batch_stats z{};
+        z.status = asym ? RCP_ERR_NOT_SYMMETRIC : RCP_ERR_NONFINITE_INPUT;
+        z.deficient_from = -1;
+        *ms = z;
+      }
+      continue;
+    }
+    const double amax = bmax(mx, S, par);
+    if (p.dbg == 1) continue;
+
+    // ---- B = Omega A (factor.py:307-309): thread i forms sketch column i
+    double x[PM];
+#pragma unroll
+    for (int r = 0; r < PM; ++r) x[r] = 0.0;
+    if (live) {
+      for (int j = 0; j < n; ++j) {
+        const double a = A[(size_t)j * lda + i];  // A[j, i] (symmetric: coalesced)
+        const double* om = p.omegaT + (size_t)j * P;
+#pragma unroll
+        for (int r = 0; r < PM; ++r)
+          if (r < P) x[r] = __fma_rn(__ldg(om + r), a, x[r]);
+      }
+    }
+    const double beta = p.armed ? bmax(live ? sc_norm<PM>(x, 0, P) : 0.0, S, par) : 0.0;
+
+    if (p.dbg == 2) continue;
+    if (live) S.permv[i] = i;
+    long long c_mul = 0, c_add = 0, c_div = 0, c_cmp = 0;  // thread 0's op counters
+    int64_t zoff = (int64_t)P * n;
+    int recomputes = 0, n2x2 = 0, nsteps = 0, npanels = 0, def_from = -1, kdone = 0;
+    int status = RCP_OK, num_kind = 0, num_step = 0;
+    double dmax = 0.0;
+    const double* Acur = A;
+    int64_t ldA = lda;
+    int nb = 0;  // next scratch buffer
+    int k = 0;
+    if (p.armed && beta == 0.0) {  // zero sketch: deficient from the start (factor.py:510-511)
+      if (live) {
+        dd[i] = 0.0;
+        dof[i] = 0.0;
+        pat[i] = 3;
+      }
+      def_from = 0;
+      k = n;
+    }
+
+    while (k < n) {
+      const int k0 = k;
+      const int m = n - k0;
+      const int width = min(b, m);
+      ++npanels;
+      if (live && i >= k0) S.pol[i] = i - k0;
+      const bool act0 = live && i >= k0;
+      __syncthreads();
+
+      // ---- guard + partial QRCP + replay (factor.py:570-600)
+      if (p.q > 1 && m > 1) {
+        if (tid == 0) {
+          c_mul += (long long)P * (m - 1);
+          c_add += (long long)P * (m - 1);
+          c_cmp += m - 1;
+        }
+        double tsel = bmax(act0 ? sc_norm<PM>(x, 0, P) : 0.0, S, par);
+        if (p.armed && tsel < p.thr[recomputes] * beta) {
+          // fresh projection of the active block from the continuing stream (factor.py:392-404)
+          if (zoff + (int64_t)P * m > p.z_len || recomputes + 1 >= kMaxThr) {
+            status = RCP_ERR_NEED_NORMALS;
+            break;
+          }
+          if (act0) {
+#pragma unroll
+            for (int r = 0; r < PM; ++r) x[r] = 0.0;
+            const int ci = i - k0;
+            for (int j = 0; j < m; ++j) {
+              const double a = Acur[(size_t)j * ldA + ci];  // T(ci, j) = T(j, ci)
+              const double* zz = p.z + zoff + j;
+#pragma unroll
+              for (int r = 0; r < PM; ++r)
+                if (r < P) x[r] = __fma_rn(__ldg(zz + (size_t)r * m), a, x[r]);
+            }
+          }
+          zoff += (int64_t)P * m;
+          ++recomputes;
+          tsel = bmax(act0 ? sc_norm<PM>(x, 0, P) : 0.0, S, par);
+          if (tsel < p.thr[recomputes] * beta) {  // "stop": deficient tail (factor.py:381-385)
+            if (act0) {
+              dd[i] = 0.0;
+              dof[i] = 0.0;
+              pat[i] = 3;
+            }
+            def_from = k0;
+            kdone = k0;
+            k = n;
+            break;
+          }
+        }
+        const int qn = min(min(p.q, width), min(m, P));
+        double y[PM];
+#pragma unroll
+        for (int r = 0; r < PM; ++r) y[r] = x[r];
+        int slot = act0 ? i - k0 : INT_MAX;
+        for (int s = 0; s < qn; ++s) {
+          double key = (slot >= s && slot != INT_MAX) ? sc_norm<PM>(y, s, P) : -1.0;
+          int idx = (slot >= s) ? slot : INT_MAX;
+          bargmax(key, idx, S, par);
+          const int sw = idx;
+          const bool winner = (slot == sw);
+          if (winner) slot = s;
+          else if (slot == s) slot = sw;
+          if (winner) {
+            double ss = 0.0;
+#pragma unroll
+            for (int r = 0; r < PM; ++r)
+              if (r >= s && r < P) ss = __fma_rn(y[r], y[r], ss);
+            const double xn = sqrt(ss);
+            int skip = xn == 0.0;
+            if (!skip) {
+              double vv = 0.0;
+#pragma unroll
+              for (int r = 0; r < PM; ++r)
+                if (r >= s && r < P) {
+                  double v = y[r];
+                  if (r == s) v = v + copysign(xn, v != 0.0 ? v : 1.0);
+                  S.vsh[r] = v;
+                  vv = __fma_rn(v, v, vv);
+                }
+              if (vv == 0.0) skip = 1;
+              else S.vsh[PM] = 2.0 / vv;
+            }
+            s_skip = skip;
+          }
+          __syncthreads();
+          if (!s_skip && slot > s && slot != INT_MAX) {
+            double dot = 0.0;
+#pragma unroll
+            for (int r = 0; r < PM; ++r)
+              if (r >= s && r < P) dot = __fma_rn(S.vsh[r], y[r], dot);
+            const double u = S.vsh[PM] * dot;
+#pragma unroll
+            for (int r = 0; r < PM; ++r)
+              if (r >= s && r < P) y[r] = __dsub_rn(y[r], __dmul_rn(S.vsh[r], u));
+          }
+        }
+        if (tid == 0)
+          for (int s = 0; s < qn; ++s) {
+            c_cmp += m - 1 - s;
+            c_mul += 2LL * P * (m - s);
+            c_add += 2LL * P * (m - s);
+          }
+        // replay: column at panel slot i-k0 moves to logical k0 + slot (same transpositions)
+        int pvi = 0;
+        if (act0) {
+          pvi = S.permv[i];
+#pragma unroll
+          for (int r = 0; r < PM; ++r)
+            if (r < P) S.scr[(size_t)r * BT + k0 + slot] = x[r];
+        }
+        __syncthreads();
+        if (act0) {
+          S.permv[k0 + slot] = pvi;
+          S.pol[k0 + slot] = i - k0;
+#pragma unroll
+          for (int r = 0; r < PM; ++r)
+            if (r < P) x[r] = S.scr[(size_t)r * BT + i];
+        }
+        __syncthreads();
+      }
+
+      if (p.dbg == 3) {
+        status = 99;
+        break;
+      }
+      // ---- SBKP steps (factor.py:602-634)
+      auto T = [&](int a, int c) -> double { return Acur[(size_t)c * ldA + a]; };
+      double tk = act0 ? T(S.pol[i], S.pol[k0]) : 0.0;
+      int t = 0;
+      bool deferred = false;
+      while (t < width && k0 + t < n) {
+        const int kk = k0 + t;
+        const int mm = n - kk;
+        const bool act = live && i >= kk;
+        double c = 0.0;
+        if (act) {
+          c = __dsub_rn(tk, panel_dot(S.Lp, S.Wp, i, kk, t));
+          S.c0s[i] = c;
+        }
+        double lam = (act && i > kk) ? fabs(c) : -1.0;
+        int r = (act && i > kk) ? i : INT_MAX;
+        bargmax(lam, r, S, par);
+        const double akk = S.c0s[kk];
+        int kind, s;
+        double dr = 0.0, tr = 0.0;
+        if (mm == 1 || lam == 0.0) {
+          kind = 0;
+          s = 1;
+        } else if (fabs(akk) >= alpha * lam) {
+          kind = 1;
+          s = 1;
+        } else {
+          const int pr = S.pol[r];
+          if (act) tr = T(S.pol[i], pr);
+          dr = __dsub_rn(T(pr, pr), panel_dot(S.Lp, S.Wp, r, r, t));
+          if (fabs(dr) >= alpha * lam) {
+            kind = 2;
+            s = 1;
+          } else {
+            kind = 3;
+            s = 2;
+          }
+        }
+        deferred = s == 2 && t > 0 && t + 2 > width;
+        if (tid == 0) {  // op counters of _decide / _eliminate (factor.py:350-367, 414-489)
+          const long long colc = t > 0 ? (long long)t * mm : 0;
+          c_mul += colc;
+          c_add += colc;
+          c_cmp += mm >= 2 ? mm - 2 : 0;
+          if (kind >= 2 && t > 0) {
+            c_mul += t;
+            c_add += t;
+          }
+          if (!deferred) {
+            c_mul += colc * s;
+            c_add += colc * s;
+            const long long w = mm - s;
+            if (kind != 0) {
+              if (s == 1) {
+                c_div += w;
+              } else {
+                c_div += 2 * w;
+                c_mul += 4 * w + 2;
+                c_add += 2 * w + 1;
+              }
+            }
+          }
+        }
+        if (deferred) break;  // defer (factor.py:622-623)
+
+        // symmetric swaps as bookkeeping + register/smem row exchanges (factor.py:624-630)
+        int sa = -1, sb = -1;
+        if (kind == 2) {
+          sa = kk;
+          sb = r;
+        } else if (kind == 3 && r != kk + 1) {
+          sa = kk + 1;
+          sb = r;
+        }
+        if (sa >= 0) {
+          if (tid == sa || tid == sb) {
+            const int h = tid == sa ? 0 : 1;
+#pragma unroll
+            for (int q = 0; q < PM; ++q)
+              if (q < P) S.xs[h * PM + q] = x[q];
+            s_tsw[h] = tr;
+          }
+          if (tid < t) {
+            double* Lc = S.Lp + (size_t)tid * BT;
+            const double u = Lc[sa];
+            Lc[sa] = Lc[sb];
+            Lc[sb] = u;
+          } else if (tid >= 32 && tid < 32 + t) {
+            double* Wc = S.Wp + (size_t)(tid - 32) * BT;
+            const double u = Wc[sa];
+            Wc[sa] = Wc[sb];
+            Wc[sb] = u;
+          } else if (tid == 64) {
+            int u = S.pol[sa];
+            S.pol[sa] = S.pol[sb];
+            S.pol[sb] = u;
+            u = S.permv[sa];
+            S.permv[sa] = S.permv[sb];
+            S.permv[sb] = u;
+          } else if (tid == 65 && kind == 3) {
+            const double u = S.c0s[sa];
+            S.c0s[sa] = S.c0s[sb];
+            S.c0s[sb] = u;
+          }
+        }
+        __syncthreads();
+        if (sa >= 0 && (tid == sa || tid == sb)) {
+          const int h = tid == sa ? 1 : 0;
+#pragma unroll
+          for (int q = 0; q < PM; ++q)
+            if (q < P) x[q] = S.xs[h * PM + q];
+          tr = s_tsw[h];
+        }
+
+        // D block and checks (factor.py:202-226, 455-466): identical in every thread
+        double d11, d21 = 0.0, d22 = 0.0, det = 1.0;
+        int nk = 0;
+        if (kind <= 1) {
+          d11 = akk;
+          if (!isfinite(d11)) nk = 3;
+        } else if (kind == 2) {
+          d11 = dr;
+          if (!isfinite(d11)) nk = 3;
+        } else {
+          d11 = akk;
+          d21 = S.c0s[kk + 1];
+          d22 = dr;
+          det = __dsub_rn(__dmul_rn(d11, d22), __dmul_rn(d21, d21));
+          if (det == 0.0) {
+            nk = 2;
+          } else if (!isfinite(d11) || !isfinite(d21) || !isfinite(d22)) {
+            nk = 3;
+          } else {
+            const double a21 = fabs(d21);
+            const double dt = __dsub_rn(__dmul_rn(d11, d22), __dmul_rn(a21, a21));
+            const double bound =
+                __dmul_rn(__dmul_rn(__dmul_rn(__dsub_rn(1.0, __dmul_rn(alpha, alpha)), a21), a21), __dsub_rn(1.0, 1e-12));
+            if (fabs(dt) < bound) nk = 4;
+          }
+        }
+        if (nk) {
+          status = RCP_ERR_NUMERICAL;
+          num_kind = nk;
+          num_step = kk;
+          break;
+        }
+        // multipliers and writes (factor.py:467-480): W keeps the unscaled columns
+        int lerr = 0;
+        if (act) {
+          if (kind <= 1) {
+            S.Wp[(size_t)t * BT + i] = c;
+            if (i > kk) {
+              const double l = kind == 0 ? 0.0 : __ddiv_rn(c, d11);
+              if (!isfinite(l)) lerr = 1;
+              S.Lp[(size_t)t * BT + i] = l;
+            }
+          } else if (kind == 2) {
+            const double c0 = __dsub_rn(tr, panel_dot(S.Lp, S.Wp, i, kk, t));
+            S.Wp[(size_t)t * BT + i] = c0;
+            if (i > kk) {
+              const double l = __ddiv_rn(c0, d11);
+              if (!isfinite(l)) lerr = 1;
+              S.Lp[(size_t)t * BT + i] = l;
+            }
+          } else {
+            const double c0 = S.c0s[i];
+            const double c1 = __dsub_rn(tr, panel_dot(S.Lp, S.Wp, i, kk + 1, t));
+            S.Wp[(size_t)t * BT + i] = c0;
+            S.Wp[(size_t)(t + 1) * BT + i] = c1;
+            if (i > kk + 1) {
+              const double l1 = __ddiv_rn(__dsub_rn(__dmul_rn(c0, d22), __dmul_rn(d21, c1)), det);
+              const double l2 = __ddiv_rn(__dsub_rn(__dmul_rn(d11, c1), __dmul_rn(d21, c0)), det);
+              if (!isfinite(l1) || !isfinite(l2)) lerr = 1;
+              S.Lp[(size_t)t * BT + i] = l1;
+              S.Lp[(size_t)(t + 1) * BT + i] = l2;
+            } else if (i == kk + 1) {
+              S.Lp[(size_t)t * BT + i] = 0.0;  // L[k+1, k] of a 2x2 block is exactly zero
+            }
+          }
+        }
+        if (tid == 0) {
+          dd[kk] = d11;
+          dof[kk] = kind == 3 ? d21 : 0.0;
+          pat[kk] = kind == 3 ? 1 : 0;
+          dmax = fmax(dmax, fabs(d11));
+          if (kind == 3) {
+            dd[kk + 1] = d22;
+            dof[kk + 1] = 0.0;
+            pat[kk + 1] = 2;
+            dmax = fmax(dmax, fmax(fabs(d21), fabs(d22)));
+            ++n2x2;
+          }
+          ++nsteps;
+        }
+        // prefetch the next pivot column (pol is final for this step)
+        const int kn = kk + s;
+        if (t + s < width && kn < n && live && i >= kn) tk = T(S.pol[i], S.pol[kn]);
+        lerr = __syncthreads_or(lerr);
+        if (lerr) {
+          status = RCP_ERR_NUMERICAL;
+          num_kind = 3;
+          num_step = kk;
+          break;
+        }
+        t += s;
+        if (p.dbg == 4) {
+          status = 99;
+          break;
+        }
+      }
+      if (p.dbg == 5) status = 99;
+      if (status != RCP_OK) break;
+      (void)deferred;
+      const int k_end = k0 + t;
+      const int mp = n - k_end;
+
+      // L columns of this panel, keyed by original row index (rows never move afterwards)
+      if (act0) {
+        double* dst = Lst + (size_t)S.permv[i] * n + k0;
+        for (int s = 0; s < t; ++s)
+          if (i > k0 + s) dst[s] = S.Lp[(size_t)s * BT + i];
+      }
+
+      if (mp > 0 && t > 0) {
+        // ---- trailing update A22 -= L21 W21^T, lower computed + mirrored (factor.py:369-379)
+        double* An = Abuf[nb];
+        const int nb4 = (mp + 3) >> 2;
+        const int ntiles = nb4 * (nb4 + 1) / 2;
+        for (int tile = tid; tile < ntiles; tile += BT) {
+          int I = (int)((sqrt(8.0 * tile + 1.0) - 1.0) * 0.5);
+          while ((I + 1) * (I + 2) / 2 <= tile) ++I;
+          while (I * (I + 1) / 2 > tile) --I;
+          const int J = tile - I * (I + 1) / 2;
+          const int i0 = k_end + 4 * I, j0 = k_end + 4 * J;
+          double acc[4][4];
+#pragma unroll
+          for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int c2 = 0; c2 < 4; ++c2) acc[a][c2] = 0.0;
+          for (int s = 0; s < t; ++s) {
+            const double* Lc = S.Lp + (size_t)s * BT;
+            const double* Wc = S.Wp + (size_t)s * BT;
+            double lv[4], wv[4];
+#pragma unroll
+            for (int a = 0; a < 4; ++a) {
+              lv[a] = (i0 + a < n) ? Lc[i0 + a] : 0.0;
+              wv[a] = (j0 + a < n) ? Wc[j0 + a] : 0.0;
+            }
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+#pragma unroll
+              for (int c2 = 0; c2 < 4; ++c2) acc[a][c2] = __fma_rn(lv[a], wv[c2], acc[a][c2]);
+          }
+#pragma unroll
+          for (int c2 = 0; c2 < 4; ++c2) {
+            const int j = j0 + c2;
+            if (j >= n) continue;
+            const int pj = S.pol[j];
+#pragma unroll
+            for (int a = 0; a < 4; ++a) {
+              const int ii = i0 + a;
+              if (ii >= n || ii < j) continue;
+              const double v = __dsub_rn(T(S.pol[ii], pj), acc[a][c2]);
+              An[(size_t)(j - k_end) * mp + (ii - k_end)] = v;
+              An[(size_t)(ii - k_end) * mp + (j - k_end)] = v;
+            }
+          }
+        }
+        if (tid == 0) {
+          c_mul += (long long)t * ((long long)mp * (mp + 1) / 2);
+          c_add += (long long)t * ((long long)mp * (mp + 1) / 2);
+        }
+        // ---- sketch correction B2 -= (B1 L11^-T) L21^T (factor.py:554-565)
+        if (p.q > 1) {
+          if (live && i >= k0 && i < k_end) {
+#pragma unroll
+            for (int q = 0; q < PM; ++q)
+              if (q < P) S.B1s[q * b + (i - k0)] = x[q];
+          }
+          __syncthreads();
+          if (tid < P) {
+            for (int s = 0; s < t; ++s) {
+              double yv = S.B1s[tid * b + s];
+              for (int u = 0; u < s; ++u) yv = __fma_rn(-S.Ys[tid * b + u], S.Lp[(size_t)u * BT + k0 + s], yv);
+              S.Ys[tid * b + s] = yv;
+            }
+          }
+          __syncthreads();
+          if (live && i >= k_end) {
+#pragma unroll
+            for (int q = 0; q < PM; ++q)
+              if (q < P) {
+                double acc = 0.0;
+                for (int s = 0; s < t; ++s) acc = __fma_rn(S.Ys[q * b + s], S.Lp[(size_t)s * BT + i], acc);
+                x[q] = __dsub_rn(x[q], acc);
+              }
+          }
+          if (tid == 0) {
+            c_mul += (long long)t * P * mp + (long long)(t * (t - 1) / 2) * mp;
+            c_add += (long long)t * P * mp + (long long)(t * (t - 1) / 2) * mp;
+          }
+        }
+        Acur = An;
+        ldA = mp;
+        nb ^= 1;
+      }
+      if (p.dbg == 6) {
+        status = 99;
+        break;
+      }
+      __syncthreads();  // trailing block + Lst visible; Lp/Wp free for the next panel
+      k = k_end;
+      kdone = k_end;
+    }
+
+    if (status != RCP_OK) {
+      if (tid == 0) {
+        rcp_batch_stats z{};
+        z.status = status;
+        z.num_kind = num_kind;
+        z.num_step = num_step;
+        z.recompute_count = recomputes;
+        z.deficient_from = -1;
+        z.amax = amax;
+        *ms = z;
+      }
+      continue;
+    }
+    __syncthreads();
+    // ---- outputs: perm, L in final order (one coalesced row gather), statistics
+    if (live) perm_o[i] = S.permv[i];
+    double mm = 0.0;
+    for (int row = warp; row < n; row += BW) {
+      const double* src = Lst + (size_t)S.permv[row] * n;
+      double* dst = Lo + (size_t)row * n;
+      for (int c = lane; c < n; c += 32) {
+        double v;
+        if (c < row) {
+          v = c < kdone ? src[c] : 0.0;
+          mm = fmax(mm, fabs(v));
+        } else {
+          v = c == row ? 1.0 : 0.0;
+        }
+        dst[c] = v;
+      }
+    }
+    mm = bmax(mm, S, par);
+    if (tid == 0) {
+      rcp_batch_stats z{};
+      z.status = RCP_OK;
+      z.recompute_count = recomputes;
+      z.deficient_from = def_from;
+      z.n_2x2 = n2x2;
+      z.n_steps = nsteps;
+      z.n_panels = npanels;
+      z.amax = amax;
+      z.dmax = dmax;
+      z.max_multiplier = n > 1 ? mm : 0.0;
+      z.rho_cheap = amax == 0.0 ? (dmax == 0.0 ? 1.0 : INFINITY) : dmax / amax;
+      z.mults = c_mul;
+      z.adds = c_add;
+      z.divs = c_div;
+      z.comps = c_cmp;
+      *ms = z;
+    }
+  }
+}
+
+// ---------------------------------------------------------------- batched solve
+// x = P^T L^-T D^-1 L^-1 P b per matrix (solve.py:34-76); one CTA per matrix, L rows read
+// coalesced (row-major), 16-row blocks.
+constexpr int SB = 16;
+
+__global__ void __launch_bounds__(BT) batched_solve_kernel(int count, int n, const int64_t* __restrict__ perm,
+                                                           const double* __restrict__ L,
+                                                           const double* __restrict__ d_diag,
+                                                           const double* __restrict__ d_off,
+                                                           const int8_t* __restrict__ pattern,
+                                                           const double* b, double* x, int32_t* singular) {
+  __shared__ double y[BT];
+  __shared__ double part[BW][SB];
+  __shared__ int s_sing;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int mat = blockIdx.x; mat < count; mat += gridDim.x) {
+    const int64_t* pm = perm + (size_t)mat * n;
+    const double* Lm = L + (size_t)mat * n * n;
+    const double* dg = d_diag + (size_t)mat * n;
+    const double* df = d_off + (size_t)mat * n;
+    const int8_t* pt = pattern + (size_t)mat * n;
+    __syncthreads();
+    if (tid < n) y[tid] = b[(size_t)mat * n + pm[tid]];  // y = b[perm]
+    if (tid == 0) s_sing = 0;
+    __syncthreads();
+    // forward: unit lower L (solve.py:69-71)
+    for (int r0 = 0; r0 < n; r0 += SB) {
+      const int rb = min(SB, n - r0);
+      // y[r0 + a] -= L[r0 + a, :r0] . y[:r0]; warp w handles rows a = w, w + BW
+      for (int a = warp; a < rb; a += BW) {
+        const double* Lr = Lm + (size_t)(r0 + a) * n;
+        double acc = 0.0;
+        for (int j = lane; j < r0; j += 32) acc = __fma_rn(Lr[j], y[j], acc);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (lane == 0) part[0][a] = acc;
+      }
+      __syncthreads();
+      if (warp == 0) {
+        double v = lane < rb ? __dsub_rn(y[r0 + lane], part[0][lane]) : 0.0;
+        const double* Lb = Lm + (size_t)(r0 + (lane < rb ? lane : 0)) * n + r0;
+        for (int j = 0; j < rb; ++j) {
+          const double yj = __shfl_sync(0xffffffffu, v, j);
+          if (lane > j && lane < rb) v = __fma_rn(-Lb[j], yj, v);
+        }
+        if (lane < rb) y[r0 + lane] = v;
+      }
+      __syncthreads();
+    }
+    // block diagonal (solve.py:47-62): exact-zero blocks give zeros and the singular flag
+    double out = 0.0;
+    if (tid < n) {
+      const int8_t pk = pt[tid];
+      const double v = y[tid];
+      int sg = 0;
+      if (pk == 1) {
+        const double d11 = dg[tid], d21 = df[tid], d22 = dg[tid + 1];
+        const double det = __dsub_rn(__dmul_rn(d11, d22), __dmul_rn(d21, d21));
+        if (det == 0.0) sg = 1;
+        else out = __ddiv_rn(__dsub_rn(__dmul_rn(d22, v), __dmul_rn(d21, y[tid + 1])), det);
+      } else if (pk == 2) {
+        const double d11 = dg[tid - 1], d21 = df[tid - 1], d22 = dg[tid];
+        const double det = __dsub_rn(__dmul_rn(d11, d22), __dmul_rn(d21, d21));
+        if (det == 0.0) sg = 1;
+        else out = __ddiv_rn(__dsub_rn(__dmul_rn(d11, v), __dmul_rn(d21, y[tid - 1])), det);
+      } else {
+        const double d = dg[tid];
+        if (d == 0.0) sg = 1;
+        else out = __ddiv_rn(v, d);
+      }
+      if (sg) atomicOr(&s_sing, 1);
+    }
+    __syncthreads();
+    if (tid < n) y[tid] = out;
+    __syncthreads();
+    // backward with L^T (solve.py:72-73): blocks from the bottom; after a block is solved,
+    // y[:r0] -= L[r0:r0+rb, :r0]^T x[r0:r0+rb] (rows of L read coalesced)
+    for (int r1 = n; r1 > 0; r1 -= SB) {
+      const int r0 = max(0, r1 - SB);
+      const int rb = r1 - r0;
+      if (warp == 0) {
+        double v = lane < rb ? y[r0 + lane] : 0.0;
+        for (int j = rb - 1; j >= 0; --j) {
+          const double xj = __shfl_sync(0xffffffffu, v, j);
+          if (lane < j) v = __fma_rn(-Lm[(size_t)(r0 + j) * n + r0 + lane], xj, v);
+        }
+        if (lane < rb) y[r0 + lane] = v;
+      }
+      __syncthreads();
+      if (tid < r0) {
+        double acc = 0.0;
+        for (int a = 0; a < rb; ++a) acc = __fma_rn(Lm[(size_t)(r0 + a) * n + tid], y[r0 + a], acc);
+        y[tid] = __dsub_rn(y[tid], acc);
+      }
+      __syncthreads();
+    }
+    if (tid < n) x[(size_t)mat * n + pm[tid]] = y[tid];  // x[perm] = v
+    if (tid == 0 && singular) singular[mat] = s_sing;
+  }
+}
+
+__global__ void transpose_omega_kernel(const double* __restrict__ om, int P, int n, double* __restrict__ omT) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j < n)
+    for (int r = 0; r < P; ++r) omT[(size_t)j * P + r] = om[(size_t)r * n + j];
+}
+
+int pick_pm(int P) {
+  if (P <= 8) return 8;
+  if (P <= 16) return 16;
+  if (P <= 24) return 24;
+  if (P <= 32) return 32;
+  if (P <= 48) return 48;
+  return 64;
+}
+
+size_t factor_smem(int PM, int b) {
+  const int SC = std::max(2 * b + 1, PM);
+  size_t d = (size_t)SC * BT + BT + 2 * PM + PM + 2 + 2 * (size_t)PM * b + 2 * BW;
+  return d * 8 + (2 * BW + 2 * BT) * 4;
+}
+
+template <int PM, int MINB>
+cudaError_t launch_pm(const BatchParams& prm, int grid, size_t smem, cudaStream_t st) {
+  cudaError_t e = cudaFuncSetAttribute(batched_factor_kernel<PM, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem);
+  if (e != cudaSuccess) return e;
+  batched_factor_kernel<PM, MINB><<<grid, BT, smem, st>>>(prm);
+  return cudaGetLastError();
+}
+
+int resident_ctas(int PM) { return PM <= 32 ? 2 : 1; }
+
+int sm_count() {
+  int dev = 0, sms = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return sms;
+}
+
+int64_t ws_stride_doubles(int64_t n) { return ((3 * n * n + 31) / 32) * 32; }
+
+}  // namespace
+
+extern "C" {
+
+size_t rcp_batched_workspace_bytes(int64_t n, const rcp_config* cfg) {
+  if (!cfg || n < 1 || n > BT || cfg->p < 1 || cfg->p > 64 || cfg->b < 1 || cfg->b > kMaxB) return 0;
+  const int grid = sm_count() * resident_ctas(pick_pm(cfg->p));
+  const size_t om_bytes = ((size_t)n * cfg->p * 8 + 255) & ~size_t(255);
+  return (size_t)grid * (size_t)ws_stride_doubles(n) * 8 + 256 + om_bytes;
+}
+
+int rcp_factor_batched(const rcp_config* cfg, int64_t count, int64_t n, const double* a, int64_t lda,
+                       int64_t a_stride, const double* normals, int64_t normals_len, void* workspace,
+                       size_t workspace_bytes, int64_t* perm, double* L, double* d_diag, double* d_off,
+                       int8_t* pattern, rcp_batch_stats* mstats, void* cuda_stream) {
+  if (!cfg || count < 0 || n < 1 || lda < n || a_stride < n * lda - (lda - n)) return RCP_ERR_INVALID_ARG;
+  if (cfg->p < 1 || cfg->b < 1 || cfg->robust_r < 0 || cfg->p < cfg->q) return RCP_ERR_INVALID_ARG;
+  if (!(cfg->q == 1 || cfg->q == cfg->b)) return RCP_ERR_INVALID_ARG;
+  if (n > BT || cfg->b > kMaxB || cfg->p > 64 || cfg->q == 1) return RCP_ERR_UNSUPPORTED;
+  if (count > INT_MAX || normals_len < (int64_t)cfg->p * n) return RCP_ERR_INVALID_ARG;
+  if (count == 0) return RCP_OK;
+  const size_t need = rcp_batched_workspace_bytes(n, cfg);
+  if (!workspace || workspace_bytes < need) return RCP_ERR_WORKSPACE;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(cuda_stream);
+  const int P = cfg->p;
+  const int PM = pick_pm(P);
+  const int grid = sm_count() * resident_ctas(PM);
+
+  // workspace: [counter | omegaT (n x P) | per-CTA scratch]
+  unsigned char* ws = static_cast<unsigned char*>(workspace);
+  int* counter = reinterpret_cast<int*>(ws);
+  double* omegaT = reinterpret_cast<double*>(ws + 256);
+  const size_t om_bytes = ((size_t)n * P * 8 + 255) & ~size_t(255);
+  double* scratch = reinterpret_cast<double*>(ws + 256 + om_bytes);
+  cudaError_t e = cudaMemsetAsync(counter, 0, sizeof(int), st);
+  if (e != cudaSuccess) return RCP_ERR_CUDA;
+  // Omega^T (n x P) from the row-major Omega at the head of the normal stream
+  transpose_omega_kernel<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(normals, P, (int)n, omegaT);
+  if (cudaGetLastError() != cudaSuccess) return RCP_ERR_CUDA;
+  BatchParams prm{};
+  prm.count = (int)count;
+  prm.n = (int)n;
+  prm.P = P;
+  prm.b = cfg->b;
+  prm.q = cfg->q;
+  prm.armed = cfg->robust_r >= 1;
+  prm.alpha = std::sqrt(2.0) / 2.0;
+  for (int j = 0; j < kMaxThr; ++j)
+    prm.thr[j] = prm.armed ? std::pow(DBL_EPSILON, (double)(j + 1) / cfg->robust_r) : 0.0;
+  prm.A = a;
+  prm.lda = lda;
+  prm.a_stride = a_stride;
+  prm.omegaT = omegaT;
+  prm.z = normals;
+  prm.z_len = normals_len;
+  prm.ws = scratch;
+  prm.ws_stride = ws_stride_doubles(n);
+  prm.perm = perm;
+  prm.L = L;
+  prm.d_diag = d_diag;
+  prm.d_off = d_off;
+  prm.pattern = pattern;
+  prm.mstats = mstats;
+  prm.next = counter;
+  if (const char* dbg = std::getenv("RCP_BATCH_DBG")) prm.dbg = std::atoi(dbg);
+  const size_t smem = factor_smem(PM, cfg->b);
+  switch (PM) {
+    case 8: e = launch_pm<8, 2>(prm, grid, smem, st); break;
+    case 16: e = launch_pm<16, 2>(prm, grid, smem, st); break;
+    case 24: e = launch_pm<24, 2>(prm, grid, smem, st); break;
+    case 32: e = launch_pm<32, 2>(prm, grid, smem, st); break;
+    case 48: e = launch_pm<48, 1>(prm, grid, smem, st); break;
+    default: e = launch_pm<64, 1>(prm, grid, smem, st); break;
+  }
+  return e == cudaSuccess ? RCP_OK : RCP_ERR_CUDA;
+}
+
+int rcp_solve_batched(int64_t count, int64_t n, const int64_t* perm, const double* L, const double* d_diag,
+                      const double* d_off, const int8_t* pattern, const double* b, double* x, int32_t* singular,
+                      void* cuda_stream) {
+  if (count < 0 || n < 1 || n > BT || count > INT_MAX) return RCP_ERR_INVALID_ARG;
+  if (count == 0) return RCP_OK;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(cuda_stream);
+  const int grid = (int)std::min<int64_t>(count, (int64_t)sm_count() * 8);
+  batched_solve_kernel<<<grid, BT, 0, st>>>((int)count, (int)n, perm, L, d_diag, d_off, pattern, b, x, singular);
+  return cudaGetLastError() == cudaSuccess ? RCP_OK : RCP_ERR_CUDA;
+}
+
+}  // extern "C"

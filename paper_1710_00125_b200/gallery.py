@@ -73,3 +73,20 @@ def scaled_member(n: int, seed: int, scaled: bool) -> np.ndarray:
 
 def rhs(n: int, seed: int = 1) -> np.ndarray:
     return _gen(seed).standard_normal(n)
+
+
+def c5_batch_device(count: int, n: int = 256, seed: int = 0, scaled_every: int = 10, device="cuda"):
+    """Config-5 stack generated on the device (bench input; same distribution as
+    :func:`scaled_member`, not the same bits): symmetrised N(0,1) matrices, every
+    ``scaled_every``-th one scaled as D A D with D = diag(10^U(-6, 6)) and re-mirrored."""
+    import torch
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+    a = torch.randn(count, n, n, dtype=torch.float64, device=device, generator=g)
+    a = torch.tril(a) + torch.tril(a, -1).transpose(1, 2)
+    if scaled_every:
+        idx = torch.arange(0, count, scaled_every, device=device)
+        d = 10.0 ** (torch.rand(idx.numel(), n, dtype=torch.float64, device=device, generator=g) * 12.0 - 6.0)
+        s = d[:, :, None] * a[idx] * d[:, None, :]
+        a[idx] = torch.tril(s) + torch.tril(s, -1).transpose(1, 2)
+    return a
