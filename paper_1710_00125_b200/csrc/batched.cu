@@ -421,6 +421,27 @@ __global__ void __launch_bounds__(BT, MINB) batched_factor_kernel(BatchParams p)
           }
         }
         deferred = s == 2 && t > 0 && t + 2 > width;
+        if (p.dbg == 9) {  // debug: every thread must have taken the same decision
+          __shared__ long long s_chk[4];
+          __syncthreads();
+          if (tid == 0) {
+            s_chk[0] = kind;
+            s_chk[1] = r;
+            s_chk[2] = __double_as_longlong(dr);
+            s_chk[3] = __double_as_longlong(lam);
+          }
+          __syncthreads();
+          const int bad = (s_chk[0] != kind) | ((s_chk[1] != r) << 1) |
+                          ((s_chk[2] != __double_as_longlong(dr)) << 2) | ((s_chk[3] != __double_as_longlong(lam)) << 3);
+          if (__syncthreads_or(bad)) {
+            if (bad) atomicOr(&s_skip, bad << 8);
+            __syncthreads();
+            status = 98;
+            num_kind = s_skip >> 8;
+            num_step = kk;
+            break;
+          }
+        }
         if (tid == 0) {  // op counters of _decide / _eliminate (factor.py:350-367, 414-489)
           const long long colc = t > 0 ? (long long)t * mm : 0;
           c_mul += colc;
@@ -457,6 +478,7 @@ __global__ void __launch_bounds__(BT, MINB) batched_factor_kernel(BatchParams p)
           sb = r;
         }
         if (sa >= 0) {
+          __syncthreads();  // every thread has read pol / Lp / Wp rows for this decision
           if (tid == sa || tid == sb) {
             const int h = tid == sa ? 0 : 1;
 #pragma unroll
@@ -688,7 +710,7 @@ __global__ void __launch_bounds__(BT, MINB) batched_factor_kernel(BatchParams p)
         ldA = mp;
         nb ^= 1;
       }
-      if (p.dbg == 6) {
+      if (p.dbg == 6 || (p.dbg > 100 && npanels >= p.dbg - 100)) {
         status = 99;
         break;
       }
@@ -711,6 +733,7 @@ __global__ void __launch_bounds__(BT, MINB) batched_factor_kernel(BatchParams p)
       continue;
     }
     __syncthreads();
+    if (p.dbg == 7) continue;
     // ---- outputs: perm, L in final order (one coalesced row gather), statistics
     if (live) perm_o[i] = S.permv[i];
     double mm = 0.0;
@@ -917,7 +940,8 @@ int rcp_factor_batched(const rcp_config* cfg, int64_t count, int64_t n, const do
   cudaStream_t st = reinterpret_cast<cudaStream_t>(cuda_stream);
   const int P = cfg->p;
   const int PM = pick_pm(P);
-  const int grid = sm_count() * resident_ctas(PM);
+  int grid = sm_count() * resident_ctas(PM);
+  if (const char* g = std::getenv("RCP_BATCH_GRID")) grid = std::max(1, std::min(grid, std::atoi(g)));
 
   // workspace: [counter | omegaT (n x P) | per-CTA scratch]
   unsigned char* ws = static_cast<unsigned char*>(workspace);
