@@ -43,7 +43,7 @@ struct BatchParams {
   double thr[kMaxThr];  // thr[j] = eps ** ((j + 1) / robust_r)  (factor.py:316, 406), host pow
   const double* A;
   int64_t lda, a_stride;
-  const double* omegaT;  // n x P: omegaT[j * P + r] = Omega[r, j]
+  const double* omegaT;  // n x PM (zero padded): omegaT[j * PM + r] = Omega[r, j]
   const double* z;       // normal stream; z[0, P n) = Omega row-major
   int64_t z_len;
   double* ws;
@@ -68,6 +68,7 @@ struct Shm {
   double* B1s;  // P x b
   double* Ys;   // P x b
   double* redk;
+  double* cand;  // 2 x BW x PM: per-warp QRCP candidate residuals (double-buffered)
   int* redi;
   int* pol;    // logical position -> storage index (relative to the panel start)
   int* permv;  // logical position -> original index
@@ -128,6 +129,20 @@ __device__ __forceinline__ double sc_norm(const double (&x)[PM], int lo, int P) 
   return am * sqrt(ss);
 }
 
+// Residual column norm for the QRCP pivot choice: plain sqrt(sum x^2) when that is safe
+// from overflow/underflow, the scaled form of core.py:122-142 otherwise (same ordering up
+// to rounding; exact ties, e.g. zero columns, stay exact ties).
+template <int PM>
+__device__ __forceinline__ double res_norm(const double (&x)[PM], int lo, int P) {
+  double ss = 0.0;
+#pragma unroll
+  for (int r = 0; r < PM; ++r)
+    if (r >= lo && r < P) ss = __fma_rn(x[r], x[r], ss);
+  if (ss == 0.0) return 0.0;
+  if (ss >= 1e-280 && ss <= 1e280) return sqrt(ss);
+  return sc_norm<PM>(x, lo, P);
+}
+
 // c = Lp[:, row] . Wp[:, col] over the first t panel columns (fixed order, every caller
 // that needs the same value gets the same bits).
 __device__ __forceinline__ double panel_dot(const double* Lp, const double* Wp, int row, int col, int t) {
@@ -162,6 +177,8 @@ __global__ void __launch_bounds__(BT, MINB) batched_factor_kernel(BatchParams p)
     d += PM * b;
     S.redk = d;
     d += 2 * BW;
+    S.cand = d;
+    d += 2 * BW * PM;
     int* ip = reinterpret_cast<int*>(d);
     S.redi = ip;
     ip += 2 * BW;
@@ -174,6 +191,7 @@ __global__ void __launch_bounds__(BT, MINB) batched_factor_kernel(BatchParams p)
   double* ws = p.ws + (size_t)blockIdx.x * (size_t)p.ws_stride;
   double* Abuf[2] = {ws, ws + (size_t)n * n};
   double* Lst = ws + 2 * (size_t)n * n;  // L entries keyed by (original row, column)
+  double* Bx = ws + 3 * (size_t)n * n;   // sketch, P x n (ld n)
   const double alpha = p.alpha;
   const int i = tid;  // owned logical row / column
   const bool live = i < n;
@@ -221,19 +239,31 @@ __global__ void __launch_bounds__(BT, MINB) batched_factor_kernel(BatchParams p)
     if (p.dbg == 1) continue;
 
     // ---- B = Omega A (factor.py:307-309): thread i forms sketch column i
-    double x[PM];
+    // the sketch lives in per-CTA global scratch Bx[r * n + i] (L1/L2-resident), loaded into
+    // registers only for the QRCP of each panel
+    double nrm0 = 0.0;
+    {
+      double x[PM];
 #pragma unroll
-    for (int r = 0; r < PM; ++r) x[r] = 0.0;
-    if (live) {
-      for (int j = 0; j < n; ++j) {
-        const double a = A[(size_t)j * lda + i];  // A[j, i] (symmetric: coalesced)
-        const double* om = p.omegaT + (size_t)j * P;
+      for (int r = 0; r < PM; ++r) x[r] = 0.0;
+      if (live) {
+        for (int j = 0; j < n; ++j) {
+          const double a = A[(size_t)j * lda + i];  // A[j, i] (symmetric: coalesced)
+          const double* om = p.omegaT + (size_t)j * PM;
+#pragma unroll
+          for (int r = 0; r < PM; r += 2) {
+            const double2 o2 = __ldg(reinterpret_cast<const double2*>(om + r));
+            x[r] = __fma_rn(o2.x, a, x[r]);
+            x[r + 1] = __fma_rn(o2.y, a, x[r + 1]);
+          }
+        }
 #pragma unroll
         for (int r = 0; r < PM; ++r)
-          if (r < P) x[r] = __fma_rn(__ldg(om + r), a, x[r]);
+          if (r < P) Bx[(size_t)r * n + i] = x[r];
+        nrm0 = sc_norm<PM>(x, 0, P);
       }
     }
-    const double beta = p.armed ? bmax(live ? sc_norm<PM>(x, 0, P) : 0.0, S, par) : 0.0;
+    const double beta = p.armed ? bmax(nrm0, S, par) : 0.0;
 
     if (p.dbg == 2) continue;
     if (live) S.permv[i] = i;
@@ -272,7 +302,10 @@ __global__ void __launch_bounds__(BT, MINB) batched_factor_kernel(BatchParams p)
           c_add += (long long)P * (m - 1);
           c_cmp += m - 1;
         }
-        double tsel = bmax(act0 ? sc_norm<PM>(x, 0, P) : 0.0, S, par);
+        double y[PM];
+#pragma unroll
+        for (int r = 0; r < PM; ++r) y[r] = (act0 && r < P) ? Bx[(size_t)r * n + i] : 0.0;
+        double tsel = bmax(act0 ? sc_norm<PM>(y, 0, P) : 0.0, S, par);
         if (p.armed && tsel < p.thr[recomputes] * beta) {
           // fresh projection of the active block from the continuing stream (factor.py:392-404)
           if (zoff + (int64_t)P * m > p.z_len || recomputes + 1 >= kMaxThr) {
@@ -281,19 +314,22 @@ __global__ void __launch_bounds__(BT, MINB) batched_factor_kernel(BatchParams p)
           }
           if (act0) {
 #pragma unroll
-            for (int r = 0; r < PM; ++r) x[r] = 0.0;
+            for (int r = 0; r < PM; ++r) y[r] = 0.0;
             const int ci = i - k0;
             for (int j = 0; j < m; ++j) {
               const double a = Acur[(size_t)j * ldA + ci];  // T(ci, j) = T(j, ci)
               const double* zz = p.z + zoff + j;
 #pragma unroll
               for (int r = 0; r < PM; ++r)
-                if (r < P) x[r] = __fma_rn(__ldg(zz + (size_t)r * m), a, x[r]);
+                if (r < P) y[r] = __fma_rn(__ldg(zz + (size_t)r * m), a, y[r]);
             }
+#pragma unroll
+            for (int r = 0; r < PM; ++r)
+              if (r < P) Bx[(size_t)r * n + i] = y[r];
           }
           zoff += (int64_t)P * m;
           ++recomputes;
-          tsel = bmax(act0 ? sc_norm<PM>(x, 0, P) : 0.0, S, par);
+          tsel = bmax(act0 ? sc_norm<PM>(y, 0, P) : 0.0, S, par);
           if (tsel < p.thr[recomputes] * beta) {  // "stop": deficient tail (factor.py:381-385)
             if (act0) {
               dd[i] = 0.0;
@@ -307,51 +343,79 @@ __global__ void __launch_bounds__(BT, MINB) batched_factor_kernel(BatchParams p)
           }
         }
         const int qn = min(min(p.q, width), min(m, P));
-        double y[PM];
-#pragma unroll
-        for (int r = 0; r < PM; ++r) y[r] = x[r];
         int slot = act0 ? i - k0 : INT_MAX;
         for (int s = 0; s < qn; ++s) {
-          double key = (slot >= s && slot != INT_MAX) ? sc_norm<PM>(y, s, P) : -1.0;
+          // one barrier per QRCP step: each warp publishes its best column's residual
+          // (speculative Householder source) next to its key; every thread then picks the
+          // winner and forms the reflector itself (identical arithmetic in every thread)
+          double key = (slot >= s && slot != INT_MAX) ? res_norm<PM>(y, s, P) : -1.0;
           int idx = (slot >= s) ? slot : INT_MAX;
-          bargmax(key, idx, S, par);
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) {
+            const double k2 = __shfl_xor_sync(0xffffffffu, key, o);
+            const int i2 = __shfl_xor_sync(0xffffffffu, idx, o);
+            if (better(k2, i2, key, idx)) {
+              key = k2;
+              idx = i2;
+            }
+          }
+          double* cw = S.cand + ((size_t)par * BW + warp) * PM;
+          if (slot == idx) {
+#pragma unroll
+            for (int r = 0; r < PM; ++r)
+              if (r >= s && r < P) cw[r] = y[r];
+          }
+          if (lane == 0) {
+            S.redk[par * BW + warp] = key;
+            S.redi[par * BW + warp] = idx;
+          }
+          __syncthreads();
+          int ww = 0;
+          key = S.redk[par * BW];
+          idx = S.redi[par * BW];
+#pragma unroll
+          for (int w = 1; w < BW; ++w) {
+            const double k2 = S.redk[par * BW + w];
+            const int i2 = S.redi[par * BW + w];
+            if (better(k2, i2, key, idx)) {
+              key = k2;
+              idx = i2;
+              ww = w;
+            }
+          }
+          const double* cv = S.cand + ((size_t)par * BW + ww) * PM;
+          par ^= 1;
           const int sw = idx;
           const bool winner = (slot == sw);
           if (winner) slot = s;
           else if (slot == s) slot = sw;
-          if (winner) {
-            double ss = 0.0;
+          // Householder reflector of the winner's residual (sketch.py:158-168)
+          double ss = 0.0;
 #pragma unroll
-            for (int r = 0; r < PM; ++r)
-              if (r >= s && r < P) ss = __fma_rn(y[r], y[r], ss);
-            const double xn = sqrt(ss);
-            int skip = xn == 0.0;
-            if (!skip) {
-              double vv = 0.0;
+          for (int r = 0; r < PM; ++r)
+            if (r >= s && r < P) ss = __fma_rn(cv[r], cv[r], ss);
+          const double xn = sqrt(ss);
+          if (xn == 0.0 || slot <= s || slot == INT_MAX) continue;
+          const double x0 = cv[s];
+          const double v0 = x0 + copysign(xn, x0 != 0.0 ? x0 : 1.0);
+          double vv = __dmul_rn(v0, v0);
 #pragma unroll
-              for (int r = 0; r < PM; ++r)
-                if (r >= s && r < P) {
-                  double v = y[r];
-                  if (r == s) v = v + copysign(xn, v != 0.0 ? v : 1.0);
-                  S.vsh[r] = v;
-                  vv = __fma_rn(v, v, vv);
-                }
-              if (vv == 0.0) skip = 1;
-              else S.vsh[PM] = 2.0 / vv;
-            }
-            s_skip = skip;
-          }
-          __syncthreads();
-          if (!s_skip && slot > s && slot != INT_MAX) {
-            double dot = 0.0;
+          for (int r = 0; r < PM; ++r)
+            if (r > s && r < P) vv = __fma_rn(cv[r], cv[r], vv);
+          if (vv == 0.0) continue;
+          const double coef = 2.0 / vv;
+          double ys = 0.0;
 #pragma unroll
-            for (int r = 0; r < PM; ++r)
-              if (r >= s && r < P) dot = __fma_rn(S.vsh[r], y[r], dot);
-            const double u = S.vsh[PM] * dot;
+          for (int r = 0; r < PM; ++r)
+            if (r == s) ys = y[r];
+          double dot = __dmul_rn(v0, ys);
 #pragma unroll
-            for (int r = 0; r < PM; ++r)
-              if (r >= s && r < P) y[r] = __dsub_rn(y[r], __dmul_rn(S.vsh[r], u));
-          }
+          for (int r = 0; r < PM; ++r)
+            if (r > s && r < P) dot = __fma_rn(cv[r], y[r], dot);
+          const double u = coef * dot;
+#pragma unroll
+          for (int r = 0; r < PM; ++r)
+            if (r >= s && r < P) y[r] = __dsub_rn(y[r], __dmul_rn(r == s ? v0 : cv[r], u));
         }
         if (tid == 0)
           for (int s = 0; s < qn; ++s) {
@@ -364,8 +428,7 @@ __global__ void __launch_bounds__(BT, MINB) batched_factor_kernel(BatchParams p)
         if (act0) {
           pvi = S.permv[i];
 #pragma unroll
-          for (int r = 0; r < PM; ++r)
-            if (r < P) S.scr[(size_t)r * BT + k0 + slot] = x[r];
+          for (int r = 0; r < PM; ++r) y[r] = r < P ? Bx[(size_t)r * n + i] : 0.0;
         }
         __syncthreads();
         if (act0) {
@@ -373,7 +436,7 @@ __global__ void __launch_bounds__(BT, MINB) batched_factor_kernel(BatchParams p)
           S.pol[k0 + slot] = i - k0;
 #pragma unroll
           for (int r = 0; r < PM; ++r)
-            if (r < P) x[r] = S.scr[(size_t)r * BT + i];
+            if (r < P) Bx[(size_t)r * n + k0 + slot] = y[r];
         }
         __syncthreads();
       }
@@ -479,12 +542,12 @@ __global__ void __launch_bounds__(BT, MINB) batched_factor_kernel(BatchParams p)
         }
         if (sa >= 0) {
           __syncthreads();  // every thread has read pol / Lp / Wp rows for this decision
-          if (tid == sa || tid == sb) {
-            const int h = tid == sa ? 0 : 1;
-#pragma unroll
-            for (int q = 0; q < PM; ++q)
-              if (q < P) S.xs[h * PM + q] = x[q];
-            s_tsw[h] = tr;
+          if (tid == sa || tid == sb) s_tsw[tid == sa ? 0 : 1] = tr;
+          if (tid >= 128 && tid < 128 + P) {  // sketch columns
+            double* bc = Bx + (size_t)(tid - 128) * n;
+            const double u = bc[sa];
+            bc[sa] = bc[sb];
+            bc[sb] = u;
           }
           if (tid < t) {
             double* Lc = S.Lp + (size_t)tid * BT;
@@ -510,13 +573,7 @@ __global__ void __launch_bounds__(BT, MINB) batched_factor_kernel(BatchParams p)
           }
         }
         __syncthreads();
-        if (sa >= 0 && (tid == sa || tid == sb)) {
-          const int h = tid == sa ? 1 : 0;
-#pragma unroll
-          for (int q = 0; q < PM; ++q)
-            if (q < P) x[q] = S.xs[h * PM + q];
-          tr = s_tsw[h];
-        }
+        if (sa >= 0 && (tid == sa || tid == sb)) tr = s_tsw[tid == sa ? 1 : 0];
 
         // D block and checks (factor.py:202-226, 455-466): identical in every thread
         double d11, d21 = 0.0, d22 = 0.0, det = 1.0;
@@ -629,77 +686,89 @@ __global__ void __launch_bounds__(BT, MINB) batched_factor_kernel(BatchParams p)
 
       if (mp > 0 && t > 0) {
         // ---- trailing update A22 -= L21 W21^T, lower computed + mirrored (factor.py:369-379)
+        // Warp work unit: a 32-row strip I x an 8-column group g of the lower triangle; lane =
+        // row.  Lower stores are coalesced across lanes, the mirror is 64 contiguous bytes
+        // per lane; the C-in gather (through pol) of the next unit is issued before this
+        // unit's FMAs.
         double* An = Abuf[nb];
-        const int nb4 = (mp + 3) >> 2;
-        const int ntiles = nb4 * (nb4 + 1) / 2;
-        for (int tile = tid; tile < ntiles; tile += BT) {
-          int I = (int)((sqrt(8.0 * tile + 1.0) - 1.0) * 0.5);
-          while ((I + 1) * (I + 2) / 2 <= tile) ++I;
-          while (I * (I + 1) / 2 > tile) --I;
-          const int J = tile - I * (I + 1) / 2;
-          const int i0 = k_end + 4 * I, j0 = k_end + 4 * J;
-          double acc[4][4];
-#pragma unroll
-          for (int a = 0; a < 4; ++a)
-#pragma unroll
-            for (int c2 = 0; c2 < 4; ++c2) acc[a][c2] = 0.0;
-          for (int s = 0; s < t; ++s) {
-            const double* Lc = S.Lp + (size_t)s * BT;
-            const double* Wc = S.Wp + (size_t)s * BT;
-            double lv[4], wv[4];
-#pragma unroll
-            for (int a = 0; a < 4; ++a) {
-              lv[a] = (i0 + a < n) ? Lc[i0 + a] : 0.0;
-              wv[a] = (j0 + a < n) ? Wc[j0 + a] : 0.0;
-            }
-#pragma unroll
-            for (int a = 0; a < 4; ++a)
-#pragma unroll
-              for (int c2 = 0; c2 < 4; ++c2) acc[a][c2] = __fma_rn(lv[a], wv[c2], acc[a][c2]);
-          }
-#pragma unroll
-          for (int c2 = 0; c2 < 4; ++c2) {
-            const int j = j0 + c2;
-            if (j >= n) continue;
-            const int pj = S.pol[j];
-#pragma unroll
-            for (int a = 0; a < 4; ++a) {
-              const int ii = i0 + a;
-              if (ii >= n || ii < j) continue;
-              const double v = __dsub_rn(T(S.pol[ii], pj), acc[a][c2]);
-              An[(size_t)(j - k_end) * mp + (ii - k_end)] = v;
-              An[(size_t)(ii - k_end) * mp + (j - k_end)] = v;
-            }
-          }
+        const int ng = (mp + 7) >> 3;
+        int uI = 0, ug = warp;
+        while (uI * 32 < mp && ug >= min(4 * uI + 4, ng)) {
+          ug -= min(4 * uI + 4, ng);
+          ++uI;
         }
+#define RCP_LOAD_CIN(I_, g_, cin_)                                                   \
+  {                                                                                  \
+    const int ii_ = k_end + 32 * (I_) + lane;                                        \
+    const int j0_ = k_end + 8 * (g_);                                                \
+    const int pi_ = ii_ < n ? S.pol[ii_] : 0;                                        \
+    _Pragma("unroll") for (int c2 = 0; c2 < 8; ++c2) {                               \
+      const int j_ = j0_ + c2;                                                       \
+      cin_[c2] = (ii_ < n && j_ < n && ii_ >= j_) ? Acur[(size_t)S.pol[j_] * ldA + pi_] : 0.0; \
+    }                                                                                \
+  }
+        double cin[8];
+        if (uI * 32 < mp) RCP_LOAD_CIN(uI, ug, cin);
+        while (uI * 32 < mp) {
+          // next unit of this warp
+          int nI = uI, ngp = ug + BW;
+          while (nI * 32 < mp && ngp >= min(4 * nI + 4, ng)) {
+            ngp -= min(4 * nI + 4, ng);
+            ++nI;
+          }
+          double cnx[8];
+          if (nI * 32 < mp) RCP_LOAD_CIN(nI, ngp, cnx);
+          const int ii = k_end + 32 * uI + lane;
+          const int j0 = k_end + 8 * ug;
+          double acc[8];
+#pragma unroll
+          for (int c2 = 0; c2 < 8; ++c2) acc[c2] = 0.0;
+          const int ir = min(ii, BT - 1);
+          for (int s2 = 0; s2 < t; ++s2) {
+            const double lv = S.Lp[(size_t)s2 * BT + ir];
+            const double* Wc = S.Wp + (size_t)s2 * BT;
+#pragma unroll
+            for (int c2 = 0; c2 < 8; ++c2) acc[c2] = __fma_rn(lv, Wc[min(j0 + c2, BT - 1)], acc[c2]);
+          }
+          if (ii < n) {
+            double* mir = An + (size_t)(ii - k_end) * mp + (j0 - k_end);
+#pragma unroll
+            for (int c2 = 0; c2 < 8; ++c2) {
+              const int j = j0 + c2;
+              if (j < n && ii >= j) {
+                const double v = __dsub_rn(cin[c2], acc[c2]);
+                An[(size_t)(j - k_end) * mp + (ii - k_end)] = v;
+                mir[c2] = v;
+              }
+            }
+          }
+#pragma unroll
+          for (int c2 = 0; c2 < 8; ++c2) cin[c2] = cnx[c2];
+          uI = nI;
+          ug = ngp;
+        }
+#undef RCP_LOAD_CIN
         if (tid == 0) {
           c_mul += (long long)t * ((long long)mp * (mp + 1) / 2);
           c_add += (long long)t * ((long long)mp * (mp + 1) / 2);
         }
         // ---- sketch correction B2 -= (B1 L11^-T) L21^T (factor.py:554-565)
         if (p.q > 1) {
-          if (live && i >= k0 && i < k_end) {
-#pragma unroll
-            for (int q = 0; q < PM; ++q)
-              if (q < P) S.B1s[q * b + (i - k0)] = x[q];
-          }
-          __syncthreads();
           if (tid < P) {
             for (int s = 0; s < t; ++s) {
-              double yv = S.B1s[tid * b + s];
+              double yv = Bx[(size_t)tid * n + k0 + s];
               for (int u = 0; u < s; ++u) yv = __fma_rn(-S.Ys[tid * b + u], S.Lp[(size_t)u * BT + k0 + s], yv);
               S.Ys[tid * b + s] = yv;
             }
           }
           __syncthreads();
           if (live && i >= k_end) {
-#pragma unroll
-            for (int q = 0; q < PM; ++q)
-              if (q < P) {
-                double acc = 0.0;
-                for (int s = 0; s < t; ++s) acc = __fma_rn(S.Ys[q * b + s], S.Lp[(size_t)s * BT + i], acc);
-                x[q] = __dsub_rn(x[q], acc);
-              }
+            for (int q = 0; q < P; ++q) {
+              double acc = 0.0;
+              for (int s = 0; s < t; ++s) acc = __fma_rn(S.Ys[q * b + s], S.Lp[(size_t)s * BT + i], acc);
+              double* bq = Bx + (size_t)q * n + i;
+              *bq = __dsub_rn(*bq, acc);
+            }
           }
           if (tid == 0) {
             c_mul += (long long)t * P * mp + (long long)(t * (t - 1) / 2) * mp;
@@ -874,10 +943,10 @@ __global__ void __launch_bounds__(BT) batched_solve_kernel(int count, int n, con
   }
 }
 
-__global__ void transpose_omega_kernel(const double* __restrict__ om, int P, int n, double* __restrict__ omT) {
+__global__ void transpose_omega_kernel(const double* __restrict__ om, int P, int PM, int n, double* __restrict__ omT) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j < n)
-    for (int r = 0; r < P; ++r) omT[(size_t)j * P + r] = om[(size_t)r * n + j];
+    for (int r = 0; r < PM; ++r) omT[(size_t)j * PM + r] = r < P ? om[(size_t)r * n + j] : 0.0;
 }
 
 int pick_pm(int P) {
@@ -891,7 +960,7 @@ int pick_pm(int P) {
 
 size_t factor_smem(int PM, int b) {
   const int SC = std::max(2 * b + 1, PM);
-  size_t d = (size_t)SC * BT + BT + 2 * PM + PM + 2 + 2 * (size_t)PM * b + 2 * BW;
+  size_t d = (size_t)SC * BT + BT + 2 * PM + PM + 2 + 2 * (size_t)PM * b + 2 * BW + 2 * BW * (size_t)PM;
   return d * 8 + (2 * BW + 2 * BT) * 4;
 }
 
@@ -912,7 +981,7 @@ int sm_count() {
   return sms;
 }
 
-int64_t ws_stride_doubles(int64_t n) { return ((3 * n * n + 31) / 32) * 32; }
+int64_t ws_stride_doubles(int64_t n, int PM) { return ((3 * n * n + (int64_t)PM * n + 31) / 32) * 32; }
 
 }  // namespace
 
@@ -921,8 +990,8 @@ extern "C" {
 size_t rcp_batched_workspace_bytes(int64_t n, const rcp_config* cfg) {
   if (!cfg || n < 1 || n > BT || cfg->p < 1 || cfg->p > 64 || cfg->b < 1 || cfg->b > kMaxB) return 0;
   const int grid = sm_count() * resident_ctas(pick_pm(cfg->p));
-  const size_t om_bytes = ((size_t)n * cfg->p * 8 + 255) & ~size_t(255);
-  return (size_t)grid * (size_t)ws_stride_doubles(n) * 8 + 256 + om_bytes;
+  const size_t om_bytes = ((size_t)n * pick_pm(cfg->p) * 8 + 255) & ~size_t(255);
+  return (size_t)grid * (size_t)ws_stride_doubles(n, pick_pm(cfg->p)) * 8 + 256 + om_bytes;
 }
 
 int rcp_factor_batched(const rcp_config* cfg, int64_t count, int64_t n, const double* a, int64_t lda,
@@ -947,12 +1016,12 @@ int rcp_factor_batched(const rcp_config* cfg, int64_t count, int64_t n, const do
   unsigned char* ws = static_cast<unsigned char*>(workspace);
   int* counter = reinterpret_cast<int*>(ws);
   double* omegaT = reinterpret_cast<double*>(ws + 256);
-  const size_t om_bytes = ((size_t)n * P * 8 + 255) & ~size_t(255);
+  const size_t om_bytes = ((size_t)n * PM * 8 + 255) & ~size_t(255);
   double* scratch = reinterpret_cast<double*>(ws + 256 + om_bytes);
   cudaError_t e = cudaMemsetAsync(counter, 0, sizeof(int), st);
   if (e != cudaSuccess) return RCP_ERR_CUDA;
   // Omega^T (n x P) from the row-major Omega at the head of the normal stream
-  transpose_omega_kernel<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(normals, P, (int)n, omegaT);
+  transpose_omega_kernel<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(normals, P, PM, (int)n, omegaT);
   if (cudaGetLastError() != cudaSuccess) return RCP_ERR_CUDA;
   BatchParams prm{};
   prm.count = (int)count;
@@ -971,7 +1040,7 @@ int rcp_factor_batched(const rcp_config* cfg, int64_t count, int64_t n, const do
   prm.z = normals;
   prm.z_len = normals_len;
   prm.ws = scratch;
-  prm.ws_stride = ws_stride_doubles(n);
+  prm.ws_stride = ws_stride_doubles(n, pick_pm(cfg->p));
   prm.perm = perm;
   prm.L = L;
   prm.d_diag = d_diag;
