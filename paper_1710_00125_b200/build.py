@@ -46,6 +46,8 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     if not force and not needs_build():
         return OUT
     extra = ["-DRCP_PANEL_PROF=1"] if os.environ.get("RCP_PANEL_PROF") == "1" else []
+    if os.environ.get("RCP_BATCH_PROF") == "1":
+        extra.append("-DRCP_BATCH_PROF=1")
     cmd = [_nvcc(), *NVCC_FLAGS, *extra, "-o", str(OUT) + ".tmp", *map(str, sources())]
     if verbose:
         print(" ".join(cmd), flush=True)

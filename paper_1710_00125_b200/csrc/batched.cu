@@ -28,6 +28,10 @@
 #include "../../include/rcp_b200.h"
 #include "rcp_common.cuh"
 
+#ifndef RCP_BATCH_PROF
+#define RCP_BATCH_PROF 0
+#endif
+
 using namespace rcp;
 
 namespace {
@@ -68,7 +72,7 @@ struct Shm {
   double* B1s;  // P x b
   double* Ys;   // P x b
   double* redk;
-  double* cand;  // 2 x BW x PM: per-warp QRCP candidate residuals (double-buffered)
+  double* cand;  // 2 x BW x (PM + 2): per-warp QRCP candidate reflectors (double-buffered)
   int* redi;
   int* pol;    // logical position -> storage index (relative to the panel start)
   int* permv;  // logical position -> original index
@@ -146,9 +150,18 @@ __device__ __forceinline__ double res_norm(const double (&x)[PM], int lo, int P)
 // c = Lp[:, row] . Wp[:, col] over the first t panel columns (fixed order, every caller
 // that needs the same value gets the same bits).
 __device__ __forceinline__ double panel_dot(const double* Lp, const double* Wp, int row, int col, int t) {
-  double acc = 0.0;
-  for (int s = 0; s < t; ++s) acc = __fma_rn(Lp[s * BT + row], Wp[s * BT + col], acc);
-  return acc;
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+  int s = 0;
+  for (; s + 4 <= t; s += 4) {
+    a0 = __fma_rn(Lp[s * BT + row], Wp[s * BT + col], a0);
+    a1 = __fma_rn(Lp[(s + 1) * BT + row], Wp[(s + 1) * BT + col], a1);
+    a2 = __fma_rn(Lp[(s + 2) * BT + row], Wp[(s + 2) * BT + col], a2);
+    a3 = __fma_rn(Lp[(s + 3) * BT + row], Wp[(s + 3) * BT + col], a3);
+  }
+  if (s < t) a0 = __fma_rn(Lp[s * BT + row], Wp[s * BT + col], a0);
+  if (s + 1 < t) a1 = __fma_rn(Lp[(s + 1) * BT + row], Wp[(s + 1) * BT + col], a1);
+  if (s + 2 < t) a2 = __fma_rn(Lp[(s + 2) * BT + row], Wp[(s + 2) * BT + col], a2);
+  return (a0 + a1) + (a2 + a3);
 }
 
 template <int PM, int MINB>
@@ -178,7 +191,7 @@ __global__ void __launch_bounds__(BT, MINB) batched_factor_kernel(BatchParams p)
     S.redk = d;
     d += 2 * BW;
     S.cand = d;
-    d += 2 * BW * PM;
+    d += 2 * BW * (PM + 2);
     int* ip = reinterpret_cast<int*>(d);
     S.redi = ip;
     ip += 2 * BW;
@@ -212,15 +225,27 @@ __global__ void __launch_bounds__(BT, MINB) batched_factor_kernel(BatchParams p)
     int8_t* pat = p.pattern + (size_t)mat * n;
     rcp_batch_stats* ms = p.mstats + mat;
 
+#if RCP_BATCH_PROF
+    long long pf[4] = {0, 0, 0, 0}, pf_t = clock64();
+#define PF(k)                         \
+  {                                   \
+    const long long now_ = clock64(); \
+    pf[k] += now_ - pf_t;             \
+    pf_t = now_;                      \
+  }
+#else
+#define PF(k)
+#endif
     // ---- input checks (core.py:48-53, factor.py:280-281) and max|A|
     int asym = 0, nonfin = 0;
     double mx = 0.0;
     if (live) {
+#pragma unroll 8
       for (int j = 0; j < n; ++j) {
         const double v = A[(size_t)j * lda + i];  // (i, j)
         const double w = A[(size_t)i * lda + j];  // (j, i)
-        if (!(v == w)) asym = 1;
-        if (!isfinite(v)) nonfin = 1;
+        asym |= !(v == w);
+        nonfin |= !isfinite(v);
         mx = fmax(mx, fabs(v));
       }
     }
@@ -267,7 +292,7 @@ __global__ void __launch_bounds__(BT, MINB) batched_factor_kernel(BatchParams p)
 
     if (p.dbg == 2) continue;
     if (live) S.permv[i] = i;
-    long long c_mul = 0, c_add = 0, c_div = 0, c_cmp = 0;  // thread 0's op counters
+    int c_mul = 0, c_add = 0, c_div = 0, c_cmp = 0;  // thread 0's op counters (n <= 256: < 2^31)
     int64_t zoff = (int64_t)P * n;
     int recomputes = 0, n2x2 = 0, nsteps = 0, npanels = 0, def_from = -1, kdone = 0;
     int status = RCP_OK, num_kind = 0, num_step = 0;
@@ -295,11 +320,12 @@ __global__ void __launch_bounds__(BT, MINB) batched_factor_kernel(BatchParams p)
       const bool act0 = live && i >= k0;
       __syncthreads();
 
+      PF(3);
       // ---- guard + partial QRCP + replay (factor.py:570-600)
       if (p.q > 1 && m > 1) {
         if (tid == 0) {
-          c_mul += (long long)P * (m - 1);
-          c_add += (long long)P * (m - 1);
+          c_mul += (int)P * (m - 1);
+          c_add += (int)P * (m - 1);
           c_cmp += m - 1;
         }
         double y[PM];
@@ -344,26 +370,53 @@ __global__ void __launch_bounds__(BT, MINB) batched_factor_kernel(BatchParams p)
         }
         const int qn = min(min(p.q, width), min(m, P));
         int slot = act0 ? i - k0 : INT_MAX;
+        // y rows >= P are zero (padding), so the loops below run over all PM rows unpredicated
+        // on P; rows < s are predicated off (they are finished)
         for (int s = 0; s < qn; ++s) {
-          // one barrier per QRCP step: each warp publishes its best column's residual
-          // (speculative Householder source) next to its key; every thread then picks the
-          // winner and forms the reflector itself (identical arithmetic in every thread)
-          double key = (slot >= s && slot != INT_MAX) ? res_norm<PM>(y, s, P) : -1.0;
-          int idx = (slot >= s) ? slot : INT_MAX;
+          // One barrier per QRCP step.  Each warp's best column publishes its Householder vector
+          // (speculative: computed before the winner is known) next to its key; after the
+          // barrier every thread reads the winner's vector and reflects its own column.
+          const bool cand_ok = slot >= s && slot != INT_MAX;
+          double key = -1.0;
+          int idx = INT_MAX;
+          if (__any_sync(0xffffffffu, cand_ok)) {
+            // residual norm: 4 independent FMA chains over rows > s, then row s
+            double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0, x0 = 0.0;
 #pragma unroll
-          for (int o = 16; o > 0; o >>= 1) {
-            const double k2 = __shfl_xor_sync(0xffffffffu, key, o);
-            const int i2 = __shfl_xor_sync(0xffffffffu, idx, o);
-            if (better(k2, i2, key, idx)) {
-              key = k2;
-              idx = i2;
+            for (int r = 0; r < PM; ++r) {
+              if (r == s) x0 = y[r];
+              if (r > s) {
+                if ((r & 3) == 0) a0 = __fma_rn(y[r], y[r], a0);
+                else if ((r & 3) == 1) a1 = __fma_rn(y[r], y[r], a1);
+                else if ((r & 3) == 2) a2 = __fma_rn(y[r], y[r], a2);
+                else a3 = __fma_rn(y[r], y[r], a3);
+              }
             }
-          }
-          double* cw = S.cand + ((size_t)par * BW + warp) * PM;
-          if (slot == idx) {
+            const double rest = (a0 + a1) + (a2 + a3);
+            const double ss = __fma_rn(x0, x0, rest);
+            if (cand_ok) {
+              key = (ss == 0.0 || (ss >= 1e-280 && ss <= 1e280)) ? sqrt(ss) : sc_norm<PM>(y, s, PM);
+              idx = slot;
+            }
 #pragma unroll
-            for (int r = 0; r < PM; ++r)
-              if (r >= s && r < P) cw[r] = y[r];
+            for (int o = 16; o > 0; o >>= 1) {
+              const double k2 = __shfl_xor_sync(0xffffffffu, key, o);
+              const int i2 = __shfl_xor_sync(0xffffffffu, idx, o);
+              if (better(k2, i2, key, idx)) {
+                key = k2;
+                idx = i2;
+              }
+            }
+            if (slot == idx) {  // reflector of this column (sketch.py:158-168)
+              double* cw = S.cand + ((size_t)par * BW + warp) * (PM + 2);
+              const double xn = key;  // = ||y[s:]||
+              const double v0 = x0 + copysign(xn, x0 != 0.0 ? x0 : 1.0);
+              const double vv = __fma_rn(v0, v0, rest);
+#pragma unroll
+              for (int r = 0; r < PM; ++r)
+                if (r >= s) cw[r] = r == s ? v0 : y[r];
+              cw[PM] = (xn == 0.0 || vv == 0.0) ? 0.0 : 2.0 / vv;  // 0: no reflection
+            }
           }
           if (lane == 0) {
             S.redk[par * BW + warp] = key;
@@ -383,39 +436,28 @@ __global__ void __launch_bounds__(BT, MINB) batched_factor_kernel(BatchParams p)
               ww = w;
             }
           }
-          const double* cv = S.cand + ((size_t)par * BW + ww) * PM;
+          const double* cv = S.cand + ((size_t)par * BW + ww) * (PM + 2);
           par ^= 1;
           const int sw = idx;
           const bool winner = (slot == sw);
           if (winner) slot = s;
           else if (slot == s) slot = sw;
-          // Householder reflector of the winner's residual (sketch.py:158-168)
-          double ss = 0.0;
+          if (slot <= s || slot == INT_MAX) continue;
+          const double coef = cv[PM];
+          if (coef == 0.0) continue;
+          double d0 = 0.0, d1 = 0.0, d2 = 0.0, d3 = 0.0;
 #pragma unroll
           for (int r = 0; r < PM; ++r)
-            if (r >= s && r < P) ss = __fma_rn(cv[r], cv[r], ss);
-          const double xn = sqrt(ss);
-          if (xn == 0.0 || slot <= s || slot == INT_MAX) continue;
-          const double x0 = cv[s];
-          const double v0 = x0 + copysign(xn, x0 != 0.0 ? x0 : 1.0);
-          double vv = __dmul_rn(v0, v0);
+            if (r >= s) {
+              if ((r & 3) == 0) d0 = __fma_rn(cv[r], y[r], d0);
+              else if ((r & 3) == 1) d1 = __fma_rn(cv[r], y[r], d1);
+              else if ((r & 3) == 2) d2 = __fma_rn(cv[r], y[r], d2);
+              else d3 = __fma_rn(cv[r], y[r], d3);
+            }
+          const double u = coef * ((d0 + d1) + (d2 + d3));
 #pragma unroll
           for (int r = 0; r < PM; ++r)
-            if (r > s && r < P) vv = __fma_rn(cv[r], cv[r], vv);
-          if (vv == 0.0) continue;
-          const double coef = 2.0 / vv;
-          double ys = 0.0;
-#pragma unroll
-          for (int r = 0; r < PM; ++r)
-            if (r == s) ys = y[r];
-          double dot = __dmul_rn(v0, ys);
-#pragma unroll
-          for (int r = 0; r < PM; ++r)
-            if (r > s && r < P) dot = __fma_rn(cv[r], y[r], dot);
-          const double u = coef * dot;
-#pragma unroll
-          for (int r = 0; r < PM; ++r)
-            if (r >= s && r < P) y[r] = __dsub_rn(y[r], __dmul_rn(r == s ? v0 : cv[r], u));
+            if (r >= s) y[r] = __dsub_rn(y[r], __dmul_rn(cv[r], u));
         }
         if (tid == 0)
           for (int s = 0; s < qn; ++s) {
@@ -445,6 +487,7 @@ __global__ void __launch_bounds__(BT, MINB) batched_factor_kernel(BatchParams p)
         status = 99;
         break;
       }
+      PF(0);
       // ---- SBKP steps (factor.py:602-634)
       auto T = [&](int a, int c) -> double { return Acur[(size_t)c * ldA + a]; };
       double tk = act0 ? T(S.pol[i], S.pol[k0]) : 0.0;
@@ -506,7 +549,7 @@ __global__ void __launch_bounds__(BT, MINB) batched_factor_kernel(BatchParams p)
           }
         }
         if (tid == 0) {  // op counters of _decide / _eliminate (factor.py:350-367, 414-489)
-          const long long colc = t > 0 ? (long long)t * mm : 0;
+          const long long colc = t > 0 ? (int)t * mm : 0;
           c_mul += colc;
           c_add += colc;
           c_cmp += mm >= 2 ? mm - 2 : 0;
@@ -677,6 +720,7 @@ __global__ void __launch_bounds__(BT, MINB) batched_factor_kernel(BatchParams p)
       const int k_end = k0 + t;
       const int mp = n - k_end;
 
+      PF(1);
       // L columns of this panel, keyed by original row index (rows never move afterwards)
       if (act0) {
         double* dst = Lst + (size_t)S.permv[i] * n + k0;
@@ -728,7 +772,7 @@ __global__ void __launch_bounds__(BT, MINB) batched_factor_kernel(BatchParams p)
             const double lv = S.Lp[(size_t)s2 * BT + ir];
             const double* Wc = S.Wp + (size_t)s2 * BT;
 #pragma unroll
-            for (int c2 = 0; c2 < 8; ++c2) acc[c2] = __fma_rn(lv, Wc[min(j0 + c2, BT - 1)], acc[c2]);
+            for (int c2 = 0; c2 < 8; ++c2) acc[c2] = __fma_rn(lv, Wc[j0 + c2], acc[c2]);  // j0 + c2 <= n + 7 stays inside smem
           }
           if (ii < n) {
             double* mir = An + (size_t)(ii - k_end) * mp + (j0 - k_end);
@@ -749,8 +793,8 @@ __global__ void __launch_bounds__(BT, MINB) batched_factor_kernel(BatchParams p)
         }
 #undef RCP_LOAD_CIN
         if (tid == 0) {
-          c_mul += (long long)t * ((long long)mp * (mp + 1) / 2);
-          c_add += (long long)t * ((long long)mp * (mp + 1) / 2);
+          c_mul += (int)t * ((int)mp * (mp + 1) / 2);
+          c_add += (int)t * ((int)mp * (mp + 1) / 2);
         }
         // ---- sketch correction B2 -= (B1 L11^-T) L21^T (factor.py:554-565)
         if (p.q > 1) {
@@ -771,8 +815,8 @@ __global__ void __launch_bounds__(BT, MINB) batched_factor_kernel(BatchParams p)
             }
           }
           if (tid == 0) {
-            c_mul += (long long)t * P * mp + (long long)(t * (t - 1) / 2) * mp;
-            c_add += (long long)t * P * mp + (long long)(t * (t - 1) / 2) * mp;
+            c_mul += (int)t * P * mp + (int)(t * (t - 1) / 2) * mp;
+            c_add += (int)t * P * mp + (int)(t * (t - 1) / 2) * mp;
           }
         }
         Acur = An;
@@ -784,6 +828,7 @@ __global__ void __launch_bounds__(BT, MINB) batched_factor_kernel(BatchParams p)
         break;
       }
       __syncthreads();  // trailing block + Lst visible; Lp/Wp free for the next panel
+      PF(2);
       k = k_end;
       kdone = k_end;
     }
@@ -837,6 +882,13 @@ __global__ void __launch_bounds__(BT, MINB) batched_factor_kernel(BatchParams p)
       z.adds = c_add;
       z.divs = c_div;
       z.comps = c_cmp;
+#if RCP_BATCH_PROF
+      PF(3);
+      z.mults = pf[0];  // QRCP (guard + QRCP + replay)
+      z.adds = pf[1];   // SBKP steps
+      z.divs = pf[2];   // L store + trailing update + sketch correction
+      z.comps = pf[3];  // validation + sketch + outputs
+#endif
       *ms = z;
     }
   }
@@ -960,7 +1012,7 @@ int pick_pm(int P) {
 
 size_t factor_smem(int PM, int b) {
   const int SC = std::max(2 * b + 1, PM);
-  size_t d = (size_t)SC * BT + BT + 2 * PM + PM + 2 + 2 * (size_t)PM * b + 2 * BW + 2 * BW * (size_t)PM;
+  size_t d = (size_t)SC * BT + BT + 2 * PM + PM + 2 + 2 * (size_t)PM * b + 2 * BW + 2 * BW * (size_t)(PM + 2);
   return d * 8 + (2 * BW + 2 * BT) * 4;
 }
 
@@ -973,7 +1025,10 @@ cudaError_t launch_pm(const BatchParams& prm, int grid, size_t smem, cudaStream_
   return cudaGetLastError();
 }
 
-int resident_ctas(int PM) { return PM <= 32 ? 2 : 1; }
+int resident_ctas(int PM) {
+  if (const char* e = std::getenv("RCP_BATCH_MINB")) return std::atoi(e) == 1 ? 1 : 2;
+  return PM <= 32 ? 2 : 1;
+}
 
 int sm_count() {
   int dev = 0, sms = 148;
@@ -1053,7 +1108,9 @@ int rcp_factor_batched(const rcp_config* cfg, int64_t count, int64_t n, const do
   switch (PM) {
     case 8: e = launch_pm<8, 2>(prm, grid, smem, st); break;
     case 16: e = launch_pm<16, 2>(prm, grid, smem, st); break;
-    case 24: e = launch_pm<24, 2>(prm, grid, smem, st); break;
+    case 24:
+      e = resident_ctas(24) == 1 ? launch_pm<24, 1>(prm, grid, smem, st) : launch_pm<24, 2>(prm, grid, smem, st);
+      break;
     case 32: e = launch_pm<32, 2>(prm, grid, smem, st); break;
     case 48: e = launch_pm<48, 1>(prm, grid, smem, st); break;
     default: e = launch_pm<64, 1>(prm, grid, smem, st); break;

@@ -26,3 +26,8 @@ for rep in range(3):
     print(f"count={count} ms={ms:.2f} GFLOP/s={flops / ms / 1e6:.1f} per-matrix-us={ms * 1e3 / count:.2f}")
 st = bf.stats
 print("status", np.bincount(st["status"]), "recomputes", np.bincount(st["recompute_count"]), "steps", st["n_steps"].mean())
+import os
+if os.environ.get("RCP_BATCH_PROF") == "1":
+    tot = st["mults"].astype(float) + st["adds"] + st["divs"] + st["comps"]
+    for nm in ("mults", "adds", "divs", "comps"):
+        print(nm, "mean cycles", st[nm].mean(), "share", (st[nm] / tot).mean())
