@@ -56,6 +56,9 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--cpu-seconds", type=float, default=20.0, help="budget of the cpu_baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--workload", default="c3", choices=["c3", "c5"],
+                    help="c3: n=32768 single matrix (headline); c5: 65536 x n=256 batched (b=16, p=8)")
+    ap.add_argument("--count", type=int, default=65536, help="c5: matrices in the whole job")
     return ap.parse_args()
 
 
@@ -295,7 +298,7 @@ def run_b200(args, rank: int, world: int, local_rank: int):
         "config": cfg_dict(args),
         "pct_fp64_peak": 100.0 * value / (world * FP64_PEAK_GFLOPS),
         "fp64_peak": {"value": FP64_PEAK_GFLOPS, "unit": "GFLOP/s", "source": FP64_PEAK_SRC},
-        "roofline": {"bound": "tensor", "kernel": "dmma_gemm_kernel<128,128> (trailing Schur update)",
+        "roofline": {"bound": "tensor", "kernel": "schur_ws_kernel (trailing Schur update, DMMA.8x8x4)",
                      "achieved": achieved, "peak": FP64_PEAK_GFLOPS / 1e3, "unit": "TFLOP/s",
                      "frac": (achieved / (FP64_PEAK_GFLOPS / 1e3)) if achieved else None,
                      "traffic": None,
@@ -314,13 +317,210 @@ def run_b200(args, rank: int, world: int, local_rank: int):
     print(json.dumps(line), flush=True)
 
 
+# ----------------------------------------------------------------------------- C5 (batched)
+C5_N, C5_B, C5_P = 256, 16, 24
+
+
+def c5_cfg(args, world):
+    return {"workload": (f"C5 batched: {args.count} symmetrised N(0,1) n={C5_N} matrices, every 10th scaled "
+                         f"D A D with D = diag(10^U(-6,6)) and re-mirrored; b=q={C5_B}, P=b+8={C5_P}; "
+                         f"sharded by matrix over {world} GPU(s)"),
+            "count": args.count, "n": C5_N, "b": C5_B, "q": C5_B, "p_sketch": C5_P, "oversampling": C5_P - C5_B,
+            "parallelism": f"shard-by-matrix x{world}",
+            "l2": f"inputs {args.count * C5_N * C5_N * 8 / 1e9:.1f} GB >> 126 MB L2 (no flush needed)"}
+
+
+def c5_host_member(i: int, seed: int) -> np.ndarray:
+    from paper_1710_00125_b200 import gallery
+    return gallery.scaled_member(C5_N, seed + i, scaled=(i % 10 == 0))
+
+
+def c5_cpu_sample(args, budget_s: float, max_count: int | None = None):
+    from oracle.rcp_oracle import OracleConfig, oracle_factor
+    cfg = OracleConfig(p=C5_P, b=C5_B, q=C5_B, seed=args.seed)
+    mats = []
+    t_total, done = 0.0, 0
+    while True:
+        a = c5_host_member(done, args.seed)
+        t0 = time.perf_counter()
+        oracle_factor(a, cfg)
+        t_total += time.perf_counter() - t0
+        done += 1
+        if (max_count is not None and done >= max_count) or (max_count is None and t_total >= budget_s):
+            break
+    return done, t_total
+
+
+def _c5_worker(job):
+    seed, idx = job
+    from oracle.rcp_oracle import OracleConfig, oracle_factor
+    cfg = OracleConfig(p=C5_P, b=C5_B, q=C5_B, seed=seed)
+    for i in idx:
+        oracle_factor(c5_host_member(i, seed), cfg)
+    return len(idx)
+
+
+def run_reference_c5(args, rank: int):
+    """All host cores (one process per core, OMP/BLAS threads 1), C5 members split across them."""
+    if rank != 0:
+        return
+    import multiprocessing as mp
+    for k in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS"):
+        os.environ[k] = "1"
+    cores = os.cpu_count() or 1
+    per_core = 4
+    ctx = mp.get_context("spawn")
+    with ctx.Pool(cores) as pool:
+        def one_step(base):
+            jobs = [(args.seed, list(range(base + c * per_core, base + (c + 1) * per_core))) for c in range(cores)]
+            t0 = time.perf_counter()
+            done = sum(pool.map(_c5_worker, jobs))
+            return done, time.perf_counter() - t0
+        for w in range(max(1, args.warmup)):
+            one_step(0)
+        steps = [one_step(0) for _ in range(args.steps)]
+    cnt = sum(c for c, _ in steps)
+    tsum = sum(t for _, t in steps)
+    value = cnt * C5_N ** 3 / 3.0 / tsum / 1e9
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tsum / len(steps),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded numpy Philox C5 members)", "config": c5_cfg(args, args.gpus),
+        "cpu_baseline": {"value": value, "unit": "GFLOP/s", "cores": cores, "kind": "port",
+                         "sample": f"oracle port factor() on {cores * per_core} C5 members per step, {cores} "
+                                   f"processes x 1 BLAS thread"},
+        "e2e": {"value": value, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_b200_c5(args, rank: int, world: int, local_rank: int):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1710_00125_b200 import api, batched, gallery
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    count = args.count // world + (1 if rank < args.count % world else 0)
+    cfg = api.FactorConfig(strategy="rcp", b=C5_B, q=C5_B, p=C5_P, seed=args.seed)
+    a = torch.empty(count, C5_N, C5_N, dtype=torch.float64, device=dev)
+    chunk = 4096
+    for c0 in range(0, count, chunk):
+        c1 = min(count, c0 + chunk)
+        a[c0:c1] = gallery.c5_batch_device(c1 - c0, C5_N, seed=args.seed + 1000 * rank + c0, device=dev)
+    normals = torch.from_numpy(batched.normal_stream(cfg, C5_N)).to(dev)
+    ws = torch.empty(batched.batched_workspace_bytes(C5_N, cfg), dtype=torch.uint8, device=dev)
+    out = None
+    for _ in range(max(3, args.warmup)):
+        out = batched.factor_batched_device(a, cfg, normals=normals, workspace=ws, out=out, check=False)
+    torch.cuda.synchronize()
+    bad = int((out.stats["status"] != 0).sum())
+    clk = ClockSampler(local_rank)
+    clk.start()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        out = batched.factor_batched_device(a, cfg, normals=normals, workspace=ws, out=out, check=False)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = clk.stop()
+    ms = e0.elapsed_time(e1) / args.steps
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    flops = args.count * C5_N ** 3 / 3.0
+    value = flops / (ms_max / 1e3) / 1e9
+    rec = out.stats
+    recomputes = int(rec["recompute_count"].sum())
+
+    # solve check on the first matrices (batched solve kernel)
+    nchk = min(count, 256)
+    rhs = torch.randn(nchk, C5_N, dtype=torch.float64, device=dev)
+    sub = batched.BatchedDeviceFactorization(out.perm[:nchk], out.L[:nchk], out.d_diag[:nchk], out.d_off[:nchk],
+                                             out.pattern[:nchk], out.stats[:nchk])
+    x, _ = batched.solve_batched_device(sub, rhs)
+    ax = torch.bmm(a[:nchk], x[:, :, None])[:, :, 0]
+    bwd = float(((ax - rhs).abs().amax(dim=1) / (a[:nchk].abs().sum(dim=2).amax(dim=1) * x.abs().amax(dim=1))).max())
+
+    # end to end: pinned host stack in -> factors (perm, L, D, pattern) in pinned host memory out
+    ecount = min(count, 8192)
+    a_pin = torch.empty(ecount, C5_N, C5_N, dtype=torch.float64, pin_memory=True)
+    a_pin.copy_(a[:ecount])
+    l_pin = torch.empty(ecount, C5_N, C5_N, dtype=torch.float64, pin_memory=True)
+    small_pin = torch.empty(ecount, C5_N, 3, dtype=torch.float64, pin_memory=True)
+    pat_pin = torch.empty(ecount, C5_N, dtype=torch.int8, pin_memory=True)
+    perm_pin = torch.empty(ecount, C5_N, dtype=torch.int64, pin_memory=True)
+    e2e_times = []
+    for _ in range(max(1, args.e2e_steps)):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        ad = a_pin.to(dev, non_blocking=True)
+        bf = batched.factor_batched_device(ad, cfg, normals=normals, workspace=ws, check=False)
+        l_pin.copy_(bf.L, non_blocking=True)
+        small_pin[:, :, 0].copy_(bf.d_diag, non_blocking=True)
+        small_pin[:, :, 1].copy_(bf.d_off, non_blocking=True)
+        pat_pin.copy_(bf.pattern, non_blocking=True)
+        perm_pin.copy_(bf.perm, non_blocking=True)
+        torch.cuda.synchronize()
+        e2e_times.append(time.perf_counter() - t0)
+        del ad, bf
+    te = torch.tensor([statistics.median(e2e_times)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_val = world * ecount * C5_N ** 3 / 3.0 / float(te.item()) / 1e9
+    h2d = ecount * C5_N * C5_N * 8
+    d2h = ecount * (C5_N * C5_N * 8 + C5_N * (8 + 8 + 8 + 1))
+
+    if rank != 0:
+        return
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        cnt, tc = c5_cpu_sample(args, budget_s=args.cpu_seconds)
+        cv = cnt * C5_N ** 3 / 3.0 / tc / 1e9
+        cpu = {"value": cv, "unit": "GFLOP/s", "cores": 1, "kind": "port",
+               "sample": f"oracle port factor() on {cnt} C5 members (numpy/OpenBLAS, one process), {tc:.1f} s"}
+    hbm_bytes = args.count * C5_N * C5_N * 8 * 2  # read A, write L (algorithmic)
+    line = {
+        "metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
+        "warmup": max(3, args.warmup), "ms_per_step": ms_max, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded torch generator on the device)",
+        "config": c5_cfg(args, world),
+        "pct_fp64_peak": 100.0 * value / (world * FP64_PEAK_GFLOPS),
+        "roofline": {"bound": "tensor", "kernel": "batched_factor_kernel (whole factorization, one CTA per matrix)",
+                     "achieved": value / 1e3, "peak": FP64_PEAK_GFLOPS / 1e3, "unit": "TFLOP/s",
+                     "frac": value / (world * FP64_PEAK_GFLOPS), "traffic": None,
+                     "hbm_achieved_gbs": hbm_bytes / (ms_max / 1e3) / 1e9 / world,
+                     "hbm_peak_gbs": 6546.6,
+                     "algorithmic": "n^3/3 flop and 2 n^2 * 8 B (A in, L out) per matrix"},
+        "cpu_baseline": cpu,
+        "e2e": {"value": e2e_val, "unit": "GFLOP/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "path": f"pinned host stack of {ecount} matrices -> factor_batched_device -> perm/L/D/pattern "
+                        f"in pinned host memory"},
+        "gpu_launches": 3 * args.steps,
+        "clocks": clocks,
+        "factor_stats": {"failed_matrices": bad, "recompute_count": recomputes,
+                         "mean_steps": float(rec["n_steps"].mean())},
+        "solve_backward_error": bwd,
+    }
+    print(json.dumps(line), flush=True)
+
+
 def main():
     args = parse()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
-        run_reference(args, rank)
+        (run_reference_c5 if args.workload == "c5" else run_reference)(args, rank)
         return
     if world > 1:
         import torch
@@ -328,7 +528,7 @@ def main():
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     try:
-        run_b200(args, rank, world, local_rank)
+        (run_b200_c5 if args.workload == "c5" else run_b200)(args, rank, world, local_rank)
     finally:
         if world > 1:
             import torch.distributed as dist
