@@ -141,17 +141,16 @@ __global__ void ysolve_kernel(int64_t n, int P, int k0, int t, int tpad, const i
   for (int f = tid; f < t * t; f += blockDim.x) L11[f] = L11g[f];  // compact copy made by gather_kernel
   const int rr = tid >> 4, l16 = tid & 15;
   const int r = blockIdx.x * 16 + rr;
-  for (int a = l16; a < tpad; a += 16) yv[rr * tpad + a] = 0.0;
+  // B1 row prefetched (the substitution below is then smem + shuffles only)
+  for (int a = l16; a < tpad; a += 16)
+    yv[rr * tpad + a] = (r < P && a < t) ? Bin[r + (int64_t)phys_of_log[k0 + a] * P] : 0.0;
   __syncthreads();
   for (int a = 0; a < t; ++a) {
     double part = 0.0;
     for (int c = l16; c < a; c += 16) part = __fma_rn(L11[a * t + c], yv[rr * tpad + c], part);
 #pragma unroll
     for (int off = 8; off > 0; off >>= 1) part = __dadd_rn(part, __shfl_xor_sync(0xffffffffu, part, off, 16));
-    if (l16 == 0) {
-      double b1 = (r < P) ? Bin[r + (int64_t)phys_of_log[k0 + a] * P] : 0.0;
-      yv[rr * tpad + a] = __dsub_rn(b1, part);
-    }
+    if (l16 == 0) yv[rr * tpad + a] = __dsub_rn(yv[rr * tpad + a], part);
     __syncwarp();
   }
   if (r < P) {
