@@ -26,13 +26,12 @@ using namespace rcp;
 namespace {
 
 constexpr size_t kAlign = 256;
-constexpr int kRowsMin = 32;
 
 size_t align_up(size_t x) { return (x + kAlign - 1) & ~(kAlign - 1); }
 
 struct Layout {
   size_t A0, A1, Lbuf, W, Lneg, Wg, B0, B1, qscr, Y, L11, omega, phys, lop, pol, perm0, perm1, poso, snap, flags, xrec, qrec,
-      qcol, sdec, qdec, state, scal, total;
+      qcol, sdec, qdec, state, scal, desc, plog, total;
   int64_t rows_pad, snap_cap;
   int tpad;
 };
@@ -79,6 +78,8 @@ Layout make_layout(int64_t n, const rcp_config& c) {
   L.qdec = take(8 * 2 * (8 + 2 * (size_t)P));
   L.state = take(sizeof(PanelState));
   L.scal = take(64);
+  L.desc = take(2 * sizeof(PanelDesc));
+  L.plog = take((size_t)(n + 2) * sizeof(PanelLog));
   L.total = off;
   return L;
 }
@@ -258,7 +259,6 @@ int rcp_factor(const rcp_config* cfg, int64_t n, const double* a, int64_t lda, c
   int curA = 0, curB = 0;  // ping-pong buffers holding the current trailing block / sketch
   int pcur = 0;      // perm buffer for the current order
   int64_t k = 0;
-  int64_t snap_off = 0;
   int64_t recomputes = 0;
   // panel-level op counters (factor.py:377-378, 564-565, 577-599); step-level ones come from the kernel
   long long h_mul = 0, h_add = 0, h_div = 0, h_cmp = 0;
@@ -272,140 +272,120 @@ int rcp_factor(const rcp_config* cfg, int64_t n, const double* a, int64_t lda, c
     k = n;
   }
 
-  while (k < n) {
-    const int k0 = (int)k;
-    const int width = (int)std::min<int64_t>(c.b, n - k0);
-    const int m0 = (int)(n - k0);
-    int G = std::min(num_sms, std::max(1, (m0 + kRowsMin - 1) / kRowsMin));
-    if (G > kMaxSMs) G = kMaxSMs;
-    int R = (m0 + G - 1) / G;
-    G = (m0 + R - 1) / R;
-    const int Wn = width + 2;
-    const int qn = (c.q > 1 && m0 > 1) ? std::min(std::min(c.q, width), std::min(m0, P)) : 0;
-    auto a16 = [](size_t x) { return (x + 15) & ~size_t(15); };
-    const size_t fixed = a16(4 * (size_t)Wn) + a16(4 * (size_t)R) + a16(8 * (size_t)P) + 4 * a16(8 * (size_t)Wn);
-    const long long avail = (long long)smem_budget - (long long)fixed;
-    // QRCP: register mode (one sketch column per thread, rows >= 32 in smem) when it fits
-    int qmode = 0, Rs = 0;
-    size_t need_q = 0;
-    if (qn > 0) {
-      const int ps_reg = P - std::min(P, 32);
-      const long long need_reg = 8LL * ps_reg * R + 64;
-      if (R <= 256 && need_reg <= avail) {
-        qmode = 1;
-        Rs = R;
-        need_q = (size_t)need_reg;
-      } else {
-        long long rs = (avail - 12LL * R - 64) / (8LL * P);
-        Rs = (int)std::max(0LL, std::min<long long>(R, rs));
-        need_q = (size_t)8 * P * Rs + 12 * (size_t)R + 64;
-      }
-    }
-    long long ls = (avail - 24LL * R - 64) / (8LL * R);
-    int Ls = 0;
-    const bool q1 = (c.q == 1);
-    if (q1) ls = (avail - 24LL * R - 8LL * P * R - 8LL * P - 128) / (8LL * R);
-    Ls = (int)std::max(0LL, std::min<long long>(Wn, ls));
-    size_t need_s = (size_t)8 * Ls * R + 24 * (size_t)R + (q1 ? (size_t)8 * P * R + 8 * (size_t)P : 0) + 128;
-    size_t smem = fixed + std::max(need_q, need_s);
+  // ---- panel loop, device driven (see PanelDesc): the host enqueues panels back to back
+  // and reads their outcome only once per batch; guard events and errors stop the device
+  // chain, the host rolls back to that panel and handles them.
+  const bool q1 = (c.q == 1);
+  const int sms_cap = std::min(num_sms, kMaxSMs);
+  const int gmax = panel_geometry(n, (int)k, c.b, c.q, P, sms_cap, smem_budget).G;
+  PanelDesc* ddesc = reinterpret_cast<PanelDesc*>(ws + Lay.desc);
+  PanelLog* dplog = reinterpret_cast<PanelLog*>(ws + Lay.plog);
+  PanelDesc* hdesc = nullptr;
+  RCP_CHECK(cudaMallocHost(&hdesc, 2 * sizeof(PanelDesc)));
+  struct DescFree {
+    PanelDesc* d;
+    ~DescFree() { cudaFreeHost(d); }
+  } desc_free{hdesc};
+  struct Hist {
+    int curA, curB, pcur;
+  };
+  std::vector<Hist> hist;
+  int guard_req = armed ? 1 : 0;
+  int pidx = 0;
+  bool chain_done = (k >= n);
+  int stop_k0 = -1;
+  if (!chain_done) {
+    hdesc[0] = PanelDesc{(int)k, 1, 0, 0, 0, 0, 0};
+    RCP_CHECK(cudaMemcpyAsync(ddesc, hdesc, sizeof(PanelDesc), cudaMemcpyHostToDevice, st));
+    int neg1 = -1;
+    RCP_CHECK(cudaMemcpyAsync(&dstate->stop_pidx, &neg1, sizeof(int), cudaMemcpyHostToDevice, st));
+  }
+  int batch = 2;
+  constexpr int kBatchMax = 16;
+  PanelParams base{};
+  base.n = n;
+  base.P = P;
+  base.alpha = std::sqrt(2.0) / 2.0;
+  base.q1 = q1 ? 1 : 0;
+  base.qscr = dptr(Lay.qscr);
+  base.Lbuf = Lbuf;
+  base.W = W;
+  base.log_of_phys = lop;
+  base.phys_of_log = pol;
+  base.perm_out = perm;
+  base.d_diag = d_diag;
+  base.d_off = d_off;
+  base.pattern = pattern;
+  base.trace_kind = trace_kind;
+  base.trace_r = trace_r;
+  base.xll = reinterpret_cast<unsigned long long*>(ws + Lay.xrec);
+  base.qll = reinterpret_cast<unsigned long long*>(ws + Lay.qrec);
+  base.qcll = reinterpret_cast<unsigned long long*>(ws + Lay.qcol);
+  base.sdll = reinterpret_cast<unsigned long long*>(ws + Lay.sdec);
+  base.qdll = reinterpret_cast<unsigned long long*>(ws + Lay.qdec);
+  base.st = dstate;
+  base.b = c.b;
+  base.q = c.q;
+  base.num_sms = sms_cap;
+  base.smem_budget = smem_budget;
 
-    PanelParams prm{};
-    prm.n = n;
-    prm.k0 = k0;
-    prm.width = width;
-    prm.P = P;
-    prm.qn = qn;
-    prm.guard_mode = (armed && (qn > 0 || q1)) ? 1 : 0;
-    prm.guard_limit = thr * beta;
-    prm.alpha = std::sqrt(2.0) / 2.0;
-    prm.G = G;
-    prm.R = R;
-    prm.Rs = Rs;
-    prm.Ls = Ls;
-    prm.Wn = Wn;
-    prm.qmode = qmode;
-    prm.A = A[curA];
-    prm.B = B[curB];
-    prm.Bout = B[curB ^ 1];
-    prm.q1 = q1 ? 1 : 0;
-    prm.qscr = dptr(Lay.qscr);
-    prm.Lbuf = Lbuf;
-    prm.W = W;
-    prm.log_of_phys = lop;
-    prm.phys_of_log = pol;
-    prm.perm_cur = permb[pcur];
-    prm.perm_out = perm;
-    prm.d_diag = d_diag;
-    prm.d_off = d_off;
-    prm.pattern = pattern;
-    prm.trace_kind = trace_kind;
-    prm.trace_r = trace_r;
-    prm.xll = reinterpret_cast<unsigned long long*>(ws + Lay.xrec);
-    prm.qll = reinterpret_cast<unsigned long long*>(ws + Lay.qrec);
-    prm.qcll = reinterpret_cast<unsigned long long*>(ws + Lay.qcol);
-    prm.sdll = reinterpret_cast<unsigned long long*>(ws + Lay.sdec);
-    prm.qdll = reinterpret_cast<unsigned long long*>(ws + Lay.qdec);
-    prm.st = dstate;
-
-    bool stopped = false;
-    for (int attempt = 0;; ++attempt) {
-      RCP_CHECK(cudaMemsetAsync(&dstate->status, 0, sizeof(int), st));
+  while (!chain_done) {
+    for (int bi = 0; bi < batch; ++bi) {
+      hist.push_back(Hist{curA, curB, pcur});
+      PanelDesc* din = ddesc + (pidx & 1);
+      PanelDesc* dout = ddesc + ((pidx + 1) & 1);
+      PanelParams prm = base;
+      prm.desc = din;
+      prm.guard_mode = guard_req;
+      prm.guard_limit = thr * beta;
+      prm.A = A[curA];
+      prm.B = B[curB];
+      prm.Bout = B[curB ^ 1];
+      prm.perm_cur = permb[pcur];
       EventPair& ep = new_pair(ev_panel);
       RCP_CHECK(cudaEventRecord(ep.a, st));
-      RCP_LAUNCH(launch_panel(prm, G, smem, st));
+      RCP_LAUNCH(launch_panel(prm, gmax, (size_t)smem_budget, st));
       RCP_CHECK(cudaEventRecord(ep.b, st));
-      RCP_CHECK(cudaMemcpyAsync(hstate, dstate, sizeof(PanelState), cudaMemcpyDeviceToHost, st));
-      RCP_CHECK(cudaStreamSynchronize(st));
-      if (hstate->status == 0) break;
-      if (hstate->status == 99) {
-        if (stats) snprintf(stats->message, sizeof(stats->message), "panel exchange watchdog fired at k=%d", k0);
-        return RCP_ERR_CUDA;
+      RCP_LAUNCH(launch_panel_commit(din, dout, dplog, dstate, n, c.b, c.q, P, (long long)Lay.snap_cap, st));
+      RCP_LAUNCH(launch_gather(n, 0, 0, 0, tpad, 0, pol, Lbuf, W, permb[pcur], permb[pcur ^ 1], snap, phys, Lneg, Wg,
+                               L11c, st, din));
+      EventPair& es = new_pair(ev_schur);
+      RCP_CHECK(cudaEventRecord(es.a, st));
+      RCP_LAUNCH(launch_schur_update(n, 0, 0, Lneg, Wg, tpad, 0, A[curA], phys, A[curA ^ 1], st, din));
+      RCP_CHECK(cudaEventRecord(es.b, st));
+      if (!q1) {  // sketch correction once per panel (factor.py:554-565)
+        RCP_LAUNCH(launch_ysolve(n, P, 0, c.b, tpad, pol, B[curB], L11c, Y, st, din));
+        RCP_LAUNCH(launch_sketch_correction(P, n, 0, Y, tpad, c.b, Lneg, B[curB], phys, B[curB ^ 1], st, din, n));
       }
-      if (hstate->status == 2) {  // confirmed collapse: deficient tail (factor.py:405-410, 381-385)
-        stopped = true;
-        break;
-      }
-      // guard trip: fresh projection of the active block (factor.py:392-404)
-      if (!draw) {
-        if (stats) snprintf(stats->message, sizeof(stats->message), "guard recompute needs normals at k=%d", k0);
-        return RCP_ERR_NEED_NORMALS;
-      }
-      draw_buf.resize((size_t)P * m0);
-      if (draw(draw_ctx, P, m0, draw_buf.data()) != 0) return RCP_ERR_NEED_NORMALS;
-      RCP_CHECK(cudaMemcpyAsync(omg, draw_buf.data(), sizeof(double) * (size_t)P * m0, cudaMemcpyHostToDevice, st));
-#if !RCP_FULL_STORAGE
-      RCP_LAUNCH(launch_mirror_lower(n, k0, A[curA], st));  // the projection reads full columns
-#endif
-      RCP_LAUNCH(launch_sketch_gemm(P, m0, omg, m0, A[curA] + k0 + (int64_t)k0 * n, n, B[curB], k0, st));
-      recomputes += 1;
-      delta += 1.0 / c.robust_r;
-      thr = std::pow(DBL_EPSILON, delta);
-      prm.guard_mode = 2;
-      prm.guard_limit = thr * beta;
-      (void)attempt;
+      // q = 1: the panel kernel itself wrote the per-step-updated sketch into B[curB ^ 1]
+      curA ^= 1;
+      curB ^= 1;
+      pcur ^= 1;
+      ++pidx;
+      guard_req = armed ? 1 : 0;  // a stop check (2) applies to a relaunched panel only
     }
-    if (!q1 && m0 > 1) {  // preselect norms (factor.py:576-577)
-      h_mul += (long long)P * (m0 - 1);
-      h_add += (long long)P * (m0 - 1);
-      h_cmp += m0 - 1;
+    RCP_CHECK(cudaMemcpyAsync(hstate, dstate, sizeof(PanelState), cudaMemcpyDeviceToHost, st));
+    RCP_CHECK(cudaMemcpyAsync(hdesc, ddesc, 2 * sizeof(PanelDesc), cudaMemcpyDeviceToHost, st));
+    RCP_CHECK(cudaStreamSynchronize(st));
+    batch = std::min(batch * 2, kBatchMax);
+    if (hstate->status == 0 && hstate->err == LLONG_MAX) {
+      if (!hdesc[pidx & 1].run) chain_done = true;  // the next descriptor ends the chain: k == n
+      continue;
     }
-    if (stopped && q1) {  // the stopping step charged its sketch norms (factor.py:608-610)
-      h_mul += (long long)P * (m0 - 1);
-      h_add += (long long)P * (m0 - 1);
-      h_cmp += m0 - 1;
+    // a guard event or an error at panel tp: later panels were no-ops; roll back to tp
+    const int tp = hstate->stop_pidx;
+    if (tp < 0 || tp >= (int)hist.size()) {
+      if (stats) snprintf(stats->message, sizeof(stats->message), "panel chain lost its stop index");
+      return RCP_ERR_CUDA;
     }
-    if (!stopped) {
-      for (int j = 0; j < qn; ++j) {  // QRCP slots (sketch.py:135-169 via factor.py:586-599)
-        h_cmp += m0 - 1 - j;
-        h_mul += 2LL * P * (m0 - j);
-        h_add += 2LL * P * (m0 - j);
-      }
-    }
-    if (stopped) {
-      RCP_LAUNCH(launch_deficient_fill(n, k0, permb[pcur], perm, d_diag, d_off, pattern, st));
-      deficient_from = k0;
-      break;
-    }
+    curA = hist[tp].curA;
+    curB = hist[tp].curB;
+    pcur = hist[tp].pcur;
+    hist.resize(tp);
+    pidx = tp;
+    const int k0 = hdesc[0].k0;  // no-op panels carry the stopped panel's k0 / snap_off forward
+    const long long so = hdesc[0].snap_off;
+    const int m0 = (int)(n - k0);
     if (hstate->err != LLONG_MAX) {
       if (stats) {
         stats->num_kind = (int)(hstate->err & 0xff);
@@ -415,37 +395,95 @@ int rcp_factor(const rcp_config* cfg, int64_t n, const double* a, int64_t lda, c
       }
       return RCP_ERR_NUMERICAL;
     }
-    const int k_end = hstate->k_end;
-    const int t = hstate->t_end;
-    const int64_t mp = n - k_end;
-    if (snap_off + m0 > Lay.snap_cap) {
-      if (stats) snprintf(stats->message, sizeof(stats->message), "snapshot capacity exceeded");
-      return RCP_ERR_WORKSPACE;
+    if (hstate->status == 99 || hstate->status == 97) {
+      if (stats)
+        snprintf(stats->message, sizeof(stats->message), "panel %s at k=%d",
+                 hstate->status == 99 ? "exchange watchdog fired" : "snapshot capacity exceeded", k0);
+      return RCP_ERR_CUDA;
     }
-    RCP_LAUNCH(launch_gather(n, k0, k_end, t, tpad, ((mp + 127) / 128) * 128, pol, Lbuf, W, permb[pcur],
-                            permb[pcur ^ 1], snap + snap_off, phys, Lneg, Wg, L11c, st));
-    panels.push_back(PanelRecord{k0, k_end, snap_off});
-    snap_off += m0;
-    if (mp > 0 && t > 0) {
-      EventPair& es = new_pair(ev_schur);
-      RCP_CHECK(cudaEventRecord(es.a, st));
-      RCP_LAUNCH(launch_schur_update(n, k_end, mp, Lneg, Wg, tpad, t, A[curA], phys, A[curA ^ 1], st));
-      RCP_CHECK(cudaEventRecord(es.b, st));
-      schur_flops += (double)t * (double)mp * (double)(mp + 1);
-      h_mul += (long long)t * (mp * (mp + 1) / 2);  // _apply_trailing (factor.py:377-378)
-      h_add += (long long)t * (mp * (mp + 1) / 2);
-      curA ^= 1;
-      if (!q1) {
-        // sketch correction once per panel (factor.py:554-565)
-        h_mul += (long long)t * P * mp + (long long)(t * (t - 1) / 2) * mp;
-        h_add += (long long)t * P * mp + (long long)(t * (t - 1) / 2) * mp;
-        RCP_LAUNCH(launch_ysolve(n, P, k0, t, tpad, pol, B[curB], L11c, Y, st));
-        RCP_LAUNCH(launch_sketch_correction(P, mp, k_end, Y, tpad, t, Lneg, B[curB], phys, B[curB ^ 1], st));
+    if (m0 > 1) {  // the stopped / tripped panel's sketch norms (factor.py:576-577, 608-610)
+      h_mul += (long long)P * (m0 - 1);
+      h_add += (long long)P * (m0 - 1);
+      h_cmp += m0 - 1;
+    }
+    if (hstate->status == 2) {  // confirmed collapse: deficient tail (factor.py:405-410, 381-385)
+      stop_k0 = k0;
+      break;
+    }
+    // guard trip: fresh projection of the active block (factor.py:392-404), relaunch panel tp
+    if (!q1 && m0 > 1) {  // charged again by the relaunch's commit -> undo the extra charge
+      h_mul -= (long long)P * (m0 - 1);
+      h_add -= (long long)P * (m0 - 1);
+      h_cmp -= m0 - 1;
+    }
+    if (q1 && m0 > 1) {  // q = 1: the relaunch charges the same step's norms itself
+      h_mul -= (long long)P * (m0 - 1);
+      h_add -= (long long)P * (m0 - 1);
+      h_cmp -= m0 - 1;
+    }
+    if (!draw) {
+      if (stats) snprintf(stats->message, sizeof(stats->message), "guard recompute needs normals at k=%d", k0);
+      return RCP_ERR_NEED_NORMALS;
+    }
+    draw_buf.resize((size_t)P * m0);
+    if (draw(draw_ctx, P, m0, draw_buf.data()) != 0) return RCP_ERR_NEED_NORMALS;
+    RCP_CHECK(cudaMemcpyAsync(omg, draw_buf.data(), sizeof(double) * (size_t)P * m0, cudaMemcpyHostToDevice, st));
+#if !RCP_FULL_STORAGE
+    RCP_LAUNCH(launch_mirror_lower(n, k0, A[curA], st));  // the projection reads full columns
+#endif
+    RCP_LAUNCH(launch_sketch_gemm(P, m0, omg, m0, A[curA] + k0 + (int64_t)k0 * n, n, B[curB], k0, st));
+    recomputes += 1;
+    delta += 1.0 / c.robust_r;
+    thr = std::pow(DBL_EPSILON, delta);
+    guard_req = 2;
+    hdesc[0] = PanelDesc{k0, 1, tp, 0, 0, 0, so};
+    RCP_CHECK(cudaMemcpyAsync(ddesc + (tp & 1), hdesc, sizeof(PanelDesc), cudaMemcpyHostToDevice, st));
+    RCP_CHECK(cudaMemsetAsync(&dstate->status, 0, sizeof(int), st));
+    int neg1 = -1;
+    RCP_CHECK(cudaMemcpyAsync(&dstate->stop_pidx, &neg1, sizeof(int), cudaMemcpyHostToDevice, st));
+    RCP_CHECK(cudaStreamSynchronize(st));  // neg1 / hdesc are host stack / pinned values
+    batch = 1;
+  }
+  if (stop_k0 >= 0) {
+    RCP_LAUNCH(launch_deficient_fill(n, stop_k0, permb[pcur], perm, d_diag, d_off, pattern, st));
+    deficient_from = stop_k0;
+  }
+  // committed panels: records for the assembly, flop and op-counter bookkeeping
+  {
+    int np = 0;
+    RCP_CHECK(cudaMemcpyAsync(hstate, dstate, sizeof(PanelState), cudaMemcpyDeviceToHost, st));
+    RCP_CHECK(cudaStreamSynchronize(st));
+    np = hstate->panels_done;
+    std::vector<PanelLog> logs((size_t)np);
+    if (np > 0) {
+      RCP_CHECK(cudaMemcpyAsync(logs.data(), dplog, sizeof(PanelLog) * (size_t)np, cudaMemcpyDeviceToHost, st));
+      RCP_CHECK(cudaStreamSynchronize(st));
+    }
+    for (const PanelLog& lg : logs) {
+      panels.push_back(PanelRecord{lg.k0, lg.k_end, (int64_t)lg.snap_off});
+      const int t = lg.k_end - lg.k0;
+      const long long mp = n - lg.k_end;
+      const int m0 = lg.m0;
+      if (!q1 && m0 > 1) {  // preselect norms (factor.py:576-577)
+        h_mul += (long long)P * (m0 - 1);
+        h_add += (long long)P * (m0 - 1);
+        h_cmp += m0 - 1;
       }
-      curB ^= 1;  // q = 1: the panel kernel already wrote the per-step-updated sketch
+      for (int j = 0; j < lg.qn; ++j) {  // QRCP slots (sketch.py:135-169 via factor.py:586-599)
+        h_cmp += m0 - 1 - j;
+        h_mul += 2LL * P * (m0 - j);
+        h_add += 2LL * P * (m0 - j);
+      }
+      if (mp > 0 && t > 0) {
+        schur_flops += (double)t * (double)mp * (double)(mp + 1);
+        h_mul += (long long)t * (mp * (mp + 1) / 2);  // _apply_trailing (factor.py:377-378)
+        h_add += (long long)t * (mp * (mp + 1) / 2);
+        if (!q1) {
+          h_mul += (long long)t * P * mp + (long long)(t * (t - 1) / 2) * mp;
+          h_add += (long long)t * P * mp + (long long)(t * (t - 1) / 2) * mp;
+        }
+      }
     }
-    pcur ^= 1;
-    k = k_end;
   }
 
   // ---- assemble L in final order + statistics (factor.py:514-538)

@@ -79,6 +79,7 @@ dmma_gemm_kernel(OperandDesc A, OperandDesc B, int64_t K, TileMap map, Epi epi) 
   constexpr int MF = WM / 8, NF = WN / 8;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   auto& sm = *reinterpret_cast<GemmSmem<BM, BN, STAGES>*>(smem_raw);
+  if (!epi.prepare(map, K, B)) return;  // device-side dimensions (no-op for most epilogues)
 
   int64_t m0, n0;
   if (!map(blockIdx.x, m0, n0)) return;
@@ -188,6 +189,20 @@ struct RectMap {
     m0 = tm * bm;
     n0 = tn * bn;
     return true;
+  }
+};
+
+// Column-major tile enumeration (bid -> tm = bid % tiles_m, tn = bid / tiles_m); tiles with
+// tn >= tiles_n (which an epilogue may lower on the device) are skipped.
+struct ColMajorRectMap {
+  int64_t tiles_n;
+  int64_t tiles_m;
+  int bm, bn;
+  RCP_D bool operator()(int bid, int64_t& m0, int64_t& n0) const {
+    const int64_t tm = bid % tiles_m, tn = bid / tiles_m;
+    m0 = tm * bm;
+    n0 = tn * bn;
+    return tn < tiles_n;
   }
 };
 

@@ -5,6 +5,7 @@
 #include <algorithm>
 #include <cfloat>
 #include "misc.cuh"
+#include "panel.cuh"
 #include "rcp_common.cuh"
 
 namespace rcp {
@@ -91,7 +92,16 @@ __global__ void gather_kernel(int64_t n, int k0, int k_end, int t, int tpad, int
                               const double* __restrict__ W, const int* __restrict__ perm_cur,
                               int* __restrict__ perm_next, int* __restrict__ snap,
                               int* __restrict__ phys, double* __restrict__ Lneg, double* __restrict__ Wg,
-                              double* __restrict__ L11) {
+                              double* __restrict__ L11, const PanelDesc* __restrict__ d) {
+  if (d) {  // device-driven: panel geometry from the committed descriptor
+    if (!d->ok) return;
+    k0 = d->k0;
+    k_end = d->k_end;
+    t = d->t;
+    const int64_t mp_ = n - k_end;
+    rows_pad = ((mp_ + 127) / 128) * 128;
+    snap += d->snap_off;
+  }
   // compact unit-lower panel block L11 (t x t, row-major ld t) in logical order, for ysolve
   {
     const int64_t nthreads = (int64_t)gridDim.x * blockDim.x * blockDim.y;
@@ -133,7 +143,12 @@ __global__ void gather_kernel(int64_t n, int k0, int k_end, int t, int tpad, int
 // CTA, 16 lanes per row.
 __global__ void ysolve_kernel(int64_t n, int P, int k0, int t, int tpad, const int* __restrict__ phys_of_log,
                               const double* __restrict__ Bin, const double* __restrict__ L11g,
-                              double* __restrict__ Y) {
+                              double* __restrict__ Y, const PanelDesc* __restrict__ d) {
+  if (d) {
+    if (!d->ok || d->t <= 0 || d->k_end >= n) return;
+    k0 = d->k0;
+    t = d->t;
+  }
   extern __shared__ double sm[];
   double* L11 = sm;                 // [t][t]
   double* yv = sm + (size_t)t * t;  // [16][tpad]
@@ -249,21 +264,21 @@ cudaError_t launch_sketch_norm_max(const double* B, int P, int64_t ncols, double
 
 cudaError_t launch_gather(int64_t n, int k0, int k_end, int t, int tpad, int64_t rows_pad, const int* phys_of_log,
                           const double* Lbuf, const double* W, const int* perm_cur, int* perm_next, int* snap,
-                          int* phys, double* Lneg, double* Wg, double* L11, cudaStream_t st) {
+                          int* phys, double* Lneg, double* Wg, double* L11, cudaStream_t st, const PanelDesc* d) {
   dim3 block(32, 8);
   int64_t rows = rows_pad > (n - k0) ? rows_pad : (n - k0);
   unsigned grid = (unsigned)std::min<int64_t>((rows + 7) / 8, 148 * 16);
   gather_kernel<<<grid, block, 0, st>>>(n, k0, k_end, t, tpad, rows_pad, phys_of_log, Lbuf, W, perm_cur,
-                                        perm_next, snap, phys, Lneg, Wg, L11);
+                                        perm_next, snap, phys, Lneg, Wg, L11, d);
   return cudaGetLastError();
 }
 
 cudaError_t launch_ysolve(int64_t n, int P, int k0, int t, int tpad, const int* phys_of_log, const double* Bin,
-                          const double* L11, double* Y, cudaStream_t st) {
-  size_t smem = sizeof(double) * ((size_t)t * t + 16 * (size_t)tpad);
+                          const double* L11, double* Y, cudaStream_t st, const PanelDesc* d) {
+  size_t smem = sizeof(double) * ((size_t)t * t + 16 * (size_t)tpad);  // t: an upper bound when d != nullptr
   cudaError_t e = cudaFuncSetAttribute(ysolve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  ysolve_kernel<<<(unsigned)((P + 15) / 16), 256, smem, st>>>(n, P, k0, t, tpad, phys_of_log, Bin, L11, Y);
+  ysolve_kernel<<<(unsigned)((P + 15) / 16), 256, smem, st>>>(n, P, k0, t, tpad, phys_of_log, Bin, L11, Y, d);
   return cudaGetLastError();
 }
 

@@ -5,14 +5,17 @@
 
 namespace rcp {
 
+struct PanelDesc;
+
 cudaError_t launch_validate_copy(const double* a, int64_t lda, int64_t n, double* out, int* flags, double* amax,
                                  cudaStream_t st);
 cudaError_t launch_sketch_norm_max(const double* B, int P, int64_t ncols, double* out, cudaStream_t st);
 cudaError_t launch_gather(int64_t n, int k0, int k_end, int t, int tpad, int64_t rows_pad, const int* phys_of_log,
                           const double* Lbuf, const double* W, const int* perm_cur, int* perm_next, int* snap,
-                          int* phys, double* Lneg, double* Wg, double* L11, cudaStream_t st);
+                          int* phys, double* Lneg, double* Wg, double* L11, cudaStream_t st,
+                          const PanelDesc* d = nullptr);
 cudaError_t launch_ysolve(int64_t n, int P, int k0, int t, int tpad, const int* phys_of_log, const double* Bin,
-                          const double* L11, double* Y, cudaStream_t st);
+                          const double* L11, double* Y, cudaStream_t st, const PanelDesc* d = nullptr);
 cudaError_t launch_assemble_panel(int64_t n, int k0, int k_end, const int* snap, int* pos_of_orig,
                                   const int64_t* perm, const double* Lbuf, double* L, double* maxmult,
                                   cudaStream_t st);
@@ -26,14 +29,15 @@ cudaError_t launch_iota(int64_t n, int* p, cudaStream_t st);
 // ---- FP64 tensor-core GEMMs (schur.cu)
 // A_out[k+i, k+j] = A_in(phys[i], phys[j]) - sum_s L[i,s] W[j,s]   for i >= j (lower tiles)
 cudaError_t launch_schur_update(int64_t n, int64_t k, int64_t mp, const double* Lneg, const double* Wg, int tpad,
-                                int K, const double* A_in, const int* phys, double* A_out, cudaStream_t st);
+                                int K, const double* A_in, const int* phys, double* A_out, cudaStream_t st,
+                                const PanelDesc* d = nullptr);
 // B[:, col0 + j] = sum_i Omega[r, i] * A[i, j]   (Omega row-major P x m, A col-major ld lda, full columns)
 cudaError_t launch_sketch_gemm(int P, int64_t m, const double* omega, int64_t ldo, const double* A, int64_t lda,
                                double* B, int64_t col0, cudaStream_t st);
 // B_out[:, k+j] = B_in[:, phys[j]] - Y * L[j,:]^T  (Y row-major P x tpad; Lneg = -L rows)
 cudaError_t launch_sketch_correction(int P, int64_t mp, int64_t k, const double* Y, int tpad, int K,
                                      const double* Lneg, const double* B_in, const int* phys, double* B_out,
-                                     cudaStream_t st);
+                                     cudaStream_t st, const PanelDesc* d = nullptr, int64_t n = 0);
 cudaError_t gemm_init_attributes();
 
 }  // namespace rcp

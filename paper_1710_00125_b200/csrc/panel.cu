@@ -144,9 +144,26 @@ RCP_D long long prof_now() { return clock64(); }
 
 }  // namespace
 
-__global__ void __launch_bounds__(kPanelThreads, 1) panel_kernel(PanelParams p) {
+__global__ void __launch_bounds__(kPanelThreads, 1) panel_kernel(PanelParams pin) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int cta = blockIdx.x, tid = threadIdx.x, nthr = blockDim.x;
+  PanelParams p = pin;
+  if (p.desc) {  // device-driven: this panel's k0 comes from the descriptor chain
+    const int run = p.desc->run;
+    if (!run) return;
+    const PanelGeom g = panel_geometry(p.n, p.desc->k0, p.b, p.q, p.P, p.num_sms, p.smem_budget);
+    p.k0 = p.desc->k0;
+    p.width = g.width;
+    p.G = g.G;
+    p.R = g.R;
+    p.Wn = g.Wn;
+    p.qn = g.qn;
+    p.qmode = g.qmode;
+    p.Rs = g.Rs;
+    p.Ls = g.Ls;
+    if (!(g.qn > 0 || p.q1)) p.guard_mode = 0;
+    if (cta >= g.G) return;
+  }
   const int64_t n = p.n;
   const int k0 = p.k0, P = p.P, R = p.R, G = p.G, Wn = p.Wn;
   const int m0 = static_cast<int>(n - k0);
@@ -1203,6 +1220,58 @@ __global__ void __launch_bounds__(kPanelThreads, 1) panel_kernel(PanelParams p) 
   if (prof) atomicAdd(reinterpret_cast<unsigned long long*>(&p.st->cyc[7]), (unsigned long long)(prof_now() - c_kernel0));
 #undef PROF_BEGIN
 #undef PROF_END
+}
+
+// Finalises panel desc_in (ok, k_end, t) for the gather / Schur / sketch kernels of the same
+// panel, logs it, and writes the next panel's descriptor.  Guard events and numerical errors
+// stop the chain (run = 0) and record the panel index for the host.
+__global__ void panel_commit_kernel(PanelDesc* din, PanelDesc* dout, PanelLog* plog, PanelState* st, int64_t n,
+                                    int b, int q, int P, long long snap_cap) {
+  const PanelDesc d = *din;
+  PanelDesc o = d;
+  o.run = 0;
+  o.ok = 0;
+  o.pidx = d.pidx + 1;
+  if (!d.run) {
+    din->ok = 0;
+    *dout = o;
+    return;
+  }
+  if (st->status != 0 || st->err != LLONG_MAX) {
+    din->ok = 0;
+    if (st->stop_pidx < 0) st->stop_pidx = d.pidx;
+    *dout = o;
+    return;
+  }
+  const int k_end = st->k_end, t = st->t_end;
+  const int m0 = (int)(n - d.k0);
+  const int width = m0 < b ? m0 : b;
+  int qn = 0;
+  if (q > 1 && m0 > 1) {
+    qn = q < width ? q : width;
+    qn = qn < m0 ? qn : m0;
+    qn = qn < P ? qn : P;
+  }
+  din->k_end = k_end;
+  din->t = t;
+  din->ok = 1;
+  plog[d.pidx] = PanelLog{d.k0, k_end, m0, qn, d.snap_off};
+  st->panels_done = d.pidx + 1;
+  o.k0 = k_end;
+  o.snap_off = d.snap_off + m0;
+  o.run = (k_end < n) ? 1 : 0;
+  if (o.snap_off + (n - k_end) > snap_cap) {  // cannot happen (every panel eliminates a column)
+    st->status = 97;
+    if (st->stop_pidx < 0) st->stop_pidx = d.pidx + 1;
+    o.run = 0;
+  }
+  *dout = o;
+}
+
+cudaError_t launch_panel_commit(PanelDesc* din, PanelDesc* dout, PanelLog* plog, PanelState* st, int64_t n, int b,
+                                int q, int P, long long snap_cap, cudaStream_t stream) {
+  panel_commit_kernel<<<1, 1, 0, stream>>>(din, dout, plog, st, n, b, q, P, snap_cap);
+  return cudaGetLastError();
 }
 
 cudaError_t panel_init_attributes(int max_dyn_smem) {

@@ -1,9 +1,84 @@
 // Panel-kernel parameter/state structs shared by panel.cu and the host driver.
 #pragma once
+#include <climits>
+#include <cstddef>
 #include <cstdint>
 #include <cuda_runtime.h>
 
 namespace rcp {
+
+#define RCP_PG __host__ __device__ inline
+
+constexpr int kPanelRowsMin = 32;   // fewest rows per CTA before the panel uses fewer CTAs
+constexpr int kPanelMaxCTAs = 160;  // == kMaxSMs (exchange buffers are sized for it)
+constexpr int kPanelRegRows = 32;   // QRCP register mode: sketch rows [0, 32) in registers
+
+// Device-driven host loop: the host enqueues panels back to back without reading their
+// outcome.  Panel p reads desc[p & 1]; its commit kernel finalises that descriptor (ok,
+// k_end, t) for the gather / Schur / sketch kernels of the same panel and writes the next
+// panel's descriptor desc[(p + 1) & 1].  A panel whose descriptor has run == 0 (finished,
+// guard event or error upstream) and every kernel reading ok == 0 is a no-op.
+struct PanelDesc {
+  int k0;      // first logical column of the panel
+  int run;     // 1: the panel must run
+  int pidx;    // panel index
+  int ok;      // set by the commit kernel: the panel completed normally
+  int k_end;   // outcome (valid when ok)
+  int t;
+  long long snap_off;  // offset of the panel's start-order snapshot
+};
+
+// Per-panel record for the final assembly and the statistics.
+struct PanelLog {
+  int k0, k_end, m0, qn;
+  long long snap_off;
+};
+
+// Launch geometry of one panel (shared by the host and the kernel).
+struct PanelGeom {
+  int m0, width, G, R, Wn, qn, qmode, Rs, Ls;
+};
+
+RCP_PG int pg_min(int a, int b) { return a < b ? a : b; }
+RCP_PG int pg_max(int a, int b) { return a > b ? a : b; }
+
+RCP_PG PanelGeom panel_geometry(int64_t n, int k0, int b, int q, int P, int num_sms, int smem_budget) {
+  PanelGeom g{};
+  g.m0 = (int)(n - k0);
+  if (g.m0 <= 0) return g;
+  g.width = pg_min(b, g.m0);
+  int G = pg_min(num_sms, pg_max(1, (g.m0 + kPanelRowsMin - 1) / kPanelRowsMin));
+  if (G > kPanelMaxCTAs) G = kPanelMaxCTAs;
+  const int R = (g.m0 + G - 1) / G;
+  g.G = (g.m0 + R - 1) / R;
+  g.R = R;
+  g.Wn = g.width + 2;
+  g.qn = (q > 1 && g.m0 > 1) ? pg_min(pg_min(q, g.width), pg_min(g.m0, P)) : 0;
+  auto a16 = [](long long x) { return (x + 15) & ~15LL; };
+  const long long fixed = a16(4LL * g.Wn) + a16(4LL * R) + a16(8LL * P) + 4 * a16(8LL * g.Wn);
+  const long long avail = (long long)smem_budget - fixed;
+  g.qmode = 0;
+  g.Rs = 0;
+  if (g.qn > 0) {
+    const int ps_reg = P - pg_min(P, kPanelRegRows);
+    const long long need_reg = 8LL * ps_reg * R + 64;
+    if (R <= 256 && need_reg <= avail) {
+      g.qmode = 1;
+      g.Rs = R;
+    } else {
+      long long rs = (avail - 12LL * R - 64) / (8LL * P);
+      if (rs > R) rs = R;
+      if (rs < 0) rs = 0;
+      g.Rs = (int)rs;
+    }
+  }
+  const bool q1 = (q == 1);
+  long long ls = q1 ? (avail - 24LL * R - 8LL * P * R - 8LL * P - 128) / (8LL * R) : (avail - 24LL * R - 64) / (8LL * R);
+  if (ls > g.Wn) ls = g.Wn;
+  if (ls < 0) ls = 0;
+  g.Ls = (int)ls;
+  return g;
+}
 
 // Device-resident state that persists across panel launches.
 struct PanelState {
@@ -15,6 +90,8 @@ struct PanelState {
   int n_steps;         // decisions taken (cumulative)
   int n_2x2;           // 2x2 blocks (cumulative)
   int end_reason;      // why the panel ended early: 0 none, 1 2x2 defer, 2 q=1 guard defer
+  int stop_pidx;       // first panel that ended with a guard event / error (-1: none)
+  int panels_done;     // panels committed
   long long cnt[4];    // step op counters (mults, adds, divs, comps), cumulative
   // SM-cycle profile of CTA 0 (cumulative), see kProfNames in capi.cu
   long long cyc[16];
@@ -75,10 +152,15 @@ struct PanelParams {
   unsigned long long* sdll;  // SBKP decision broadcast by the reducer CTA [2][kXWords]
   unsigned long long* qdll;  // QRCP decision header [2][8]
   PanelState* st;
+  // device-driven geometry (desc != nullptr): k0 from the descriptor, the rest recomputed
+  const PanelDesc* desc;
+  int b, q, num_sms, smem_budget;
 };
 
 cudaError_t panel_init_attributes(int max_dyn_smem);
 cudaError_t launch_panel(const PanelParams& prm, int G, size_t smem, cudaStream_t st);
+cudaError_t launch_panel_commit(PanelDesc* din, PanelDesc* dout, PanelLog* plog, PanelState* st, int64_t n, int b,
+                                int q, int P, long long snap_cap, cudaStream_t stream);
 int panel_static_smem_bytes();
 
 }  // namespace rcp

@@ -13,6 +13,8 @@ namespace {
 struct SketchEpi {
   static constexpr bool kHasInput = false;
   static constexpr bool kMirror = false;
+  template <class Map>
+  RCP_D bool prepare(Map&, int64_t&, OperandDesc&) { return true; }
   RCP_D double* cout_mirror(int64_t, int64_t) const { return nullptr; }
   double* b;
   int64_t P, ncols, col0;
@@ -26,6 +28,20 @@ struct SketchEpi {
 struct SketchCorrEpi {
   static constexpr bool kHasInput = true;
   static constexpr bool kMirror = false;
+  // device-driven: mp / k / K / tile count from the committed panel descriptor
+  const PanelDesc* d;
+  int64_t n;
+  template <class Map>
+  RCP_D bool prepare(Map& map, int64_t& K, OperandDesc& B) {
+    if (!d) return true;
+    if (!d->ok || d->t <= 0 || d->k_end >= n) return false;
+    k = d->k_end;
+    mp = n - k;
+    K = ((d->t + kBK - 1) / kBK) * kBK;
+    B.rows = mp;
+    map.tiles_n = (mp + 127) / 128;
+    return true;
+  }
   RCP_D double* cout_mirror(int64_t, int64_t) const { return nullptr; }
   const double* bin;
   double* bout;
@@ -61,13 +77,22 @@ cudaError_t gemm_init_attributes() {
   e = cudaFuncSetAttribute(dmma_gemm_kernel<64, 128, kRectStages, 1, RectMap, SketchEpi>,
                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gemm_smem_bytes<64, 128, kRectStages>());
   if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(dmma_gemm_kernel<64, 128, kRectStages, 2, RectMap, SketchCorrEpi>,
+  e = cudaFuncSetAttribute(dmma_gemm_kernel<64, 128, kRectStages, 2, ColMajorRectMap, SketchCorrEpi>,
                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gemm_smem_bytes<64, 128, kRectStages>());
   return e;
 }
 
 cudaError_t launch_schur_update(int64_t n, int64_t k, int64_t mp, const double* Lneg, const double* Wg, int tpad,
-                                int K, const double* A_in, const int* phys, double* A_out, cudaStream_t st) {
+                                int K, const double* A_in, const int* phys, double* A_out, cudaStream_t st,
+                                const PanelDesc* d) {
+  if (d) {  // persistent grid; the kernel reads the panel outcome
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    schur_ws_kernel<<<(unsigned)sms, ws::kThreads, schur_ws_smem_bytes(), st>>>(Lneg, Wg, tpad, 0, A_in, A_out, phys,
+                                                                               n, 0, 0, 0, d);
+    return cudaGetLastError();
+  }
   if (mp <= 0 || K <= 0) return cudaSuccess;
   const int64_t nbi = (mp + kSchurBM - 1) / kSchurBM;
   const long long tiles = nbi * (nbi + 1);  // row block I has 2I+2 column blocks of 64
@@ -77,7 +102,7 @@ cudaError_t launch_schur_update(int64_t n, int64_t k, int64_t mp, const double* 
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const long long grid = std::min<long long>(tiles, sms);
   schur_ws_kernel<<<(unsigned)grid, ws::kThreads, schur_ws_smem_bytes(), st>>>(Lneg, Wg, tpad, Kl, A_in, A_out, phys,
-                                                                               n, k, mp, tiles);
+                                                                               n, k, mp, tiles, nullptr);
   return cudaGetLastError();
 }
 
@@ -102,15 +127,16 @@ cudaError_t launch_sketch_gemm(int P, int64_t m, const double* omega, int64_t ld
 
 cudaError_t launch_sketch_correction(int P, int64_t mp, int64_t k, const double* Y, int tpad, int K,
                                      const double* Lneg, const double* B_in, const int* phys, double* B_out,
-                                     cudaStream_t st) {
+                                     cudaStream_t st, const PanelDesc* d, int64_t n) {
+  // with d: mp / k / K are upper bounds for the grid; the kernel reads the actual values
   if (mp <= 0 || K <= 0) return cudaSuccess;
   const int64_t tm = (P + 63) / 64, tn = (mp + 127) / 128;
   const int Kl = ((K + kBK - 1) / kBK) * kBK;
   OperandDesc a{Y, tpad, P, tpad};
   OperandDesc b{Lneg, tpad, mp, tpad};
-  SketchCorrEpi epi{B_in, B_out, phys, P, mp, k};
-  RectMap map{tn, 64, 128};
-  dmma_gemm_kernel<64, 128, kRectStages, 2, RectMap, SketchCorrEpi>
+  SketchCorrEpi epi{d, n, B_in, B_out, phys, P, mp, k};
+  ColMajorRectMap map{tn, tm, 64, 128};
+  dmma_gemm_kernel<64, 128, kRectStages, 2, ColMajorRectMap, SketchCorrEpi>
       <<<(unsigned)(tm * tn), kGemmThreads, gemm_smem_bytes<64, 128, kRectStages>(), st>>>(a, b, Kl, map, epi);
   return cudaGetLastError();
 }

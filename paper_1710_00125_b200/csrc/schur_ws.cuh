@@ -13,6 +13,7 @@
 // Roles synchronise through shared-memory mbarriers (cp.async.mbarrier.arrive for data
 // arrival), so the tensor pipe keeps issuing while the previous tile drains to HBM.
 #pragma once
+#include "panel.cuh"
 #include "gemm_dmma.cuh"
 
 namespace rcp {
@@ -99,8 +100,16 @@ RCP_D void tile_of(long long x, int64_t& m0, int64_t& n0) {
 __global__ void __launch_bounds__(ws::kThreads, 1)
 schur_ws_kernel(const double* __restrict__ Lneg, const double* __restrict__ Wg, int tpad, int Kl,
                 const double* __restrict__ ain, double* __restrict__ aout, const int* __restrict__ phys, int64_t n,
-                int64_t k, int64_t mp, long long tiles) {
+                int64_t k, int64_t mp, long long tiles, const PanelDesc* __restrict__ d) {
   using namespace ws;
+  if (d) {  // device-driven: the panel outcome comes from the committed descriptor
+    if (!d->ok || d->t <= 0 || d->k_end >= n) return;
+    k = d->k_end;
+    mp = n - k;
+    Kl = ((d->t + kBK - 1) / kBK) * kBK;
+    const long long nbi = (mp + BM - 1) / BM;
+    tiles = nbi * (nbi + 1);
+  }
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;

@@ -182,6 +182,8 @@ __global__ void scale_ld_kernel(int64_t n, const double* __restrict__ L, const d
 struct ReconEpi {
   static constexpr bool kHasInput = false;
   static constexpr bool kMirror = false;
+  template <class Map>
+  RCP_D bool prepare(Map&, int64_t&, OperandDesc&) { return true; }
   RCP_D double* cout_mirror(int64_t, int64_t) const { return nullptr; }
   double* out;
   int64_t n;
