@@ -10,9 +10,9 @@ P = b + 16 = 144 (reference FactorConfig(strategy="rcp", b=128, q=128, p=144)).
 resident in HBM, max over ranks), summed over ranks.  The input (8.6 GB) is far
 larger than the 126 MB L2, so no L2 flush is needed between steps.
 
-Multi-GPU (torchrun, one process per GPU): round 1 runs independent replicas
-(each rank factors its own matrix; "scaling": "weak"); the 1D block-cyclic
-distributed factorization is future work.
+Multi-GPU (torchrun, one process per GPU): one factorization per step whose trailing Schur
+updates are shared by all N GPUs over NVLink peer memory (paper_1710_00125_b200.dist; rank 0
+runs the panels); "scaling": "strong", value = n^3/3 / max-over-ranks step time.
 
 ``--impl reference`` times the reference algorithm's CPU implementation (the
 oracle port in oracle/rcp_oracle.py — the reference is pure Python and cannot be
@@ -67,9 +67,11 @@ def workload_name(a):
             f"P=b+{a.p - a.b}={a.p} sketch rows, seed={a.seed}")
 
 
-def cfg_dict(a):
+def cfg_dict(a, world: int = 1):
     return {"workload": workload_name(a), "n": a.n, "b": a.b, "q": a.b, "p_sketch": a.p,
-            "oversampling": a.p - a.b, "parallelism": "replicas",
+            "oversampling": a.p - a.b,
+            "parallelism": "single GPU" if world == 1 else
+                           f"{world} GPUs: panels on rank 0, trailing-update tiles dealt round robin over NVLink",
             "l2": "input 8.6 GB >> 126 MB L2 (no flush needed)"}
 
 
@@ -189,7 +191,7 @@ def run_reference(args, rank: int):
         "impl": "reference", "metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tsum / max(1, len(res["times"])),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (seeded numpy Philox type6)", "config": cfg_dict(args),
+        "data": "synthetic (seeded numpy Philox type6)", "config": cfg_dict(args, args.gpus),
         "cpu_baseline": {"value": value, "unit": "GFLOP/s", "cores": cores_used(), "kind": "port",
                          "sample": sample},
         "e2e": {"value": value, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -199,24 +201,36 @@ def run_reference(args, rank: int):
 
 # ----------------------------------------------------------------------------- B200 arm
 def run_b200(args, rank: int, world: int, local_rank: int):
+    """C3: one factorization per step.  N > 1: the same single factorization with its trailing
+    updates shared by all N GPUs (paper_1710_00125_b200.dist; strong scaling)."""
     import torch
     import torch.distributed as dist
 
     from paper_1710_00125_b200 import api, gallery
+    from paper_1710_00125_b200 import dist as rdist
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     n, P = args.n, args.p
     cfg = api.FactorConfig(strategy="rcp", b=args.b, q=args.b, p=P, seed=args.seed)
 
-    a_host = gallery.type6(n, args.seed + rank)
-    a_pin = torch.from_numpy(a_host).pin_memory()
-    a_dev = a_pin.to(dev, non_blocking=True)
-    omega = torch.from_numpy(np.random.Generator(np.random.Philox(cfg.seed)).standard_normal((P, n))).to(dev)
-    ws = torch.empty(api.workspace_bytes(n, cfg), dtype=torch.uint8, device=dev)
+    a_host = a_pin = a_dev = omega = ws = None
+    if rank == 0:
+        a_host = gallery.type6(n, args.seed)
+        a_pin = torch.from_numpy(a_host).pin_memory()
+        a_dev = a_pin.to(dev, non_blocking=True)
+        omega = torch.from_numpy(np.random.Generator(np.random.Philox(cfg.seed)).standard_normal((P, n))).to(dev)
+        if world == 1:
+            ws = torch.empty(api.workspace_bytes(n, cfg), dtype=torch.uint8, device=dev)
     out = None
+
+    def one_step(out):
+        if world == 1:
+            return api.factor_device(a_dev, cfg, omega=omega, workspace=ws, out=out)
+        return rdist.factor_distributed_device(a_dev, cfg)
+
     for _ in range(max(3, args.warmup)):
-        out = api.factor_device(a_dev, cfg, omega=omega, workspace=ws, out=out)
+        out = one_step(out)
     torch.cuda.synchronize()
 
     clk = ClockSampler(local_rank)
@@ -229,10 +243,11 @@ def run_b200(args, rank: int, world: int, local_rank: int):
     e0.record(stream)
     schur_ms, schur_flops, panel_ms = 0.0, 0.0, 0.0
     for _ in range(args.steps):
-        out = api.factor_device(a_dev, cfg, omega=omega, workspace=ws, out=out)
-        schur_ms += out.stats["t_schur_ms"]
-        schur_flops += out.stats["schur_flops"]
-        panel_ms += out.stats["t_panel_ms"]
+        out = one_step(out)
+        if out is not None:
+            schur_ms += out.stats["t_schur_ms"]
+            schur_flops += out.stats["schur_flops"]
+            panel_ms += out.stats["t_panel_ms"]
     e1.record(stream)
     torch.cuda.synchronize()
     if world > 1:
@@ -244,34 +259,37 @@ def run_b200(args, rank: int, world: int, local_rank: int):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max = float(t.item())
     flops = n ** 3 / 3.0
-    value = world * flops / (ms_max / 1e3) / 1e9
-    stats = dict(out.stats)
+    value = flops / (ms_max / 1e3) / 1e9  # one factorization per step on all N GPUs together
+    stats = dict(out.stats) if out is not None else {}
 
-    # quick accuracy check of the last factorization on the device (solve + residual)
-    rhs = torch.from_numpy(gallery.rhs(n, 1)).to(dev)
-    x, _ = api.solve_device(out, rhs)
-    resid = float((a_dev @ x - rhs).abs().max())
-    bwd = resid / (float(a_dev.abs().sum(dim=1).max()) * float(x.abs().max()))
+    bwd = None
+    if rank == 0:  # quick accuracy check of the last factorization on the device (solve + residual)
+        rhs = torch.from_numpy(gallery.rhs(n, 1)).to(dev)
+        x, _ = api.solve_device(out, rhs)
+        resid = float((a_dev @ x - rhs).abs().max())
+        bwd = resid / (float(a_dev.abs().sum(dim=1).max()) * float(x.abs().max()))
 
     # end to end through the public API: numpy in (pinned) -> Factorization out
-    e2e_val = None
     h2d = n * n * 8 + P * n * 8
     d2h = n * n * 8 + n * (8 + 8 + 8 + 1)
-    a_np_pinned = a_pin.numpy()
     e2e_times = []
     for _ in range(max(1, args.e2e_steps)):
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
         t0 = time.perf_counter()
-        f = api.factor(a_np_pinned, cfg)
-        _ = f.L[-1, 0]
+        if world == 1:
+            f = api.factor(a_pin.numpy(), cfg)
+        else:
+            f = rdist.factor_distributed(a_pin.numpy() if rank == 0 else None, cfg)
+        if f is not None:
+            _ = f.L[-1, 0]
         e2e_times.append(time.perf_counter() - t0)
         del f
     te = torch.tensor([statistics.median(e2e_times)], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
-    e2e_val = world * flops / float(te.item()) / 1e9
+    e2e_val = flops / float(te.item()) / 1e9
 
     if rank != 0:
         return
@@ -293,25 +311,29 @@ def run_b200(args, rank: int, world: int, local_rank: int):
     achieved = schur_flops / (schur_ms / 1e3) / 1e12 if schur_ms > 0 else None
     line = {
         "metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
-        "warmup": max(3, args.warmup), "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak",
+        "warmup": max(3, args.warmup), "ms_per_step": ms_max, "higher_is_better": True,
+        "scaling": "strong" if world > 1 else "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded numpy Philox type6; Omega from Philox(seed))",
-        "config": cfg_dict(args),
+        "config": cfg_dict(args, world),
         "pct_fp64_peak": 100.0 * value / (world * FP64_PEAK_GFLOPS),
         "fp64_peak": {"value": FP64_PEAK_GFLOPS, "unit": "GFLOP/s", "source": FP64_PEAK_SRC},
         "roofline": {"bound": "tensor", "kernel": "schur_ws_kernel (trailing Schur update, DMMA.8x8x4)",
                      "achieved": achieved, "peak": FP64_PEAK_GFLOPS / 1e3, "unit": "TFLOP/s",
                      "frac": (achieved / (FP64_PEAK_GFLOPS / 1e3)) if achieved else None,
                      "traffic": None,
-                     "algorithmic": "sum over panels of t*m*(m+1) flops (lower-triangle rank-t update)",
+                     "algorithmic": "sum over panels of t*m*(m+1) flops (lower-triangle rank-t update)"
+                                    + (" (rank 0's share of the tiles; achieved over its Schur time)" if world > 1
+                                       else ""),
                      "share_of_step": schur_ms / (ms * args.steps) if ms > 0 else None,
                      "panel_share_of_step": panel_ms / (ms * args.steps) if ms > 0 else None},
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_val, "unit": "GFLOP/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                "path": "paper_1710_00125_b200.factor(numpy array in pinned memory) -> Factorization"},
-        "gpu_launches": int(stats["n_launches"]) * args.steps,
+                "path": ("paper_1710_00125_b200.factor" if world == 1 else "paper_1710_00125_b200.dist.factor_distributed")
+                        + "(numpy array in pinned memory) -> Factorization"},
+        "gpu_launches": int(stats.get("n_launches", 0)) * args.steps,
         "clocks": clocks,
-        "factor_stats": {k: stats[k] for k in ("n_panels", "n_steps", "n_2x2", "recompute_count", "rho_cheap",
-                                               "max_multiplier", "t_panel_ms", "t_schur_ms")},
+        "factor_stats": {k: stats.get(k) for k in ("n_panels", "n_steps", "n_2x2", "recompute_count", "rho_cheap",
+                                                   "max_multiplier", "t_panel_ms", "t_schur_ms")},
         "solve_backward_error": bwd,
     }
     print(json.dumps(line), flush=True)

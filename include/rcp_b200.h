@@ -13,6 +13,10 @@
  *   rcp_solve           <- randldl.solve / solve_many        (solve.py:79-107)
  *   rcp_reconstruct     <- randldl.reconstruct               (factor.py:663-665)
  *   rcp_workspace_bytes    workspace query (no reference counterpart)
+ *   rcp_factor_dist     <- randldl.factor on several GPUs of one node (config C3,
+ *                          "1/2/4/8 GPU"): rank 0 owns the matrix and the panels,
+ *                          the trailing update is dealt over all GPUs (rcp_schur_worker
+ *                          on the other ranks) through NVLink peer memory
  *   rcp_factor_batched  <- a loop of randldl.factor over independent small
  *                          matrices sharing one FactorConfig (BASELINE config C5;
  *                          q = b, n <= 256): one CTA per matrix, no host round trip
@@ -135,6 +139,32 @@ size_t rcp_solve_workspace_bytes(int64_t n, int64_t nrhs);
 /* out (n x n row-major) = L D L^T (factor.py:663-665). */
 int rcp_reconstruct(int64_t n, const double* L, const double* d_diag, const double* d_off,
                     const int8_t* pattern, double* out, void* cuda_stream);
+
+/* ---- several GPUs of one node (C3) --------------------------------------------------------
+ * Rank 0 calls rcp_factor_dist(world = N); ranks 1..N-1 call rcp_schur_worker with rank 0's
+ * workspace mapped into their address space (rcp_ipc_export / rcp_ipc_import of a workspace
+ * obtained from rcp_device_alloc).  Before the workers attach, rank 0 calls rcp_dist_prepare.
+ * Every panel's trailing Schur update (the O(n^3) part) is split tile-round-robin over the N
+ * devices; C-in tiles are read from and results written to rank 0's matrix over NVLink, the
+ * panel operands are copied once per panel.  emulate = 1 runs the N-1 worker parts on this
+ * device instead (same kernels, same results; used by the tests); worker_ws then holds
+ * N-1 slots of rcp_worker_workspace_bytes. */
+int rcp_factor_dist(const rcp_config* cfg, int64_t n, const double* a, int64_t lda,
+                    const double* omega, rcp_draw_fn draw, void* draw_ctx,
+                    void* workspace, size_t workspace_bytes,
+                    int64_t* perm, double* L, double* d_diag, double* d_off, int8_t* pattern,
+                    int8_t* trace_kind, int32_t* trace_r, rcp_stats* stats,
+                    int world, int emulate, void* worker_ws, size_t worker_ws_bytes, void* cuda_stream);
+size_t rcp_worker_workspace_bytes(int64_t n, const rcp_config* cfg);
+int rcp_dist_prepare(int64_t n, const rcp_config* cfg, void* workspace, void* cuda_stream);
+int rcp_schur_worker(const rcp_config* cfg, int64_t n, int rank, int world, void* rank0_workspace,
+                     void* worker_ws, size_t worker_ws_bytes, void* cuda_stream);
+int rcp_device_alloc(size_t bytes, void** ptr);
+int rcp_device_free(void* ptr);
+/* handle_out: 64 bytes (cudaIpcMemHandle_t); base must come from rcp_device_alloc. */
+int rcp_ipc_export(const void* base, void* handle_out);
+int rcp_ipc_import(const void* handle, void** ptr);
+int rcp_ipc_close(void* ptr);
 
 /* ---- batched small matrices (C5) -------------------------------------------------------- */
 

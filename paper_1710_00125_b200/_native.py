@@ -42,6 +42,15 @@ EXPORTED_SYMBOLS = (
     "rcp_batched_workspace_bytes",
     "rcp_factor_batched",
     "rcp_solve_batched",
+    "rcp_factor_dist",
+    "rcp_worker_workspace_bytes",
+    "rcp_dist_prepare",
+    "rcp_schur_worker",
+    "rcp_device_alloc",
+    "rcp_device_free",
+    "rcp_ipc_export",
+    "rcp_ipc_import",
+    "rcp_ipc_close",
 )
 
 
@@ -151,6 +160,26 @@ def load(path: str | os.PathLike | None = None):
     lib.rcp_factor_batched.restype = ctypes.c_int
     lib.rcp_solve_batched.argtypes = [i64, i64, vp, vp, vp, vp, vp, vp, vp, vp, vp]
     lib.rcp_solve_batched.restype = ctypes.c_int
+    lib.rcp_factor_dist.argtypes = [ctypes.POINTER(RcpConfig), i64, vp, i64, vp, DRAW_FN, vp, vp, sz,
+                                    vp, vp, vp, vp, vp, vp, vp, ctypes.POINTER(RcpStats), ctypes.c_int, ctypes.c_int,
+                                    vp, sz, vp]
+    lib.rcp_factor_dist.restype = ctypes.c_int
+    lib.rcp_worker_workspace_bytes.argtypes = [i64, ctypes.POINTER(RcpConfig)]
+    lib.rcp_worker_workspace_bytes.restype = sz
+    lib.rcp_dist_prepare.argtypes = [i64, ctypes.POINTER(RcpConfig), vp, vp]
+    lib.rcp_dist_prepare.restype = ctypes.c_int
+    lib.rcp_schur_worker.argtypes = [ctypes.POINTER(RcpConfig), i64, ctypes.c_int, ctypes.c_int, vp, vp, sz, vp]
+    lib.rcp_schur_worker.restype = ctypes.c_int
+    lib.rcp_device_alloc.argtypes = [sz, ctypes.POINTER(ctypes.c_void_p)]
+    lib.rcp_device_alloc.restype = ctypes.c_int
+    lib.rcp_device_free.argtypes = [vp]
+    lib.rcp_device_free.restype = ctypes.c_int
+    lib.rcp_ipc_export.argtypes = [vp, vp]
+    lib.rcp_ipc_export.restype = ctypes.c_int
+    lib.rcp_ipc_import.argtypes = [vp, ctypes.POINTER(ctypes.c_void_p)]
+    lib.rcp_ipc_import.restype = ctypes.c_int
+    lib.rcp_ipc_close.argtypes = [vp]
+    lib.rcp_ipc_close.restype = ctypes.c_int
     lib.rcp_version.argtypes = []
     lib.rcp_version.restype = ctypes.c_char_p
     _lib = lib

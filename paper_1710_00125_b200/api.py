@@ -308,13 +308,17 @@ def workspace_bytes(n: int, cfg: FactorConfig) -> int:
 
 
 def factor_device(a: torch.Tensor, cfg: FactorConfig | None = None, *, omega: torch.Tensor | None = None,
-                  trace: bool = False, workspace: torch.Tensor | None = None,
-                  out: DeviceFactorization | None = None, **overrides) -> DeviceFactorization:
+                  trace: bool = False, workspace: torch.Tensor | tuple | None = None,
+                  out: DeviceFactorization | None = None, world: int = 1, emulate: bool = False,
+                  **overrides) -> DeviceFactorization:
     """Factor a CUDA float64 symmetric matrix; results stay on the device.
 
     ``omega`` (p x n, CUDA float64) may be passed pre-drawn; it must then be the
     first draw of ``Generator(Philox(cfg.seed))`` for results to match the
-    reference.  ``workspace``/``out`` let a caller reuse device buffers.
+    reference.  ``workspace``/``out`` let a caller reuse device buffers (``workspace`` may also be a
+    raw ``(device_pointer, nbytes)`` pair).  ``world > 1`` shares every trailing update with
+    ``world - 1`` other GPUs running :func:`paper_1710_00125_b200.dist.schur_worker`
+    (``emulate=True``: their parts run on this device, for testing; results are identical).
     """
     cfg = _config(cfg, overrides)
     _check_supported(cfg)
@@ -338,8 +342,18 @@ def factor_device(a: torch.Tensor, cfg: FactorConfig | None = None, *, omega: to
         omega = omega.contiguous()
     c = _native.RcpConfig(cfg.p, cfg.b, cfg.q, cfg.robust_r)
     need = int(lib.rcp_workspace_bytes(n, ctypes.byref(c)))
-    if workspace is None or workspace.numel() < need:
-        workspace = torch.empty(need, dtype=torch.uint8, device=dev)
+    if isinstance(workspace, tuple):
+        ws_ptr, ws_bytes = int(workspace[0]), int(workspace[1])
+        if ws_bytes < need:
+            raise ValueError("workspace too small")
+    else:
+        if workspace is None or workspace.numel() < need:
+            workspace = torch.empty(need, dtype=torch.uint8, device=dev)
+        ws_ptr, ws_bytes = workspace.data_ptr(), workspace.numel()
+    wws = None
+    if world > 1 and emulate:
+        wws = torch.empty(int(lib.rcp_worker_workspace_bytes(n, ctypes.byref(c))) * (world - 1),
+                          dtype=torch.uint8, device=dev)
     if out is None:
         out = DeviceFactorization(
             perm=torch.empty(n, dtype=torch.int64, device=dev),
@@ -353,12 +367,12 @@ def factor_device(a: torch.Tensor, cfg: FactorConfig | None = None, *, omega: to
         out.trace_kind = torch.empty(n, dtype=torch.int8, device=dev)
         out.trace_r = torch.empty(n, dtype=torch.int32, device=dev)
     st = _native.RcpStats()
-    status = lib.rcp_factor(
+    status = lib.rcp_factor_dist(
         ctypes.byref(c), n, a.data_ptr(), lda, omega.data_ptr(), normals.cfunc, None,
-        workspace.data_ptr(), workspace.numel(), out.perm.data_ptr(), out.L.data_ptr(),
+        ws_ptr, ws_bytes, out.perm.data_ptr(), out.L.data_ptr(),
         out.d_diag.data_ptr(), out.d_off.data_ptr(), out.pattern.data_ptr(),
         _ptr(out.trace_kind if trace else None), _ptr(out.trace_r if trace else None),
-        ctypes.byref(st), _stream())
+        ctypes.byref(st), int(world), 1 if emulate else 0, _ptr(wws), 0 if wws is None else wws.numel(), _stream())
     _raise_status(status, st)
     out.stats = {
         "rho_cheap": float(st.rho_cheap), "max_multiplier": float(st.max_multiplier),

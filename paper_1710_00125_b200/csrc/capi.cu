@@ -20,68 +20,26 @@
 #include "panel.cuh"
 #include "rcp_common.cuh"
 #include "solve.cuh"
+#include "layout.cuh"
+#include "dist.cuh"
 
 using namespace rcp;
 
 namespace {
 
-constexpr size_t kAlign = 256;
-
-size_t align_up(size_t x) { return (x + kAlign - 1) & ~(kAlign - 1); }
-
-struct Layout {
-  size_t A0, A1, Lbuf, W, Lneg, Wg, B0, B1, qscr, Y, L11, omega, phys, lop, pol, perm0, perm1, poso, snap, flags, xrec, qrec,
-      qcol, sdec, qdec, state, scal, desc, plog, total;
-  int64_t rows_pad, snap_cap;
-  int tpad;
-};
-
-Layout make_layout(int64_t n, const rcp_config& c) {
-  Layout L{};
+WorkerBufs carve_worker(unsigned char* b, int64_t n, const Layout& L) {
+  WorkerBufs w{};
   size_t off = 0;
   auto take = [&](size_t bytes) {
-    size_t o = off;
-    off = align_up(off + bytes);
-    return o;
+    unsigned char* p = b + off;
+    off += align_up(bytes);
+    return p;
   };
-  const size_t nn = (size_t)n * (size_t)n;
-  const int P = c.p;
-  L.tpad = ((c.b + 2 + 15) / 16) * 16;
-  L.rows_pad = ((n + 127) / 128) * 128;
-  int64_t per_panel_min = std::max<int64_t>(1, (int64_t)c.b - 1);
-  int64_t max_panels = n / per_panel_min + 2;
-  L.snap_cap = std::min<int64_t>(max_panels * n, n * (n + 1) / 2 + n);
-  L.A0 = take(nn * 8);
-  L.A1 = take(nn * 8);
-  L.Lbuf = take(nn * 8);
-  L.W = take((size_t)n * (c.b + 2) * 8);
-  L.Lneg = take((size_t)L.rows_pad * L.tpad * 8);
-  L.Wg = take((size_t)L.rows_pad * L.tpad * 8);
-  L.B0 = take((size_t)P * n * 8);
-  L.B1 = take((size_t)P * n * 8);
-  L.qscr = take((size_t)P * n * 8);
-  L.Y = take((size_t)P * L.tpad * 8);
-  L.L11 = take((size_t)L.tpad * L.tpad * 8);
-  L.omega = take((size_t)P * n * 8);
-  L.phys = take((size_t)n * 4);
-  L.lop = take((size_t)n * 4);
-  L.pol = take((size_t)n * 4);
-  L.perm0 = take((size_t)n * 4);
-  L.perm1 = take((size_t)n * 4);
-  L.poso = take((size_t)n * 4);
-  L.snap = take((size_t)L.snap_cap * 4);
-  L.flags = take(0);
-  L.xrec = take(8 * 2 * kMaxSMs * (size_t)kXWords);
-  L.qrec = take(8 * 2 * kMaxSMs * (size_t)kQWords);
-  L.qcol = take(8 * 2 * kMaxSMs * 2 * (size_t)P);
-  L.sdec = take(8 * 2 * (size_t)kXWords);
-  L.qdec = take(8 * 2 * (8 + 2 * (size_t)P));
-  L.state = take(sizeof(PanelState));
-  L.scal = take(64);
-  L.desc = take(2 * sizeof(PanelDesc));
-  L.plog = take((size_t)(n + 2) * sizeof(PanelLog));
-  L.total = off;
-  return L;
+  w.Lneg = reinterpret_cast<double*>(take((size_t)L.rows_pad * L.tpad * 8));
+  w.Wg = reinterpret_cast<double*>(take((size_t)L.rows_pad * L.tpad * 8));
+  w.phys = reinterpret_cast<int*>(take((size_t)n * 4));
+  w.dyn = reinterpret_cast<SchurDyn*>(take(sizeof(SchurDyn)));
+  return w;
 }
 
 int validate_cfg(const rcp_config* c, int64_t n) {
@@ -134,10 +92,25 @@ size_t rcp_workspace_bytes(int64_t n, const rcp_config* cfg) {
   return make_layout(n, *cfg).total;
 }
 
+size_t rcp_worker_workspace_bytes(int64_t n, const rcp_config* cfg) {
+  if (validate_cfg(cfg, n) != RCP_OK) return 0;
+  const Layout L = make_layout(n, *cfg);
+  return align_up((size_t)L.rows_pad * L.tpad * 8) * 2 + align_up((size_t)n * 4) + align_up(sizeof(SchurDyn)) + kAlign;
+}
+
 int rcp_factor(const rcp_config* cfg, int64_t n, const double* a, int64_t lda, const double* omega_dev,
                rcp_draw_fn draw, void* draw_ctx, void* workspace, size_t workspace_bytes, int64_t* perm,
                double* Lout, double* d_diag, double* d_off, int8_t* pattern, int8_t* trace_kind, int32_t* trace_r,
                rcp_stats* stats, void* cuda_stream) {
+  return rcp_factor_dist(cfg, n, a, lda, omega_dev, draw, draw_ctx, workspace, workspace_bytes, perm, Lout, d_diag,
+                         d_off, pattern, trace_kind, trace_r, stats, 1, 0, nullptr, 0, cuda_stream);
+}
+
+int rcp_factor_dist(const rcp_config* cfg, int64_t n, const double* a, int64_t lda, const double* omega_dev,
+                    rcp_draw_fn draw, void* draw_ctx, void* workspace, size_t workspace_bytes, int64_t* perm,
+                    double* Lout, double* d_diag, double* d_off, int8_t* pattern, int8_t* trace_kind,
+                    int32_t* trace_r, rcp_stats* stats, int world, int emulate, void* worker_ws,
+                    size_t worker_ws_bytes, void* cuda_stream) {
   if (stats) {
     memset(stats, 0, sizeof(*stats));
     stats->deficient_from = -1;
@@ -148,8 +121,32 @@ int rcp_factor(const rcp_config* cfg, int64_t n, const double* a, int64_t lda, c
   const rcp_config c = *cfg;
   const Layout Lay = make_layout(n, c);
   if (!workspace || workspace_bytes < Lay.total) return RCP_ERR_WORKSPACE;
+  if (world < 1 || world > kMaxWorld) return RCP_ERR_INVALID_ARG;
+  const size_t wslot = rcp_worker_workspace_bytes(n, cfg);
+  if (world > 1 && emulate && (!worker_ws || worker_ws_bytes < wslot * (size_t)(world - 1))) return RCP_ERR_WORKSPACE;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(cuda_stream);
   unsigned char* ws = reinterpret_cast<unsigned char*>(workspace);
+  DistShared* dsh = reinterpret_cast<DistShared*>(ws + Lay.dist);
+  unsigned long long dseq = 0;  // multi-GPU signal sequence
+  std::vector<WorkerBufs> vworkers;  // emulation: the other ranks' scratch on this device
+  if (world > 1 && emulate) {
+    for (int r = 1; r < world; ++r) {
+      unsigned char* b = reinterpret_cast<unsigned char*>(worker_ws) + wslot * (size_t)(r - 1);
+      vworkers.push_back(carve_worker(b, n, Lay));
+    }
+  }
+  // the workers must be released whatever happens (errors included)
+  struct DistFinish {
+    DistShared* sh;
+    cudaStream_t st;
+    int world;
+    ~DistFinish() {
+      if (world > 1) {
+        launch_dist_finish(sh, st);
+        cudaStreamSynchronize(st);
+      }
+    }
+  } dist_finish{dsh, st, world};
   auto dptr = [&](size_t off) { return reinterpret_cast<double*>(ws + off); };
   auto iptr = [&](size_t off) { return reinterpret_cast<int*>(ws + off); };
 
@@ -230,6 +227,7 @@ int rcp_factor(const rcp_config* cfg, int64_t n, const double* a, int64_t lda, c
   RCP_CHECK(cudaMemcpyAsync(dstate, &init, sizeof(init), cudaMemcpyHostToDevice, st));
   RCP_CHECK(cudaMemsetAsync(ws + Lay.xrec, 0, Lay.state - Lay.xrec, st));  // LL exchange buffers: no stale tags
   RCP_CHECK(cudaMemsetAsync(dscal, 0, sizeof(Scal), st));
+  if (world > 1 && emulate) RCP_CHECK(cudaMemsetAsync(dsh, 0, sizeof(DistShared), st));
   RCP_CHECK(cudaMemsetAsync(d_off, 0, sizeof(double) * n, st));
   if (trace_kind) RCP_CHECK(cudaMemsetAsync(trace_kind, -1, n, st));
   if (trace_r) RCP_CHECK(cudaMemsetAsync(trace_r, 0xff, sizeof(int32_t) * n, st));
@@ -351,8 +349,16 @@ int rcp_factor(const rcp_config* cfg, int64_t n, const double* a, int64_t lda, c
                                L11c, st, din));
       EventPair& es = new_pair(ev_schur);
       RCP_CHECK(cudaEventRecord(es.a, st));
-      RCP_LAUNCH(launch_schur_update(n, 0, 0, Lneg, Wg, tpad, 0, A[curA], phys, A[curA ^ 1], st, din));
+      if (world > 1) {  // hand the panel to the other devices (dist.cuh)
+        ++dseq;
+        RCP_LAUNCH(launch_dist_signal(dsh, dseq, curA, pidx & 1, st));
+        for (int r = 1; r < (int)vworkers.size() + 1; ++r)
+          RCP_LAUNCH(launch_worker_panel(dsh, r, world, dseq, A[0], A[1], ddesc, Lneg, Wg, phys, n, tpad,
+                                         vworkers[r - 1], st));
+      }
+      RCP_LAUNCH(launch_schur_update(n, 0, 0, Lneg, Wg, tpad, 0, A[curA], phys, A[curA ^ 1], st, din, 0, world));
       RCP_CHECK(cudaEventRecord(es.b, st));
+      if (world > 1) RCP_LAUNCH(launch_dist_wait_done(dsh, world, dseq, st));
       if (!q1) {  // sketch correction once per panel (factor.py:554-565)
         RCP_LAUNCH(launch_ysolve(n, P, 0, c.b, tpad, pol, B[curB], L11c, Y, st, din));
         RCP_LAUNCH(launch_sketch_correction(P, n, 0, Y, tpad, c.b, Lneg, B[curB], phys, B[curB ^ 1], st, din, n));
@@ -443,6 +449,15 @@ int rcp_factor(const rcp_config* cfg, int64_t n, const double* a, int64_t lda, c
     RCP_CHECK(cudaMemcpyAsync(&dstate->stop_pidx, &neg1, sizeof(int), cudaMemcpyHostToDevice, st));
     RCP_CHECK(cudaStreamSynchronize(st));  // neg1 / hdesc are host stack / pinned values
     batch = 1;
+  }
+  if (world > 1) {
+    int derr = 0;
+    RCP_CHECK(cudaMemcpyAsync(&derr, &dsh->error, sizeof(int), cudaMemcpyDeviceToHost, st));
+    RCP_CHECK(cudaStreamSynchronize(st));
+    if (derr) {
+      if (stats) snprintf(stats->message, sizeof(stats->message), "multi-GPU peer watchdog fired");
+      return RCP_ERR_CUDA;
+    }
   }
   if (stop_k0 >= 0) {
     RCP_LAUNCH(launch_deficient_fill(n, stop_k0, permb[pcur], perm, d_diag, d_off, pattern, st));
@@ -543,6 +558,70 @@ int rcp_factor(const rcp_config* cfg, int64_t n, const double* a, int64_t lda, c
   return RCP_OK;
 }
 
+
+int rcp_dist_prepare(int64_t n, const rcp_config* cfg, void* workspace, void* cuda_stream) {
+  if (validate_cfg(cfg, n) != RCP_OK || !workspace) return RCP_ERR_INVALID_ARG;
+  const Layout Lay = make_layout(n, *cfg);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(cuda_stream);
+  if (cudaMemsetAsync(reinterpret_cast<unsigned char*>(workspace) + Lay.dist, 0, sizeof(DistShared), st) != cudaSuccess)
+    return RCP_ERR_CUDA;
+  return cudaStreamSynchronize(st) == cudaSuccess ? RCP_OK : RCP_ERR_CUDA;
+}
+
+int rcp_schur_worker(const rcp_config* cfg, int64_t n, int rank, int world, void* rank0_workspace, void* worker_ws,
+                     size_t worker_ws_bytes, void* cuda_stream) {
+  if (validate_cfg(cfg, n) != RCP_OK || !rank0_workspace || rank < 1 || rank >= world || world > kMaxWorld)
+    return RCP_ERR_INVALID_ARG;
+  if (!worker_ws || worker_ws_bytes < rcp_worker_workspace_bytes(n, cfg)) return RCP_ERR_WORKSPACE;
+  const Layout Lay = make_layout(n, *cfg);
+  unsigned char* b0 = reinterpret_cast<unsigned char*>(rank0_workspace);
+  DistShared* sh = reinterpret_cast<DistShared*>(b0 + Lay.dist);
+  double* A0 = reinterpret_cast<double*>(b0 + Lay.A0);
+  double* A1 = reinterpret_cast<double*>(b0 + Lay.A1);
+  const PanelDesc* desc = reinterpret_cast<const PanelDesc*>(b0 + Lay.desc);
+  const double* Lneg0 = reinterpret_cast<const double*>(b0 + Lay.Lneg);
+  const double* Wg0 = reinterpret_cast<const double*>(b0 + Lay.Wg);
+  const int* phys0 = reinterpret_cast<const int*>(b0 + Lay.phys);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(cuda_stream);
+  const WorkerBufs wb = carve_worker(reinterpret_cast<unsigned char*>(worker_ws), n, Lay);
+  if (gemm_init_attributes() != cudaSuccess) return RCP_ERR_CUDA;
+  unsigned long long seq = 0;
+  SchurDyn hd{};
+  int hflags[2] = {0, 0};
+  for (int batch = 2;; batch = std::min(batch * 2, 16)) {
+    for (int i = 0; i < batch; ++i)
+      if (launch_worker_panel(sh, rank, world, ++seq, A0, A1, desc, Lneg0, Wg0, phys0, n, Lay.tpad, wb, st) !=
+          cudaSuccess)
+        return RCP_ERR_CUDA;
+    if (cudaMemcpyAsync(&hd, wb.dyn, sizeof(SchurDyn), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+        cudaMemcpyAsync(hflags, &sh->finished, 2 * sizeof(int), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+        cudaStreamSynchronize(st) != cudaSuccess)
+      return RCP_ERR_CUDA;
+    if (hflags[1]) return RCP_ERR_CUDA;  // watchdog
+    if (!hd.go) return RCP_OK;            // rank 0 finished
+  }
+}
+
+int rcp_device_alloc(size_t bytes, void** ptr) {
+  return cudaMalloc(ptr, bytes) == cudaSuccess ? RCP_OK : RCP_ERR_CUDA;
+}
+
+int rcp_device_free(void* ptr) { return cudaFree(ptr) == cudaSuccess ? RCP_OK : RCP_ERR_CUDA; }
+
+int rcp_ipc_export(const void* base, void* handle_out) {
+  cudaIpcMemHandle_t h;
+  if (cudaIpcGetMemHandle(&h, const_cast<void*>(base)) != cudaSuccess) return RCP_ERR_CUDA;
+  memcpy(handle_out, &h, sizeof(h));
+  return RCP_OK;
+}
+
+int rcp_ipc_import(const void* handle, void** ptr) {
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, sizeof(h));
+  return cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess) == cudaSuccess ? RCP_OK : RCP_ERR_CUDA;
+}
+
+int rcp_ipc_close(void* ptr) { return cudaIpcCloseMemHandle(ptr) == cudaSuccess ? RCP_OK : RCP_ERR_CUDA; }
 
 size_t rcp_solve_workspace_bytes(int64_t n, int64_t nrhs) {
   if (n < 1 || nrhs < 1) return 0;

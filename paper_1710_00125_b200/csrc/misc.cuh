@@ -6,6 +6,7 @@
 namespace rcp {
 
 struct PanelDesc;
+struct SchurDyn;
 
 cudaError_t launch_validate_copy(const double* a, int64_t lda, int64_t n, double* out, int* flags, double* amax,
                                  cudaStream_t st);
@@ -30,7 +31,10 @@ cudaError_t launch_iota(int64_t n, int* p, cudaStream_t st);
 // A_out[k+i, k+j] = A_in(phys[i], phys[j]) - sum_s L[i,s] W[j,s]   for i >= j (lower tiles)
 cudaError_t launch_schur_update(int64_t n, int64_t k, int64_t mp, const double* Lneg, const double* Wg, int tpad,
                                 int K, const double* A_in, const int* phys, double* A_out, cudaStream_t st,
-                                const PanelDesc* d = nullptr);
+                                const PanelDesc* d = nullptr, int part = 0, int nparts = 1);
+// multi-GPU worker: buffers / panel outcome resolved on the device (dist.cuh)
+cudaError_t launch_schur_update_dyn(int64_t n, const double* Lneg, const double* Wg, int tpad, const int* phys,
+                                    const SchurDyn* dyn, int part, int nparts, cudaStream_t st);
 // B[:, col0 + j] = sum_i Omega[r, i] * A[i, j]   (Omega row-major P x m, A col-major ld lda, full columns)
 cudaError_t launch_sketch_gemm(int P, int64_t m, const double* omega, int64_t ldo, const double* A, int64_t lda,
                                double* B, int64_t col0, cudaStream_t st);

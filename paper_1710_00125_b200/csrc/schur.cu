@@ -84,13 +84,13 @@ cudaError_t gemm_init_attributes() {
 
 cudaError_t launch_schur_update(int64_t n, int64_t k, int64_t mp, const double* Lneg, const double* Wg, int tpad,
                                 int K, const double* A_in, const int* phys, double* A_out, cudaStream_t st,
-                                const PanelDesc* d) {
+                                const PanelDesc* d, int part, int nparts) {
   if (d) {  // persistent grid; the kernel reads the panel outcome
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     schur_ws_kernel<<<(unsigned)sms, ws::kThreads, schur_ws_smem_bytes(), st>>>(Lneg, Wg, tpad, 0, A_in, A_out, phys,
-                                                                               n, 0, 0, 0, d);
+                                                                               n, 0, 0, 0, d, part, nparts, nullptr);
     return cudaGetLastError();
   }
   if (mp <= 0 || K <= 0) return cudaSuccess;
@@ -102,7 +102,17 @@ cudaError_t launch_schur_update(int64_t n, int64_t k, int64_t mp, const double* 
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const long long grid = std::min<long long>(tiles, sms);
   schur_ws_kernel<<<(unsigned)grid, ws::kThreads, schur_ws_smem_bytes(), st>>>(Lneg, Wg, tpad, Kl, A_in, A_out, phys,
-                                                                               n, k, mp, tiles, nullptr);
+                                                                               n, k, mp, tiles, nullptr, 0, 1, nullptr);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_schur_update_dyn(int64_t n, const double* Lneg, const double* Wg, int tpad, const int* phys,
+                                    const SchurDyn* dyn, int part, int nparts, cudaStream_t st) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  schur_ws_kernel<<<(unsigned)sms, ws::kThreads, schur_ws_smem_bytes(), st>>>(Lneg, Wg, tpad, 0, nullptr, nullptr, phys,
+                                                                             n, 0, 0, 0, nullptr, part, nparts, dyn);
   return cudaGetLastError();
 }
 

@@ -14,6 +14,7 @@
 // arrival), so the tensor pipe keeps issuing while the previous tile drains to HBM.
 #pragma once
 #include "panel.cuh"
+#include "dist.cuh"
 #include "gemm_dmma.cuh"
 
 namespace rcp {
@@ -100,8 +101,15 @@ RCP_D void tile_of(long long x, int64_t& m0, int64_t& n0) {
 __global__ void __launch_bounds__(ws::kThreads, 1)
 schur_ws_kernel(const double* __restrict__ Lneg, const double* __restrict__ Wg, int tpad, int Kl,
                 const double* __restrict__ ain, double* __restrict__ aout, const int* __restrict__ phys, int64_t n,
-                int64_t k, int64_t mp, long long tiles, const PanelDesc* __restrict__ d) {
+                int64_t k, int64_t mp, long long tiles, const PanelDesc* __restrict__ d, int part, int nparts,
+                const SchurDyn* __restrict__ dyn) {
   using namespace ws;
+  if (dyn) {  // multi-GPU worker: buffers resolved on the device from rank 0's signal
+    if (!dyn->go) return;
+    ain = dyn->ain;
+    aout = dyn->aout;
+    d = dyn->d;
+  }
   if (d) {  // device-driven: the panel outcome comes from the committed descriptor
     if (!d->ok || d->t <= 0 || d->k_end >= n) return;
     k = d->k_end;
@@ -114,6 +122,10 @@ schur_ws_kernel(const double* __restrict__ Lneg, const double* __restrict__ Wg, 
   Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int KT = Kl / kBK;
+  // tile sequence of this CTA: x0, x0 + xs, ...  (multi-GPU: tiles are dealt round robin to the
+  // nparts devices sharing the update, then to their CTAs)
+  const long long x0 = part + (long long)nparts * blockIdx.x;
+  const long long xs = (long long)nparts * gridDim.x;
   if (tid == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&sm.full[s], kProdThreads);
@@ -134,7 +146,7 @@ schur_ws_kernel(const double* __restrict__ Lneg, const double* __restrict__ Wg, 
     constexpr int MF = WM / 8, NF = 4;
     unsigned stage = 0, sphase = 0;
     int it = 0;
-    for (long long x = blockIdx.x; x < tiles; x += gridDim.x, ++it) {
+    for (long long x = x0; x < tiles; x += xs, ++it) {
       double acc[MF][NF][2];
 #pragma unroll
       for (int i = 0; i < MF; ++i)
@@ -187,7 +199,7 @@ schur_ws_kernel(const double* __restrict__ Lneg, const double* __restrict__ Wg, 
     const int pt = tid - 32 * kMmaWarps;  // 0..63
     const int srow = pt / 8, soff = (pt % 8) * 2;
     unsigned stage = 0, ephase = 1;  // fresh "empty" barriers count as released
-    for (long long x = blockIdx.x; x < tiles; x += gridDim.x) {
+    for (long long x = x0; x < tiles; x += xs) {
       int64_t m0, n0;
       tile_of(x, m0, n0);
       const double* ab = Lneg + (m0 + srow) * (int64_t)tpad + soff;
@@ -234,11 +246,10 @@ schur_ws_kernel(const double* __restrict__ Lneg, const double* __restrict__ Wg, 
       }
       mbar_arrive_cpasync(&sm.cin[b]);
     };
-    long long x0 = blockIdx.x;
     for (int b = 0; b < NBUF; ++b)
-      if (x0 + (long long)b * gridDim.x < tiles) gather(x0 + (long long)b * gridDim.x, b);
+      if (x0 + (long long)b * xs < tiles) gather(x0 + (long long)b * xs, b);
     int it = 0;
-    for (long long x = x0; x < tiles; x += gridDim.x, ++it) {
+    for (long long x = x0; x < tiles; x += xs, ++it) {
       const int b = it % NBUF;
       int64_t m0, n0;
       tile_of(x, m0, n0);
@@ -266,7 +277,7 @@ schur_ws_kernel(const double* __restrict__ Lneg, const double* __restrict__ Wg, 
         }
       }
       named_sync(1, kEpiThreads);  // every epilogue thread done reading buffer b
-      if (x + (long long)NBUF * gridDim.x < tiles) gather(x + (long long)NBUF * gridDim.x, b);
+      if (x + (long long)NBUF * xs < tiles) gather(x + (long long)NBUF * xs, b);
     }
   }
 }
