@@ -69,7 +69,11 @@ cudaError_t gemm_init_attributes() {
   e = cudaFuncSetAttribute(schur_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)schur_smem_bytes());
   if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(schur_ws_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)schur_ws_smem_bytes());
+  e = cudaFuncSetAttribute(schur_ws_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)schur_ws_smem_bytes());
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(schur_ws_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)schur_ws_smem_bytes());
   if (e != cudaSuccess) return e;
   e = cudaFuncSetAttribute(dmma_gemm_kernel<64, 128, kRectStages, 2, RectMap, SketchEpi>,
                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gemm_smem_bytes<64, 128, kRectStages>());
@@ -89,7 +93,11 @@ cudaError_t launch_schur_update(int64_t n, int64_t k, int64_t mp, const double* 
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    schur_ws_kernel<<<(unsigned)sms, ws::kThreads, schur_ws_smem_bytes(), st>>>(Lneg, Wg, tpad, 0, A_in, A_out, phys,
+    if (nparts > 1)
+      schur_ws_kernel<true><<<(unsigned)sms, ws::kThreads, schur_ws_smem_bytes(), st>>>(
+          Lneg, Wg, tpad, 0, A_in, A_out, phys, n, 0, 0, 0, d, part, nparts, nullptr);
+    else
+      schur_ws_kernel<false><<<(unsigned)sms, ws::kThreads, schur_ws_smem_bytes(), st>>>(Lneg, Wg, tpad, 0, A_in, A_out, phys,
                                                                                n, 0, 0, 0, d, part, nparts, nullptr);
     return cudaGetLastError();
   }
@@ -101,7 +109,7 @@ cudaError_t launch_schur_update(int64_t n, int64_t k, int64_t mp, const double* 
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const long long grid = std::min<long long>(tiles, sms);
-  schur_ws_kernel<<<(unsigned)grid, ws::kThreads, schur_ws_smem_bytes(), st>>>(Lneg, Wg, tpad, Kl, A_in, A_out, phys,
+  schur_ws_kernel<false><<<(unsigned)grid, ws::kThreads, schur_ws_smem_bytes(), st>>>(Lneg, Wg, tpad, Kl, A_in, A_out, phys,
                                                                                n, k, mp, tiles, nullptr, 0, 1, nullptr);
   return cudaGetLastError();
 }
@@ -111,7 +119,7 @@ cudaError_t launch_schur_update_dyn(int64_t n, const double* Lneg, const double*
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  schur_ws_kernel<<<(unsigned)sms, ws::kThreads, schur_ws_smem_bytes(), st>>>(Lneg, Wg, tpad, 0, nullptr, nullptr, phys,
+  schur_ws_kernel<true><<<(unsigned)sms, ws::kThreads, schur_ws_smem_bytes(), st>>>(Lneg, Wg, tpad, 0, nullptr, nullptr, phys,
                                                                              n, 0, 0, 0, nullptr, part, nparts, dyn);
   return cudaGetLastError();
 }

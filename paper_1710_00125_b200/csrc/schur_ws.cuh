@@ -98,13 +98,14 @@ RCP_D void tile_of(long long x, int64_t& m0, int64_t& n0) {
 
 }  // namespace ws
 
+template <bool kMulti>
 __global__ void __launch_bounds__(ws::kThreads, 1)
 schur_ws_kernel(const double* __restrict__ Lneg, const double* __restrict__ Wg, int tpad, int Kl,
                 const double* __restrict__ ain, double* __restrict__ aout, const int* __restrict__ phys, int64_t n,
                 int64_t k, int64_t mp, long long tiles, const PanelDesc* __restrict__ d, int part, int nparts,
                 const SchurDyn* __restrict__ dyn) {
   using namespace ws;
-  if (dyn) {  // multi-GPU worker: buffers resolved on the device from rank 0's signal
+  if (kMulti && dyn) {  // multi-GPU worker: buffers resolved on the device from rank 0's signal
     if (!dyn->go) return;
     ain = dyn->ain;
     aout = dyn->aout;
@@ -124,8 +125,8 @@ schur_ws_kernel(const double* __restrict__ Lneg, const double* __restrict__ Wg, 
   const int KT = Kl / kBK;
   // tile sequence of this CTA: x0, x0 + xs, ...  (multi-GPU: tiles are dealt round robin to the
   // nparts devices sharing the update, then to their CTAs)
-  const long long x0 = part + (long long)nparts * blockIdx.x;
-  const long long xs = (long long)nparts * gridDim.x;
+  const long long x0 = kMulti ? part + (long long)nparts * blockIdx.x : (long long)blockIdx.x;
+  const long long xs = kMulti ? (long long)nparts * gridDim.x : (long long)gridDim.x;
   if (tid == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&sm.full[s], kProdThreads);
