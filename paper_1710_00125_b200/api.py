@@ -277,9 +277,13 @@ class _NormalStream:
     def __init__(self, seed: int):
         self.gen = np.random.Generator(np.random.Philox(seed))
         self.draws = 0
+        self.pending_skip = None  # (p, n): Omega was supplied; discard its draw on first use
 
         def _cb(_ctx, rows, cols, out):
             try:
+                if self.pending_skip is not None:  # rare path (guard recompute): catch up first
+                    self.gen.standard_normal(self.pending_skip)
+                    self.pending_skip = None
                 z = self.gen.standard_normal((int(rows), int(cols)))
                 ctypes.memmove(out, z.ctypes.data, z.nbytes)
                 self.draws += 1
@@ -291,6 +295,10 @@ class _NormalStream:
 
     def first(self, p: int, n: int) -> np.ndarray:
         return self.gen.standard_normal((p, n))
+
+    def skip_first(self, p: int, n: int) -> None:
+        """Omega was drawn elsewhere: advance past it lazily (only a recompute needs it)."""
+        self.pending_skip = (p, n)
 
 
 def _config(cfg: FactorConfig | None, overrides: dict) -> FactorConfig:
@@ -338,7 +346,7 @@ def factor_device(a: torch.Tensor, cfg: FactorConfig | None = None, *, omega: to
     if omega is None:
         omega = torch.from_numpy(normals.first(cfg.p, n)).to(dev)
     else:
-        normals.first(cfg.p, n)  # advance the stream past the supplied first draw
+        normals.skip_first(cfg.p, n)  # advance past the supplied first draw when needed
         omega = omega.contiguous()
     c = _native.RcpConfig(cfg.p, cfg.b, cfg.q, cfg.robust_r)
     need = int(lib.rcp_workspace_bytes(n, ctypes.byref(c)))

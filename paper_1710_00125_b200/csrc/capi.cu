@@ -27,6 +27,63 @@ using namespace rcp;
 
 namespace {
 
+struct Scal {  // scalar results block (device)
+  double amax, beta, dmax, maxmult;
+  int vflags[2];
+};
+
+struct HostCache {
+  int dev = -1;
+  bool ok = false;
+  PanelState* hstate = nullptr;
+  PanelState* hsnap = nullptr;  // 2 slots
+  Scal* hscal = nullptr;
+  PanelDesc* hdesc = nullptr;   // 2 slots x 2 descriptors
+  cudaEvent_t bev[2] = {nullptr, nullptr};
+  std::vector<cudaEvent_t> pool;
+  size_t used = 0;
+  void reset() { used = 0; }
+  cudaEvent_t event() {
+    if (used == pool.size()) {
+      cudaEvent_t e = nullptr;
+      cudaEventCreate(&e);
+      pool.push_back(e);
+    }
+    return pool[used++];
+  }
+  void release() {
+    for (cudaEvent_t e : pool) cudaEventDestroy(e);
+    pool.clear();
+    used = 0;
+    for (int i = 0; i < 2; ++i)
+      if (bev[i]) cudaEventDestroy(bev[i]);
+    if (hstate) cudaFreeHost(hstate);
+    if (hsnap) cudaFreeHost(hsnap);
+    if (hscal) cudaFreeHost(hscal);
+    if (hdesc) cudaFreeHost(hdesc);
+    hstate = hsnap = nullptr;
+    hscal = nullptr;
+    hdesc = nullptr;
+    bev[0] = bev[1] = nullptr;
+    ok = false;
+  }
+  ~HostCache() {}  // process teardown: leave the driver to reclaim (the context may be gone)
+};
+
+HostCache& host_cache(int dev) {
+  thread_local HostCache hc;
+  if (hc.ok && hc.dev == dev) return hc;
+  if (hc.ok) hc.release();
+  hc.dev = dev;
+  hc.ok = cudaMallocHost(&hc.hstate, sizeof(PanelState)) == cudaSuccess &&
+          cudaMallocHost(&hc.hsnap, 2 * sizeof(PanelState)) == cudaSuccess &&
+          cudaMallocHost(&hc.hscal, sizeof(Scal)) == cudaSuccess &&
+          cudaMallocHost(&hc.hdesc, 4 * sizeof(PanelDesc)) == cudaSuccess &&
+          cudaEventCreateWithFlags(&hc.bev[0], cudaEventDisableTiming) == cudaSuccess &&
+          cudaEventCreateWithFlags(&hc.bev[1], cudaEventDisableTiming) == cudaSuccess;
+  return hc;
+}
+
 WorkerBufs carve_worker(unsigned char* b, int64_t n, const Layout& L) {
   WorkerBufs w{};
   size_t off = 0;
@@ -51,10 +108,6 @@ int validate_cfg(const rcp_config* c, int64_t n) {
   return RCP_OK;
 }
 
-struct Scal {  // scalar results block (device)
-  double amax, beta, dmax, maxmult;
-  int vflags[2];
-};
 
 #define RCP_CHECK(expr)                                                                           \
   do {                                                                                            \
@@ -179,40 +232,20 @@ int rcp_factor_dist(const rcp_config* cfg, int64_t n, const double* a, int64_t l
   RCP_CHECK(gemm_init_attributes());
   const int smem_budget = max_optin - panel_static_smem_bytes() - 1024;
 
-  PanelState* hstate = nullptr;
-  Scal* hscal = nullptr;
-  RCP_CHECK(cudaMallocHost(&hstate, sizeof(PanelState)));
-  RCP_CHECK(cudaMallocHost(&hscal, sizeof(Scal)));
-  struct HostFree {
-    PanelState* s;
-    Scal* c;
-    ~HostFree() {
-      cudaFreeHost(s);
-      cudaFreeHost(c);
-    }
-  } host_free{hstate, hscal};
-
-  cudaEvent_t ev_start, ev_stop;
-  RCP_CHECK(cudaEventCreate(&ev_start));
-  RCP_CHECK(cudaEventCreate(&ev_stop));
+  // pinned snapshots and CUDA events come from a per-thread cache (cudaMallocHost /
+  // cudaFreeHost and event creation per call cost milliseconds of GPU idle time)
+  HostCache& hc = host_cache(dev);
+  if (!hc.ok) {
+    if (stats) snprintf(stats->message, sizeof(stats->message), "pinned host cache allocation failed");
+    return RCP_ERR_CUDA;
+  }
+  hc.reset();
+  PanelState* hstate = hc.hstate;
+  Scal* hscal = hc.hscal;
+  cudaEvent_t ev_start = hc.event(), ev_stop = hc.event();
   std::vector<EventPair> ev_panel, ev_schur;
-  struct EvFree {
-    cudaEvent_t* a;
-    cudaEvent_t* b;
-    std::vector<EventPair>* p;
-    std::vector<EventPair>* s;
-    ~EvFree() {
-      cudaEventDestroy(*a);
-      cudaEventDestroy(*b);
-      for (auto& e : *p) { cudaEventDestroy(e.a); cudaEventDestroy(e.b); }
-      for (auto& e : *s) { cudaEventDestroy(e.a); cudaEventDestroy(e.b); }
-    }
-  } ev_free{&ev_start, &ev_stop, &ev_panel, &ev_schur};
   auto new_pair = [&](std::vector<EventPair>& v) -> EventPair& {
-    EventPair e;
-    cudaEventCreate(&e.a);
-    cudaEventCreate(&e.b);
-    v.push_back(e);
+    v.push_back(EventPair{hc.event(), hc.event()});
     return v.back();
   };
 
@@ -275,15 +308,13 @@ int rcp_factor_dist(const rcp_config* cfg, int64_t n, const double* a, int64_t l
   // chain, the host rolls back to that panel and handles them.
   const bool q1 = (c.q == 1);
   const int sms_cap = std::min(num_sms, kMaxSMs);
-  const int gmax = panel_geometry(n, (int)k, c.b, c.q, P, sms_cap, smem_budget).G;
+  // launch grid: the largest G any panel can ask for (G(m0) is not monotone in m0); CTAs
+  // beyond a panel's own G return at once
+  const int gmax = sms_cap;
   PanelDesc* ddesc = reinterpret_cast<PanelDesc*>(ws + Lay.desc);
   PanelLog* dplog = reinterpret_cast<PanelLog*>(ws + Lay.plog);
-  PanelDesc* hdesc = nullptr;
-  RCP_CHECK(cudaMallocHost(&hdesc, 2 * sizeof(PanelDesc)));
-  struct DescFree {
-    PanelDesc* d;
-    ~DescFree() { cudaFreeHost(d); }
-  } desc_free{hdesc};
+  PanelDesc* hdesc = hc.hdesc;  // [slot][2]: double-buffered chain snapshots
+  PanelState* hsnap = hc.hsnap;  // [slot]
   struct Hist {
     int curA, curB, pcur;
   };
@@ -300,6 +331,8 @@ int rcp_factor_dist(const rcp_config* cfg, int64_t n, const double* a, int64_t l
   }
   int batch = 2;
   constexpr int kBatchMax = 16;
+  int nbatch = 0;                // batches enqueued since the last fix-up
+  int batch_end[2] = {0, 0};     // pidx after each snapshot slot's batch
   PanelParams base{};
   base.n = n;
   base.P = P;
@@ -370,14 +403,35 @@ int rcp_factor_dist(const rcp_config* cfg, int64_t n, const double* a, int64_t l
       ++pidx;
       guard_req = armed ? 1 : 0;  // a stop check (2) applies to a relaunched panel only
     }
-    RCP_CHECK(cudaMemcpyAsync(hstate, dstate, sizeof(PanelState), cudaMemcpyDeviceToHost, st));
-    RCP_CHECK(cudaMemcpyAsync(hdesc, ddesc, 2 * sizeof(PanelDesc), cudaMemcpyDeviceToHost, st));
-    RCP_CHECK(cudaStreamSynchronize(st));
+    // snapshot the chain after this batch, then inspect the PREVIOUS batch's snapshot: the
+    // device always has one batch queued while the host waits
+    {
+      const int slot = nbatch & 1;
+      RCP_CHECK(cudaMemcpyAsync(hsnap + slot, dstate, sizeof(PanelState), cudaMemcpyDeviceToHost, st));
+      RCP_CHECK(cudaMemcpyAsync(hdesc + 2 * slot, ddesc, 2 * sizeof(PanelDesc), cudaMemcpyDeviceToHost, st));
+      RCP_CHECK(cudaEventRecord(hc.bev[slot], st));
+      batch_end[slot] = pidx;
+      ++nbatch;
+    }
     batch = std::min(batch * 2, kBatchMax);
-    if (hstate->status == 0 && hstate->err == LLONG_MAX) {
-      if (!hdesc[pidx & 1].run) chain_done = true;  // the next descriptor ends the chain: k == n
+    int chk;  // snapshot slot to inspect
+    if (nbatch == 1) {  // first batch: nothing older to look at yet
       continue;
     }
+    chk = (nbatch - 2) & 1;
+    RCP_CHECK(cudaEventSynchronize(hc.bev[chk]));
+    *hstate = hsnap[chk];
+    if (hstate->status == 0 && hstate->err == LLONG_MAX) {
+      // the descriptor after that batch's last panel decides whether the chain went on
+      if (!hdesc[2 * chk + (batch_end[chk] & 1)].run) {
+        chain_done = true;  // k == n; the newer batch is all no-ops
+        RCP_CHECK(cudaStreamSynchronize(st));
+      }
+      continue;
+    }
+    RCP_CHECK(cudaStreamSynchronize(st));  // drain the newer (no-op) batch before any fix-up
+    hdesc[0] = hdesc[2 * chk];
+    hdesc[1] = hdesc[2 * chk + 1];
     // a guard event or an error at panel tp: later panels were no-ops; roll back to tp
     const int tp = hstate->stop_pidx;
     if (tp < 0 || tp >= (int)hist.size()) {
@@ -449,6 +503,7 @@ int rcp_factor_dist(const rcp_config* cfg, int64_t n, const double* a, int64_t l
     RCP_CHECK(cudaMemcpyAsync(&dstate->stop_pidx, &neg1, sizeof(int), cudaMemcpyHostToDevice, st));
     RCP_CHECK(cudaStreamSynchronize(st));  // neg1 / hdesc are host stack / pinned values
     batch = 1;
+    nbatch = 0;
   }
   if (world > 1) {
     int derr = 0;

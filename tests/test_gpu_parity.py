@@ -198,3 +198,22 @@ def test_q1_guard_detects_zero_tail(cuda_ok):
     den = float(np.abs(a).max())
     rec = f.L @ f.D.to_dense() @ f.L.T
     assert float(np.abs(rec - a[np.ix_(f.perm, f.perm)]).max()) / den <= 1e-12
+
+
+def test_large_panel_grid_reconstructs(cuda_ok):
+    """n > 32 x #SMs: the panel CTA count G(m0) is capped by the SM count and is not monotone
+    in m0 (regression: the launch grid must cover the largest G of every panel)."""
+    import torch
+
+    from paper_1710_00125_b200 import api, gallery
+    n = 6144
+    a = torch.from_numpy(gallery.type6(n, 3)).cuda()
+    f = api.factor_device(a, api.FactorConfig(strategy="rcp", b=64, q=64, p=80, seed=1))
+    rec = api.reconstruct_device(f)
+    perm = f.perm
+    err = float((rec - a[perm][:, perm]).abs().max()) / float(a.abs().max())
+    assert err <= 1e-11
+    x, sing = api.solve_device(f, torch.ones(n, dtype=torch.float64, device="cuda"))
+    assert not sing
+    r = float((a @ x - 1.0).abs().max()) / (float(a.abs().sum(dim=1).max()) * float(x.abs().max()))
+    assert r <= 1e-13
