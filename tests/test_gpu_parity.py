@@ -217,3 +217,19 @@ def test_large_panel_grid_reconstructs(cuda_ok):
     assert not sing
     r = float((a @ x - 1.0).abs().max()) / (float(a.abs().sum(dim=1).max()) * float(x.abs().max()))
     assert r <= 1e-13
+
+
+def test_supplied_omega_with_guard_recompute(cuda_ok):
+    """Omega passed in (its draw is skipped lazily): a guard recompute must still continue the
+    same normal stream (g_c5_scaled recomputes once)."""
+    import torch
+
+    from paper_1710_00125_b200 import api
+    g = load_golden("g_c5_scaled")
+    cfg = api.FactorConfig(**g["cfg"])
+    n = g["a"].shape[0]
+    om = np.random.Generator(np.random.Philox(cfg.seed)).standard_normal((cfg.p, n))
+    a = torch.from_numpy(g["a"]).cuda()
+    f = api.factor_device(a, cfg, omega=torch.from_numpy(om).cuda())
+    assert f.stats["recompute_count"] == int(g["recompute_count"]) == 1
+    assert np.array_equal(f.perm.cpu().numpy(), g["perm"])
