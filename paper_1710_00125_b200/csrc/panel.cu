@@ -31,6 +31,9 @@ constexpr int kPanelThreads = 256;
 constexpr int kWarps = kPanelThreads / 32;
 constexpr int kRegRows = 32;  // QRCP register mode: sketch rows [0, 32) of each column live in registers
 constexpr long long kWatchdogCycles = 8000000000LL;
+#ifndef RCP_SBKP_SHARED
+#define RCP_SBKP_SHARED 0  // 1: SBKP decision on one shared line polled by every CTA (A/B switch)
+#endif
 
 struct BlockBest {
   double key;
@@ -49,32 +52,37 @@ RCP_D void argmax_step(double& key, long long& idx, int& slot, int off) {
   }
 }
 
-// Block-wide argmax (numpy first-index semantics), broadcast to all threads; two
-// barriers.  `parity` alternates between consecutive calls (double-buffered result).
+// Block-wide argmax (numpy first-index semantics), broadcast to all threads; one barrier:
+// warps reduce by shuffles, then every thread reduces the kWarps warp results itself (`better`
+// is a strict total order, so every thread gets the same answer).  `parity` alternates between
+// consecutive calls (the per-warp slots are double-buffered).
 __device__ BlockBest block_argmax(double key, long long idx, int slot, int parity) {
-  __shared__ double sk[kWarps];
-  __shared__ long long si[kWarps];
-  __shared__ int ss[kWarps];
-  __shared__ BlockBest res[2];
+  __shared__ double sk[2][kWarps];
+  __shared__ long long si[2][kWarps];
+  __shared__ int ss[2][kWarps];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) argmax_step(key, idx, slot, off);
   if (lane == 0) {
-    sk[warp] = key;
-    si[warp] = idx;
-    ss[warp] = slot;
+    sk[parity][warp] = key;
+    si[parity][warp] = idx;
+    ss[parity][warp] = slot;
   }
   __syncthreads();
-  if (warp == 0) {
-    key = lane < kWarps ? sk[lane] : -1.0;
-    idx = lane < kWarps ? si[lane] : LLONG_MAX;
-    slot = lane < kWarps ? ss[lane] : -1;
+  double wk[kWarps];
+  long long wi[kWarps];
+  int wsl[kWarps];
 #pragma unroll
-    for (int off = 16; off > 0; off >>= 1) argmax_step(key, idx, slot, off);
-    if (lane == 0) res[parity] = BlockBest{key, idx, slot};
+  for (int w = 0; w < kWarps; ++w) {
+    wk[w] = sk[parity][w];
+    wi[w] = si[parity][w];
+    wsl[w] = ss[parity][w];
   }
-  __syncthreads();
-  return res[parity];
+  BlockBest r{wk[0], wi[0], wsl[0]};
+#pragma unroll
+  for (int w = 1; w < kWarps; ++w)
+    if (better(wk[w], wi[w], r.key, r.idx)) r = BlockBest{wk[w], wi[w], wsl[w]};
+  return r;
 }
 
 // Deterministic sum of squares over vals[lo, hi) by warp 0 (lane-strided partials + fixed
@@ -196,7 +204,7 @@ __global__ void __launch_bounds__(kPanelThreads, 1) panel_kernel(PanelParams pin
   double* wnext = reinterpret_cast<double*>(carve(sizeof(double) * Wn));
   unsigned char* region = sp;  // QRCP and SBKP phases reuse the rest
 
-  __shared__ int s_abort, s_gerr, s_lerr, s_skip, s_moved, s_wcol;
+  __shared__ int s_abort, s_gerr, s_lerr, s_skip, s_wcol;
   __shared__ double s_coef, s_gakk, s_akk;
   __shared__ XRec s_win;
   __shared__ unsigned s_qhdr[8], s_dhdr[12];
@@ -337,60 +345,59 @@ __global__ void __launch_bounds__(kPanelThreads, 1) panel_kernel(PanelParams pin
       // ---- speculative Householder vector of this CTA's candidate (sketch.py:159-168):
       //      only the global winner's v is used, so every CTA prepares its own and the
       //      reducer broadcasts just a small header.
-      if (lb.slot >= 0) {
-        if (regmode) {
-          if (tid == lb.slot) {
+      {
+        // Built by the warp holding the candidate column (warp 0 in generic mode), no CTA barrier.
+        const int lane = tid & 31;
+        const int hwarp = lb.slot < 0 ? -1 : (regmode ? (lb.slot >> 5) : 0);
+        if ((tid >> 5) == hwarp) {
+          if (regmode && lane == (lb.slot & 31)) {
 #pragma unroll
             for (int r = 0; r < kRegRows; ++r)
               if (r >= j && r < PRr) vvec[r] = rg[r];
           }
-          for (int r = max(j, PRr) + tid; r < P; r += nthr) vvec[r] = Bs[(r - PRr) * Rs + lb.slot];
-        } else {
-          for (int r = j + tid; r < P; r += nthr) vvec[r] = bsm(r, lb.slot);
-        }
-      }
-      __syncthreads();
-      if (lb.slot >= 0 && tid < 32) {
-        double xn = sqrt(warp0_sum_sq(vvec, j, P));
-        xn = __shfl_sync(0xffffffffu, xn, 0);
-        if (xn == 0.0) {
-          if (tid == 0) {
-            s_skip = 1;
-            s_coef = 0.0;
-          }
-        } else {
-          if (tid == 0) {
-            const double x0 = vvec[j];
-            vvec[j] = __dadd_rn(x0, copysign(xn, x0 != 0.0 ? x0 : 1.0));
-          }
+          for (int r = max(j, PRr) + lane; r < P; r += 32)
+            vvec[r] = regmode ? Bs[(r - PRr) * Rs + lb.slot] : bsm(r, lb.slot);
           __syncwarp();
-          const double vn2 = warp0_sum_sq(vvec, j, P);
-          if (tid == 0) {
-            s_skip = (vn2 == 0.0) ? 1 : 0;
-            s_coef = (vn2 == 0.0) ? 0.0 : 2.0 / vn2;
+          const double xn = __shfl_sync(0xffffffffu, sqrt(warp0_sum_sq(vvec, j, P)), 0);
+          double coef = 0.0;
+          unsigned skip = 1;
+          if (xn != 0.0) {
+            if (lane == 0) {
+              const double x0 = vvec[j];
+              vvec[j] = __dadd_rn(x0, copysign(xn, x0 != 0.0 ? x0 : 1.0));
+            }
+            __syncwarp();
+            const double vn2 = __shfl_sync(0xffffffffu, warp0_sum_sq(vvec, j, P), 0);
+            skip = (vn2 == 0.0) ? 1u : 0u;
+            coef = (vn2 == 0.0) ? 0.0 : 2.0 / vn2;
+          }
+          u64* dst = p.qcll + ((size_t)pb * G + cta) * 2 * P;
+          for (int r = j + lane; r < P; r += 32) ll_put_d(dst + 2 * r, tag, vvec[r]);
+          if (lane == 0) {
+            u64* q = p.qll + ((size_t)pb * G + cta) * kQWords;
+            ll_put_d(q, tag, lb.key);
+            ll_put(q + 2, tag, static_cast<unsigned>(lb.idx));
+            ll_put(q + 3, tag, static_cast<unsigned>(r0 + lb.slot));
+            ll_put_d(q + 4, tag, coef);
+            ll_put(q + 6, tag, skip);
           }
         }
-      }
-      __syncthreads();
-      if (lb.slot >= 0) {
-        u64* dst = p.qcll + ((size_t)pb * G + cta) * 2 * P;
-        for (int r = j + tid; r < P; r += nthr) ll_put_d(dst + 2 * r, tag, vvec[r]);
-      }
-      if (tid == 0) {
-        u64* q = p.qll + ((size_t)pb * G + cta) * kQWords;
-        const bool has = lb.slot >= 0;
-        ll_put_d(q, tag, has ? lb.key : -1.0);
-        ll_put(q + 2, tag, has ? static_cast<unsigned>(lb.idx) : 0x7fffffffu);
-        ll_put(q + 3, tag, has ? static_cast<unsigned>(r0 + lb.slot) : 0xffffffffu);
-        ll_put_d(q + 4, tag, has ? s_coef : 0.0);
-        ll_put(q + 6, tag, has ? static_cast<unsigned>(s_skip) : 1u);
+        if (lb.slot < 0 && tid == 0) {
+          u64* q = p.qll + ((size_t)pb * G + cta) * kQWords;
+          ll_put_d(q, tag, -1.0);
+          ll_put(q + 2, tag, 0x7fffffffu);
+          ll_put(q + 3, tag, 0xffffffffu);
+          ll_put_d(q + 4, tag, 0.0);
+          ll_put(q + 6, tag, 1u);
+        }
       }
       seq = nseq;
+      __syncthreads();  // records out before anyone polls (measured: avoids a delayed store)
       PROF_END(9);
       PROF_BEGIN();
-      // ---- reducer CTA 0: winner over all records -> small LL header (winner CTA, position,
-      //      column, norm, coef, skip); every CTA then reads v from the winner's buffer.
-      u64* dec = p.qdll + (size_t)pb * 8;
+      // ---- reducer CTA 0: winner over all records -> a 6-word decision pushed into every CTA's
+      //      mailbox (winner CTA, position, column, coef, flags); every CTA then reads v from
+      //      the winner's buffer.
       if (cta == 0) {
         double gk = -1.0;
         long long gi = LLONG_MAX;
@@ -415,27 +422,35 @@ __global__ void __launch_bounds__(kPanelThreads, 1) panel_kernel(PanelParams pin
         BlockBest gb = block_argmax(gk, gi, gs, par);
         if (gs >= 0 && gs == gb.slot) {  // the thread that loaded the winning record
           const bool gstop = (j == 0 && p.guard_mode != 0 && gb.key < p.guard_limit);
-          s_wcta = gs;
-          s_wpos = static_cast<int>(gw[2]);
-          s_wcol = static_cast<int>(gw[3]);
-          s_coef = ll_d(gw[4], gw[5]);
-          s_skip = static_cast<int>(gw[6]);
-          s_qflags = (gw[6] ? 1 : 0) | (gstop ? 2 : 0) | (s_abort ? 4 : 0);
-          ll_put(dec + 0, tag, static_cast<unsigned>(gs));
-          ll_put(dec + 1, tag, gw[2]);
-          ll_put(dec + 2, tag, gw[3]);
-          ll_put(dec + 3, tag, gw[4]);
-          ll_put(dec + 4, tag, gw[5]);
-          ll_put(dec + 5, tag, static_cast<unsigned>(s_qflags));
+          s_qhdr[0] = static_cast<unsigned>(gs);
+          s_qhdr[1] = gw[2];
+          s_qhdr[2] = gw[3];
+          s_qhdr[3] = gw[4];
+          s_qhdr[4] = gw[5];
+          s_qhdr[5] = (gw[6] ? 1u : 0u) | (gstop ? 2u : 0u);
         }
-        if (s_abort && tid == 0) {
-          s_qflags = 4;
-          ll_put(dec + 5, tag, 4u);
+        if (gb.slot < 0 && tid == 0) s_qhdr[5] = 4u;  // no candidate anywhere: cannot happen
+        __syncthreads();
+        unsigned hw[6];
+#pragma unroll
+        for (int u = 0; u < 6; ++u) hw[u] = s_qhdr[u];
+        if (s_abort) hw[5] = 4u;
+        for (int f = tid; f < G * 6; f += nthr) {
+          const int c = f / 6, u = f - c * 6;
+          if (c != 0) ll_put(p.qdll + ((size_t)pb * G + c) * kMWords + u, tag, hw[u]);
+        }
+        if (tid == 0) {
+          s_wcta = static_cast<int>(hw[0]);
+          s_wpos = static_cast<int>(hw[1]);
+          s_wcol = static_cast<int>(hw[2]);
+          s_coef = ll_d(hw[3], hw[4]);
+          s_qflags = static_cast<int>(hw[5]);
+          s_skip = hw[5] & 1;
         }
       } else {
         if (tid < 6) {
           unsigned w[1];
-          if (!ll_read<1>(dec + tid, tag, w)) {
+          if (!ll_read<1>(p.qdll + ((size_t)pb * G + cta) * kMWords + tid, tag, w)) {
             s_abort = 1;
             w[0] = 0;
           }
@@ -454,6 +469,11 @@ __global__ void __launch_bounds__(kPanelThreads, 1) panel_kernel(PanelParams pin
       }
       par ^= 1;
       __syncthreads();
+      const int wpos = s_wpos;
+      const int wcol = s_wcol;
+      // replay bookkeeping (factor.py:586-599), position j <-> wpos: every thread reads the
+      // displaced column now; thread 0 rewrites `win` after the next barrier
+      const int moved = (wpos != j) ? win[j] : -1;
       if (!(s_qflags & 6)) {  // fetch the winner's Householder vector
         const u64* src = p.qcll + ((size_t)pb * G + s_wcta) * 2 * P;
         for (int r = j + tid; r < P; r += nthr) {
@@ -475,34 +495,22 @@ __global__ void __launch_bounds__(kPanelThreads, 1) panel_kernel(PanelParams pin
         s_abort = 2;
         break;
       }
-      const int wpos = s_wpos;
-      const int wcol = s_wcol;
-      // ---- replay bookkeeping (factor.py:586-599): position j <-> wpos
-      if (tid == 0) {
-        int moved = -1;
-        if (wpos != j) {
-          moved = win[j];
-          win[j] = wcol;
-          if (wpos < Wn) win[wpos] = moved;
-        }
-        s_moved = moved;
+      if (tid == 0 && moved >= 0) {
+        win[j] = wcol;
+        if (wpos < Wn) win[wpos] = moved;
       }
-      __syncthreads();
-      {
-        const int moved = s_moved;
-        if (regmode) {
-          if (own && r0 + tid == wcol) {
-            mypos = j;
-            mysel = true;
-          }
-          if (own && moved >= 0 && r0 + tid == moved) mypos = wpos;
-        } else if (tid == 0) {
-          if (wcol >= r0 && wcol < r0 + rcnt) {
-            lpos[wcol - r0] = j;
-            qsel[wcol - r0] = 1;
-          }
-          if (moved >= 0 && moved >= r0 && moved < r0 + rcnt) lpos[moved - r0] = wpos;
+      if (regmode) {
+        if (own && r0 + tid == wcol) {
+          mypos = j;
+          mysel = true;
         }
+        if (own && moved >= 0 && r0 + tid == moved) mypos = wpos;
+      } else if (tid == 0) {
+        if (wcol >= r0 && wcol < r0 + rcnt) {
+          lpos[wcol - r0] = j;
+          qsel[wcol - r0] = 1;
+        }
+        if (moved >= 0 && moved >= r0 && moved < r0 + rcnt) lpos[moved - r0] = wpos;
       }
       // ---- reflect the remaining columns and refresh their residual norms
       PROF_END(10);
@@ -714,7 +722,7 @@ __global__ void __launch_bounds__(kPanelThreads, 1) panel_kernel(PanelParams pin
           ll_put(q + 3, tag1, has ? static_cast<unsigned>(r0 + lb1.slot) : 0xffffffffu);
         }
         seq = nseq1;
-        u64* dec1 = p.qdll + (size_t)pb1 * 8;
+        __syncthreads();  // records out before anyone polls
         if (cta == 0) {
           double gk = -1.0;
           long long gi = LLONG_MAX;
@@ -744,19 +752,31 @@ __global__ void __launch_bounds__(kPanelThreads, 1) panel_kernel(PanelParams pin
               else if (t > 0) fl = 8;                        // defer
               else fl = 1;                                   // trip: recompute
             }
-            s_qflags = fl | (s_abort ? 4u : 0u);
-            s_wpos = static_cast<int>(gb.idx);
-            s_wcol = gph;
-            s_gs1 = gs;
-            ll_put(dec1 + 0, tag1, static_cast<unsigned>(gs));
-            ll_put(dec1 + 1, tag1, static_cast<unsigned>(s_wpos));
-            ll_put(dec1 + 2, tag1, static_cast<unsigned>(gph));
-            ll_put(dec1 + 3, tag1, static_cast<unsigned>(s_qflags));
+            s_qhdr[0] = static_cast<unsigned>(gs);
+            s_qhdr[1] = static_cast<unsigned>(gb.idx);
+            s_qhdr[2] = static_cast<unsigned>(gph);
+            s_qhdr[3] = fl;
+          }
+          if (gb.slot < 0 && tid == 0) s_qhdr[3] = 4u;
+          __syncthreads();
+          unsigned hw[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) hw[u] = s_qhdr[u];
+          if (s_abort) hw[3] |= 4u;
+          for (int f = tid; f < G * 4; f += nthr) {
+            const int c = f >> 2, u = f & 3;
+            if (c != 0) ll_put(p.qdll + ((size_t)pb1 * G + c) * kMWords + u, tag1, hw[u]);
+          }
+          if (tid == 0) {
+            s_gs1 = static_cast<int>(hw[0]);
+            s_wpos = static_cast<int>(hw[1]);
+            s_wcol = static_cast<int>(hw[2]);
+            s_qflags = static_cast<int>(hw[3]);
           }
         } else {
           if (tid < 4) {
             unsigned w[1];
-            if (!ll_read<1>(dec1 + tid, tag1, w)) {
+            if (!ll_read<1>(p.qdll + ((size_t)pb1 * G + cta) * kMWords + tid, tag1, w)) {
               s_abort = 1;
               w[0] = 4;
             }
@@ -862,11 +882,12 @@ __global__ void __launch_bounds__(kPanelThreads, 1) panel_kernel(PanelParams pin
       ll_put(q + 10, tag, ((pk >= r0 && pk < r0 + rcnt) ? 1u : 0u) | (s_lerr ? 2u : 0u));
     }
     seq = nseq;
+    __syncthreads();  // record out before anyone polls
     PROF_END(8);
     PROF_BEGIN();
 
-    // ---- reducer CTA 0 reads all records and broadcasts the decision inputs (one LL record)
-    u64* dec = p.sdll + (size_t)pb * kXWords;
+    // ---- reducer CTA 0 reads all records and pushes the decision inputs (12 LL words) into
+    //      every CTA's mailbox
     if (cta == 0) {
       double gk = -1.0;
       long long gi = LLONG_MAX;
@@ -901,17 +922,34 @@ __global__ void __launch_bounds__(kPanelThreads, 1) panel_kernel(PanelParams pin
       if (gb.slot >= 0 && gs == gb.slot) s_win = mine;  // the thread holding the winning record
       if (tid == 0) s_hascand = gb.slot >= 0 ? 1 : 0;
       __syncthreads();
-      if (tid == 0) {
-        ll_put_d(dec + 0, tag, s_win.key);
-        ll_put_d(dec + 2, tag, s_win.val);
-        ll_put_d(dec + 4, tag, s_win.diag);
-        ll_put_d(dec + 6, tag, s_gakk);
-        ll_put(dec + 8, tag, static_cast<unsigned>(s_win.lidx));
-        ll_put(dec + 9, tag, static_cast<unsigned>(s_win.phys));
-        ll_put(dec + 10, tag, (s_hascand ? 1u : 0u) | (s_gerr ? 2u : 0u) | (s_abort ? 4u : 0u));
-        ll_put(dec + 11, tag, static_cast<unsigned>(gb.slot));
-        s_gs2 = gb.slot;
+      {
+        unsigned hw[12];
+        const u64 kb = static_cast<u64>(__double_as_longlong(s_win.key));
+        const u64 vb = static_cast<u64>(__double_as_longlong(s_win.val));
+        const u64 db = static_cast<u64>(__double_as_longlong(s_win.diag));
+        const u64 ab = static_cast<u64>(__double_as_longlong(s_gakk));
+        hw[0] = static_cast<unsigned>(kb);
+        hw[1] = static_cast<unsigned>(kb >> 32);
+        hw[2] = static_cast<unsigned>(vb);
+        hw[3] = static_cast<unsigned>(vb >> 32);
+        hw[4] = static_cast<unsigned>(db);
+        hw[5] = static_cast<unsigned>(db >> 32);
+        hw[6] = static_cast<unsigned>(ab);
+        hw[7] = static_cast<unsigned>(ab >> 32);
+        hw[8] = static_cast<unsigned>(s_win.lidx);
+        hw[9] = static_cast<unsigned>(s_win.phys);
+        hw[10] = (s_hascand ? 1u : 0u) | (s_gerr ? 2u : 0u) | (s_abort ? 4u : 0u);
+        hw[11] = static_cast<unsigned>(gb.slot);
+#if RCP_SBKP_SHARED
+        if (tid < 12) ll_put(p.sdll + (size_t)pb * G * kMWords + tid, tag, hw[tid]);
+#else
+        for (int f = tid; f < G * 12; f += nthr) {
+          const int c = f / 12, u = f - c * 12;
+          if (c != 0) ll_put(p.sdll + ((size_t)pb * G + c) * kMWords + u, tag, hw[u]);
+        }
+#endif
       }
+      if (tid == 0) s_gs2 = gb.slot;
       // The decision will need the partner column r unless the 1x1 test passes: start pulling it
       // into L2 now, while the workers are still waiting for this broadcast.
       if (s_hascand && !(fabs(s_gakk) >= __dmul_rn(alpha, s_win.key))) {
@@ -921,7 +959,7 @@ __global__ void __launch_bounds__(kPanelThreads, 1) panel_kernel(PanelParams pin
     } else {
       if (tid < 12) {
         unsigned w[1];
-        if (!ll_read<1>(dec + tid, tag, w)) {
+        if (!ll_read<1>(p.sdll + ((size_t)pb * G + (RCP_SBKP_SHARED ? 0 : cta)) * kMWords + tid, tag, w)) {
           s_abort = 1;
           w[0] = 0;
         }

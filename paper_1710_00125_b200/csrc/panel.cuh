@@ -99,6 +99,7 @@ struct PanelState {
 
 constexpr int kXWords = 16;  // 11 used, padded to 128 B per record
 constexpr int kQWords = 8;  // norm(2) pos col coef(2) skip, padded
+constexpr int kMWords = 16;  // one 128-byte decision mailbox line per CTA
 
 // One CTA's contribution to a pivot-search exchange (SBKP step).
 struct XRec {
@@ -149,8 +150,10 @@ struct PanelParams {
   unsigned long long* xll;   // SBKP records  [2][G][kXWords]
   unsigned long long* qll;   // QRCP records  [2][G][kQWords]
   unsigned long long* qcll;  // QRCP candidate columns [2][G][2P]
-  unsigned long long* sdll;  // SBKP decision broadcast by the reducer CTA [2][kXWords]
-  unsigned long long* qdll;  // QRCP decision header [2][8]
+  // Decisions are pushed by the reducer CTA into one private mailbox line per CTA, so each CTA
+  // polls its own line (no hot line polled by the whole grid).
+  unsigned long long* sdll;  // SBKP decision mailboxes [2][G][kMWords]
+  unsigned long long* qdll;  // QRCP / q = 1 decision mailboxes [2][G][kMWords]
   PanelState* st;
   // device-driven geometry (desc != nullptr): k0 from the descriptor, the rest recomputed
   const PanelDesc* desc;
