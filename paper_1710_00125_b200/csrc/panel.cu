@@ -180,7 +180,10 @@ __global__ void __launch_bounds__(kPanelThreads, 1) panel_kernel(PanelParams pin
 #ifndef RCP_PANEL_PROF
 #define RCP_PANEL_PROF 0  // build with -DRCP_PANEL_PROF=1 for the per-phase cycle profile
 #endif
-  const bool prof = RCP_PANEL_PROF && (cta == 0 && tid == 0);
+#ifndef RCP_PROF_CTA
+#define RCP_PROF_CTA 0  // CTA whose phases the profile build times
+#endif
+  const bool prof = RCP_PANEL_PROF && (cta == RCP_PROF_CTA && tid == 0);
   const long long c_kernel0 = prof ? prof_now() : 0;
   long long c_mark = 0;
 #define PROF_BEGIN() \
@@ -198,6 +201,7 @@ __global__ void __launch_bounds__(kPanelThreads, 1) panel_kernel(PanelParams pin
   int* win = reinterpret_cast<int*>(carve(sizeof(int) * Wn));
   int* lpos = reinterpret_cast<int*>(carve(sizeof(int) * R));
   double* vvec = reinterpret_cast<double*>(carve(sizeof(double) * P));
+  double* vvec2 = reinterpret_cast<double*>(carve(sizeof(double) * P));  // QRCP: previous reflector
   double* wrow = reinterpret_cast<double*>(carve(sizeof(double) * Wn));
   double* wrrow = reinterpret_cast<double*>(carve(sizeof(double) * Wn));
   double* lnext = reinterpret_cast<double*>(carve(sizeof(double) * Wn));
@@ -245,6 +249,11 @@ __global__ void __launch_bounds__(kPanelThreads, 1) panel_kernel(PanelParams pin
     double myn = -1.0, myn2 = 0.0, myn2x = 0.0;
     bool exact_only = false;
     int mypos = own ? r0 + tid : INT_MAX;
+    // Register mode defers each reflector's update of the smem rows to the next step's pass
+    // (x <- x - v_prev * w_prev, then the dot with v): one smem pass per step instead of two, with
+    // bit-identical values.  Reflectors alternate between vvec / vvec2.
+    double wpend = 0.0;  // w of the pending (previous) reflector for the own column
+    bool pend = false;   // rows >= j of Bs still need the previous reflector
 
     // ---- load
     if (own) {
@@ -299,7 +308,162 @@ __global__ void __launch_bounds__(kPanelThreads, 1) panel_kernel(PanelParams pin
       }
       myn2x = myn2;
     };
+    // Householder reflector (vv over rows [jj, P), coef, skip) applied to the own column, then the
+    // residual-norm downdate.  Residual norms are downdated (|r|^2 -= y^2) and recomputed exactly
+    // whenever cancellation could cost more than ~1e-10 relative accuracy (LAPACK xLAQP2 policy).
+    auto reflect_own = [&](const double* vv, int jj, double coef, int skip) {
+      double yj;
+      if (!skip) {
+        double d0 = 0.0, d1 = 0.0, d2 = 0.0, d3 = 0.0;
+#pragma unroll
+        for (int r = 0; r < kRegRows; r += 4) {
+          if (r >= jj && r < PRr) d0 = __fma_rn(vv[r], rg[r], d0);
+          if (r + 1 >= jj && r + 1 < PRr) d1 = __fma_rn(vv[r + 1], rg[r + 1], d1);
+          if (r + 2 >= jj && r + 2 < PRr) d2 = __fma_rn(vv[r + 2], rg[r + 2], d2);
+          if (r + 3 >= jj && r + 3 < PRr) d3 = __fma_rn(vv[r + 3], rg[r + 3], d3);
+        }
+        int r = max(jj, PRr);
+        const double* bc = Bs + (size_t)(r - PRr) * Rs + tid;
+#pragma unroll 2
+        for (; r + 4 <= P; r += 4, bc += 4 * Rs) {
+          d0 = __fma_rn(vv[r], bc[0], d0);
+          d1 = __fma_rn(vv[r + 1], bc[Rs], d1);
+          d2 = __fma_rn(vv[r + 2], bc[2 * Rs], d2);
+          d3 = __fma_rn(vv[r + 3], bc[3 * Rs], d3);
+        }
+        for (; r < P; ++r, bc += Rs) d0 = __fma_rn(vv[r], bc[0], d0);
+        const double wv = __dmul_rn(coef, __dadd_rn(__dadd_rn(d0, d1), __dadd_rn(d2, d3)));
+#pragma unroll
+        for (int r2 = 0; r2 < kRegRows; ++r2)
+          if (r2 >= jj && r2 < PRr) rg[r2] = __fma_rn(-vv[r2], wv, rg[r2]);
+        r = max(jj, PRr);
+        double* bw = Bs + (size_t)(r - PRr) * Rs + tid;
+        // batched: all loads of a group before its stores (smem aliasing would
+        // otherwise serialise every element on the load latency)
+        for (; r + 8 <= P; r += 8, bw += 8 * Rs) {
+          double x[8], vl[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            x[u] = bw[u * Rs];
+            vl[u] = vv[r + u];
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u) bw[u * Rs] = __fma_rn(-vl[u], wv, x[u]);
+        }
+        for (; r < P; ++r, bw += Rs) *bw = __fma_rn(-vv[r], wv, *bw);
+      }
+      if (jj < PRr) {
+        yj = 0.0;
+#pragma unroll
+        for (int r2 = 0; r2 < kRegRows; ++r2)
+          if (r2 == jj) yj = rg[r2];
+      } else {
+        yj = Bs[(jj - PRr) * Rs + tid];
+      }
+      const double n2 = __fma_rn(-yj, yj, myn2);
+      if (exact_only || !(n2 > 1e-6 * myn2x) || !(n2 > 1e-280)) {
+        exact_norm(jj + 1);
+      } else {
+        myn2 = n2;
+        myn = sqrt(n2);
+      }
+    };
+    // Fused variant (register mode): the pending reflector (vp, wpend) of the previous step is
+    // applied to the smem rows while forming this step's dot, and this step's reflector becomes
+    // the pending one.  Values are bit-identical to reflect_own applied step by step.
+    auto reflect_fused = [&](const double* vc, const double* vp, int jj, double coef, int skip) {
+      double d0 = 0.0, d1 = 0.0, d2 = 0.0, d3 = 0.0;
+      if (!skip) {
+#pragma unroll
+        for (int r = 0; r < kRegRows; r += 4) {
+          if (r >= jj && r < PRr) d0 = __fma_rn(vc[r], rg[r], d0);
+          if (r + 1 >= jj && r + 1 < PRr) d1 = __fma_rn(vc[r + 1], rg[r + 1], d1);
+          if (r + 2 >= jj && r + 2 < PRr) d2 = __fma_rn(vc[r + 2], rg[r + 2], d2);
+          if (r + 3 >= jj && r + 3 < PRr) d3 = __fma_rn(vc[r + 3], rg[r + 3], d3);
+        }
+      }
+      const int rs = max(jj, PRr);
+      double xjj = 0.0;  // x at row jj (smem rows) after the pending update
+      {
+        int r = rs;
+        double* bw = Bs + (size_t)(r - PRr) * Rs + tid;
+        if (pend) {
+          const double wp = wpend;
+          for (; r + 4 <= P; r += 4, bw += 4 * Rs) {
+            double x0 = bw[0], x1 = bw[Rs], x2 = bw[2 * Rs], x3 = bw[3 * Rs];
+            x0 = __fma_rn(-vp[r], wp, x0);
+            x1 = __fma_rn(-vp[r + 1], wp, x1);
+            x2 = __fma_rn(-vp[r + 2], wp, x2);
+            x3 = __fma_rn(-vp[r + 3], wp, x3);
+            bw[0] = x0;
+            bw[Rs] = x1;
+            bw[2 * Rs] = x2;
+            bw[3 * Rs] = x3;
+            if (r == jj) xjj = x0;
+            if (!skip) {
+              d0 = __fma_rn(vc[r], x0, d0);
+              d1 = __fma_rn(vc[r + 1], x1, d1);
+              d2 = __fma_rn(vc[r + 2], x2, d2);
+              d3 = __fma_rn(vc[r + 3], x3, d3);
+            }
+          }
+          for (; r < P; ++r, bw += Rs) {
+            const double x = __fma_rn(-vp[r], wp, *bw);
+            *bw = x;
+            if (r == jj) xjj = x;
+            if (!skip) d0 = __fma_rn(vc[r], x, d0);
+          }
+        } else {
+          for (; r + 4 <= P; r += 4, bw += 4 * Rs) {
+            const double x0 = bw[0], x1 = bw[Rs], x2 = bw[2 * Rs], x3 = bw[3 * Rs];
+            if (r == jj) xjj = x0;
+            if (!skip) {
+              d0 = __fma_rn(vc[r], x0, d0);
+              d1 = __fma_rn(vc[r + 1], x1, d1);
+              d2 = __fma_rn(vc[r + 2], x2, d2);
+              d3 = __fma_rn(vc[r + 3], x3, d3);
+            }
+          }
+          for (; r < P; ++r, bw += Rs) {
+            const double x = *bw;
+            if (r == jj) xjj = x;
+            if (!skip) d0 = __fma_rn(vc[r], x, d0);
+          }
+        }
+      }
+      double wv = 0.0;
+      if (!skip) {
+        wv = __dmul_rn(coef, __dadd_rn(__dadd_rn(d0, d1), __dadd_rn(d2, d3)));
+#pragma unroll
+        for (int r2 = 0; r2 < kRegRows; ++r2)
+          if (r2 >= jj && r2 < PRr) rg[r2] = __fma_rn(-vc[r2], wv, rg[r2]);
+      }
+      double yj;
+      if (jj < PRr) {
+        yj = 0.0;
+#pragma unroll
+        for (int r2 = 0; r2 < kRegRows; ++r2)
+          if (r2 == jj) yj = rg[r2];
+      } else {
+        yj = skip ? xjj : __fma_rn(-vc[jj], wv, xjj);
+      }
+      wpend = wv;
+      const double n2 = __fma_rn(-yj, yj, myn2);
+      if (exact_only || !(n2 > 1e-6 * myn2x) || !(n2 > 1e-280)) {
+        // the exact recompute needs the current values: apply this step's reflector now
+        if (!skip) {
+          double* bw = Bs + (size_t)(rs - PRr) * Rs + tid;
+          for (int r = rs; r < P; ++r, bw += Rs) *bw = __fma_rn(-vc[r], wv, *bw);
+          wpend = 0.0;  // already applied; x - v * 0 leaves the values unchanged next step
+        }
+        exact_norm(jj + 1);
+      } else {
+        myn2 = n2;
+        myn = sqrt(n2);
+      }
+    };
     if (own) exact_norm(0);
+
     if (!regmode) {
       for (int c = tid; c < rcnt; c += nthr) {
         double ss = 0.0, am = 0.0;
@@ -314,6 +478,8 @@ __global__ void __launch_bounds__(kPanelThreads, 1) panel_kernel(PanelParams pin
     __syncthreads();
 
     for (int j = 0; j < p.qn; ++j) {
+      double* const vcur = (regmode && (j & 1)) ? vvec2 : vvec;  // this step's reflector
+      const double* const vprv = (regmode && (j & 1)) ? vvec : vvec2;  // the pending one (regmode)
       // ---- local candidate: largest residual norm, ties to the lowest position
       PROF_BEGIN();
       double bk = -1.0;
@@ -353,26 +519,33 @@ __global__ void __launch_bounds__(kPanelThreads, 1) panel_kernel(PanelParams pin
           if (regmode && lane == (lb.slot & 31)) {
 #pragma unroll
             for (int r = 0; r < kRegRows; ++r)
-              if (r >= j && r < PRr) vvec[r] = rg[r];
+              if (r >= j && r < PRr) vcur[r] = rg[r];
           }
-          for (int r = max(j, PRr) + lane; r < P; r += 32)
-            vvec[r] = regmode ? Bs[(r - PRr) * Rs + lb.slot] : bsm(r, lb.slot);
+          const double wc = __shfl_sync(0xffffffffu, wpend, lb.slot & 31);  // candidate's pending w
+          for (int r = max(j, PRr) + lane; r < P; r += 32) {
+            if (regmode) {
+              const double x = Bs[(r - PRr) * Rs + lb.slot];
+              vcur[r] = pend ? __fma_rn(-vprv[r], wc, x) : x;
+            } else {
+              vcur[r] = bsm(r, lb.slot);
+            }
+          }
           __syncwarp();
-          const double xn = __shfl_sync(0xffffffffu, sqrt(warp0_sum_sq(vvec, j, P)), 0);
+          const double xn = __shfl_sync(0xffffffffu, sqrt(warp0_sum_sq(vcur, j, P)), 0);
           double coef = 0.0;
           unsigned skip = 1;
           if (xn != 0.0) {
             if (lane == 0) {
-              const double x0 = vvec[j];
-              vvec[j] = __dadd_rn(x0, copysign(xn, x0 != 0.0 ? x0 : 1.0));
+              const double x0 = vcur[j];
+              vcur[j] = __dadd_rn(x0, copysign(xn, x0 != 0.0 ? x0 : 1.0));
             }
             __syncwarp();
-            const double vn2 = __shfl_sync(0xffffffffu, warp0_sum_sq(vvec, j, P), 0);
+            const double vn2 = __shfl_sync(0xffffffffu, warp0_sum_sq(vcur, j, P), 0);
             skip = (vn2 == 0.0) ? 1u : 0u;
             coef = (vn2 == 0.0) ? 0.0 : 2.0 / vn2;
           }
           u64* dst = p.qcll + ((size_t)pb * G + cta) * 2 * P;
-          for (int r = j + lane; r < P; r += 32) ll_put_d(dst + 2 * r, tag, vvec[r]);
+          for (int r = j + lane; r < P; r += 32) ll_put_d(dst + 2 * r, tag, vcur[r]);
           if (lane == 0) {
             u64* q = p.qll + ((size_t)pb * G + cta) * kQWords;
             ll_put_d(q, tag, lb.key);
@@ -479,7 +652,7 @@ __global__ void __launch_bounds__(kPanelThreads, 1) panel_kernel(PanelParams pin
         for (int r = j + tid; r < P; r += nthr) {
           unsigned w[2];
           if (!ll_read<2>(src + 2 * r, tag, w)) s_abort = 1;
-          vvec[r] = ll_d(w[0], w[1]);
+          vcur[r] = ll_d(w[0], w[1]);
         }
       }
       __syncthreads();
@@ -520,65 +693,8 @@ __global__ void __launch_bounds__(kPanelThreads, 1) panel_kernel(PanelParams pin
         const int skip = s_skip;
         const double coef = s_coef;
         if (regmode) {
-          if (own && !mysel) {
-            // Residual norms are downdated (|r|^2 -= y_j^2) and recomputed exactly whenever
-            // cancellation could cost more than ~1e-10 relative accuracy (LAPACK xLAQP2 policy).
-            double yj;
-            if (!skip) {
-              double d0 = 0.0, d1 = 0.0, d2 = 0.0, d3 = 0.0;
-#pragma unroll
-              for (int r = 0; r < kRegRows; r += 4) {
-                if (r >= j && r < PRr) d0 = __fma_rn(vvec[r], rg[r], d0);
-                if (r + 1 >= j && r + 1 < PRr) d1 = __fma_rn(vvec[r + 1], rg[r + 1], d1);
-                if (r + 2 >= j && r + 2 < PRr) d2 = __fma_rn(vvec[r + 2], rg[r + 2], d2);
-                if (r + 3 >= j && r + 3 < PRr) d3 = __fma_rn(vvec[r + 3], rg[r + 3], d3);
-              }
-              int r = max(j, PRr);
-              const double* bc = Bs + (size_t)(r - PRr) * Rs + tid;
-#pragma unroll 2
-              for (; r + 4 <= P; r += 4, bc += 4 * Rs) {
-                d0 = __fma_rn(vvec[r], bc[0], d0);
-                d1 = __fma_rn(vvec[r + 1], bc[Rs], d1);
-                d2 = __fma_rn(vvec[r + 2], bc[2 * Rs], d2);
-                d3 = __fma_rn(vvec[r + 3], bc[3 * Rs], d3);
-              }
-              for (; r < P; ++r, bc += Rs) d0 = __fma_rn(vvec[r], bc[0], d0);
-              const double wv = __dmul_rn(coef, __dadd_rn(__dadd_rn(d0, d1), __dadd_rn(d2, d3)));
-#pragma unroll
-              for (int r2 = 0; r2 < kRegRows; ++r2)
-                if (r2 >= j && r2 < PRr) rg[r2] = __fma_rn(-vvec[r2], wv, rg[r2]);
-              r = max(j, PRr);
-              double* bw = Bs + (size_t)(r - PRr) * Rs + tid;
-              // batched: all loads of a group before its stores (smem aliasing would
-              // otherwise serialise every element on the load latency)
-              for (; r + 8 <= P; r += 8, bw += 8 * Rs) {
-                double x[8], vv[8];
-#pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                  x[u] = bw[u * Rs];
-                  vv[u] = vvec[r + u];
-                }
-#pragma unroll
-                for (int u = 0; u < 8; ++u) bw[u * Rs] = __fma_rn(-vv[u], wv, x[u]);
-              }
-              for (; r < P; ++r, bw += Rs) *bw = __fma_rn(-vvec[r], wv, *bw);
-            }
-            if (j < PRr) {
-              yj = 0.0;
-#pragma unroll
-              for (int r2 = 0; r2 < kRegRows; ++r2)
-                if (r2 == j) yj = rg[r2];
-            } else {
-              yj = Bs[(j - PRr) * Rs + tid];
-            }
-            const double n2 = __fma_rn(-yj, yj, myn2);
-            if (exact_only || !(n2 > 1e-6 * myn2x) || !(n2 > 1e-280)) {
-              exact_norm(j + 1);
-            } else {
-              myn2 = n2;
-              myn = sqrt(n2);
-            }
-          }
+          if (own && !mysel) reflect_fused(vcur, vprv, j, coef, skip);
+          pend = !skip;
         } else {
           for (int c = tid; c < rcnt; c += nthr) {
             if (qsel[c]) continue;

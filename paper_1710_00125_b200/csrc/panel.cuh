@@ -55,7 +55,7 @@ RCP_PG PanelGeom panel_geometry(int64_t n, int k0, int b, int q, int P, int num_
   g.Wn = g.width + 2;
   g.qn = (q > 1 && g.m0 > 1) ? pg_min(pg_min(q, g.width), pg_min(g.m0, P)) : 0;
   auto a16 = [](long long x) { return (x + 15) & ~15LL; };
-  const long long fixed = a16(4LL * g.Wn) + a16(4LL * R) + a16(8LL * P) + 4 * a16(8LL * g.Wn);
+  const long long fixed = a16(4LL * g.Wn) + a16(4LL * R) + 2 * a16(8LL * P) + 4 * a16(8LL * g.Wn);
   const long long avail = (long long)smem_budget - fixed;
   g.qmode = 0;
   g.Rs = 0;
