@@ -60,7 +60,7 @@ inline Layout make_layout(int64_t n, const rcp_config& c) {
   L.flags = take(0);
   L.xrec = take(8 * 2 * kMaxSMs * (size_t)kXWords);
   L.qrec = take(8 * 2 * kMaxSMs * (size_t)kQWords);
-  L.qcol = take(8 * 2 * kMaxSMs * 2 * (size_t)P);
+  L.qcol = take(8 * 2 * kMaxSMs * qcol_stride(P));
   L.sdec = take(8 * 2 * kMaxSMs * (size_t)kMWords);  // per-CTA decision mailboxes (SBKP)
   L.qdec = take(8 * 2 * kMaxSMs * (size_t)kMWords);  // per-CTA decision mailboxes (QRCP, q = 1 pivot)
   L.state = take(sizeof(PanelState));

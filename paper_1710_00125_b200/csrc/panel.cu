@@ -174,6 +174,7 @@ __global__ void __launch_bounds__(kPanelThreads, 1) panel_kernel(PanelParams pin
   }
   const int64_t n = p.n;
   const int k0 = p.k0, P = p.P, R = p.R, G = p.G, Wn = p.Wn;
+  const size_t QS = qcol_stride(P);  // LL words per candidate-column buffer
   const int m0 = static_cast<int>(n - k0);
   const int r0 = cta * R;
   const int rcnt = max(0, min(R, m0 - r0));
@@ -511,8 +512,19 @@ __global__ void __launch_bounds__(kPanelThreads, 1) panel_kernel(PanelParams pin
       // ---- speculative Householder vector of this CTA's candidate (sketch.py:159-168):
       //      only the global winner's v is used, so every CTA prepares its own and the
       //      reducer broadcasts just a small header.
+      if (tid == 0) {  // the record goes out first; the reflector is built while it travels
+        u64* q = p.qll + ((size_t)pb * G + cta) * kQWords;
+        const bool has = lb.slot >= 0;
+        ll_put_d(q, tag, has ? lb.key : -1.0);
+        ll_put(q + 2, tag, has ? static_cast<unsigned>(lb.idx) : 0x7fffffffu);
+        ll_put(q + 3, tag, has ? static_cast<unsigned>(r0 + lb.slot) : 0xffffffffu);
+      }
+      seq = nseq;
+      __syncthreads();  // records out before anyone polls (measured: avoids a delayed store)
+      PROF_END(9);
       {
-        // Built by the warp holding the candidate column (warp 0 in generic mode), no CTA barrier.
+        // Speculative reflector of this CTA's candidate (sketch.py:159-168), built by the warp holding
+        // the column (warp 0 in generic mode) while the exchange is in flight; only the winner's is read.
         const int lane = tid & 31;
         const int hwarp = lb.slot < 0 ? -1 : (regmode ? (lb.slot >> 5) : 0);
         if ((tid >> 5) == hwarp) {
@@ -544,29 +556,14 @@ __global__ void __launch_bounds__(kPanelThreads, 1) panel_kernel(PanelParams pin
             skip = (vn2 == 0.0) ? 1u : 0u;
             coef = (vn2 == 0.0) ? 0.0 : 2.0 / vn2;
           }
-          u64* dst = p.qcll + ((size_t)pb * G + cta) * 2 * P;
+          u64* dst = p.qcll + ((size_t)pb * G + cta) * QS;
           for (int r = j + lane; r < P; r += 32) ll_put_d(dst + 2 * r, tag, vcur[r]);
           if (lane == 0) {
-            u64* q = p.qll + ((size_t)pb * G + cta) * kQWords;
-            ll_put_d(q, tag, lb.key);
-            ll_put(q + 2, tag, static_cast<unsigned>(lb.idx));
-            ll_put(q + 3, tag, static_cast<unsigned>(r0 + lb.slot));
-            ll_put_d(q + 4, tag, coef);
-            ll_put(q + 6, tag, skip);
+            ll_put_d(dst + 2 * P, tag, coef);
+            ll_put(dst + 2 * P + 2, tag, skip);
           }
         }
-        if (lb.slot < 0 && tid == 0) {
-          u64* q = p.qll + ((size_t)pb * G + cta) * kQWords;
-          ll_put_d(q, tag, -1.0);
-          ll_put(q + 2, tag, 0x7fffffffu);
-          ll_put(q + 3, tag, 0xffffffffu);
-          ll_put_d(q + 4, tag, 0.0);
-          ll_put(q + 6, tag, 1u);
-        }
       }
-      seq = nseq;
-      __syncthreads();  // records out before anyone polls (measured: avoids a delayed store)
-      PROF_END(9);
       PROF_BEGIN();
       // ---- reducer CTA 0: winner over all records -> a 6-word decision pushed into every CTA's
       //      mailbox (winner CTA, position, column, coef, flags); every CTA then reads v from
@@ -575,10 +572,10 @@ __global__ void __launch_bounds__(kPanelThreads, 1) panel_kernel(PanelParams pin
         double gk = -1.0;
         long long gi = LLONG_MAX;
         int gs = -1;
-        unsigned gw[7] = {0, 0, 0, 0, 0, 0, 0};
+        unsigned gw[4] = {0, 0, 0, 0};
         for (int c = tid; c < G; c += nthr) {
-          unsigned w[7];
-          if (!ll_read<7>(p.qll + ((size_t)pb * G + c) * kQWords, tag, w)) {
+          unsigned w[4];
+          if (!ll_read<4>(p.qll + ((size_t)pb * G + c) * kQWords, tag, w)) {
             s_abort = 1;
             continue;
           }
@@ -589,7 +586,7 @@ __global__ void __launch_bounds__(kPanelThreads, 1) panel_kernel(PanelParams pin
             gi = ps;
             gs = c;
 #pragma unroll
-            for (int u = 0; u < 7; ++u) gw[u] = w[u];
+            for (int u = 0; u < 4; ++u) gw[u] = w[u];
           }
         }
         BlockBest gb = block_argmax(gk, gi, gs, par);
@@ -598,30 +595,26 @@ __global__ void __launch_bounds__(kPanelThreads, 1) panel_kernel(PanelParams pin
           s_qhdr[0] = static_cast<unsigned>(gs);
           s_qhdr[1] = gw[2];
           s_qhdr[2] = gw[3];
-          s_qhdr[3] = gw[4];
-          s_qhdr[4] = gw[5];
-          s_qhdr[5] = (gw[6] ? 1u : 0u) | (gstop ? 2u : 0u);
+          s_qhdr[3] = gstop ? 2u : 0u;
         }
-        if (gb.slot < 0 && tid == 0) s_qhdr[5] = 4u;  // no candidate anywhere: cannot happen
+        if (gb.slot < 0 && tid == 0) s_qhdr[3] = 4u;  // no candidate anywhere: cannot happen
         __syncthreads();
-        unsigned hw[6];
+        unsigned hw[4];
 #pragma unroll
-        for (int u = 0; u < 6; ++u) hw[u] = s_qhdr[u];
-        if (s_abort) hw[5] = 4u;
-        for (int f = tid; f < G * 6; f += nthr) {
-          const int c = f / 6, u = f - c * 6;
+        for (int u = 0; u < 4; ++u) hw[u] = s_qhdr[u];
+        if (s_abort) hw[3] = 4u;
+        for (int f = tid; f < G * 4; f += nthr) {
+          const int c = f >> 2, u = f & 3;
           if (c != 0) ll_put(p.qdll + ((size_t)pb * G + c) * kMWords + u, tag, hw[u]);
         }
         if (tid == 0) {
           s_wcta = static_cast<int>(hw[0]);
           s_wpos = static_cast<int>(hw[1]);
           s_wcol = static_cast<int>(hw[2]);
-          s_coef = ll_d(hw[3], hw[4]);
-          s_qflags = static_cast<int>(hw[5]);
-          s_skip = hw[5] & 1;
+          s_qflags = static_cast<int>(hw[3]);
         }
       } else {
-        if (tid < 6) {
+        if (tid < 4) {
           unsigned w[1];
           if (!ll_read<1>(p.qdll + ((size_t)pb * G + cta) * kMWords + tid, tag, w)) {
             s_abort = 1;
@@ -634,9 +627,7 @@ __global__ void __launch_bounds__(kPanelThreads, 1) panel_kernel(PanelParams pin
           s_wcta = static_cast<int>(s_qhdr[0]);
           s_wpos = static_cast<int>(s_qhdr[1]);
           s_wcol = static_cast<int>(s_qhdr[2]);
-          s_coef = ll_d(s_qhdr[3], s_qhdr[4]);
-          s_qflags = static_cast<int>(s_qhdr[5]);
-          s_skip = s_qflags & 1;
+          s_qflags = static_cast<int>(s_qhdr[3]);
           if (s_abort) s_qflags |= 4;
         }
       }
@@ -647,12 +638,18 @@ __global__ void __launch_bounds__(kPanelThreads, 1) panel_kernel(PanelParams pin
       // replay bookkeeping (factor.py:586-599), position j <-> wpos: every thread reads the
       // displaced column now; thread 0 rewrites `win` after the next barrier
       const int moved = (wpos != j) ? win[j] : -1;
-      if (!(s_qflags & 6)) {  // fetch the winner's Householder vector
-        const u64* src = p.qcll + ((size_t)pb * G + s_wcta) * 2 * P;
+      if (!(s_qflags & 6)) {  // fetch the winner's Householder vector, coef and skip flag
+        const u64* src = p.qcll + ((size_t)pb * G + s_wcta) * QS;
         for (int r = j + tid; r < P; r += nthr) {
           unsigned w[2];
           if (!ll_read<2>(src + 2 * r, tag, w)) s_abort = 1;
           vcur[r] = ll_d(w[0], w[1]);
+        }
+        if (tid == nthr - 1) {
+          unsigned w[3];
+          if (!ll_read<3>(src + 2 * P, tag, w)) s_abort = 1;
+          s_coef = ll_d(w[0], w[1]);
+          s_skip = static_cast<int>(w[2]);
         }
       }
       __syncthreads();
@@ -827,7 +824,7 @@ __global__ void __launch_bounds__(kPanelThreads, 1) panel_kernel(PanelParams pin
         const int pb1 = static_cast<int>(nseq1 & 1);
         const unsigned tag1 = static_cast<unsigned>(nseq1);
         if (lb1.slot >= 0) {
-          u64* dst = p.qcll + ((size_t)pb1 * G + cta) * 2 * P;
+          u64* dst = p.qcll + ((size_t)pb1 * G + cta) * QS;
           for (int r = tid; r < P; r += nthr) ll_put_d(dst + 2 * r, tag1, Bq[r * R + lb1.slot]);
         }
         if (tid == 0) {
@@ -924,7 +921,7 @@ __global__ void __launch_bounds__(kPanelThreads, 1) panel_kernel(PanelParams pin
         }
         // pivot sketch column (for the per-step downdate) from the winner's LL buffer
         {
-          const u64* src = p.qcll + ((size_t)pb1 * G + s_gs1) * 2 * P;
+          const u64* src = p.qcll + ((size_t)pb1 * G + s_gs1) * QS;
           for (int r = tid; r < P; r += nthr) {
             unsigned w[2];
             ll_read<2>(src + 2 * r, tag1, w);
@@ -983,7 +980,7 @@ __global__ void __launch_bounds__(kPanelThreads, 1) panel_kernel(PanelParams pin
     const int pb = static_cast<int>(nseq & 1);
     const unsigned tag = static_cast<unsigned>(nseq);
     if (q1 && lb.slot >= 0) {
-      u64* dst = p.qcll + ((size_t)pb * G + cta) * 2 * P;
+      u64* dst = p.qcll + ((size_t)pb * G + cta) * QS;
       for (int r = tid; r < P; r += nthr) ll_put_d(dst + 2 * r, tag, Bq[r * R + lb.slot]);
     }
     if (tid == 0) {
@@ -1194,7 +1191,7 @@ __global__ void __launch_bounds__(kPanelThreads, 1) panel_kernel(PanelParams pin
     if (kind >= 2) {
       for (int s2 = tid; s2 < t; s2 += nthr) wrrow[s2] = __ldcg(p.W + (k0 + pr) + (int64_t)s2 * n);
       if (q1) {  // partner's sketch column (per-step downdate, factor.py:486-489)
-        const u64* src = p.qcll + ((size_t)pb * G + s_gs2) * 2 * P;
+        const u64* src = p.qcll + ((size_t)pb * G + s_gs2) * QS;
         for (int r = tid; r < P; r += nthr) {
           unsigned w[2];
           ll_read<2>(src + 2 * r, tag, w);

@@ -100,6 +100,8 @@ struct PanelState {
 constexpr int kXWords = 16;  // 11 used, padded to 128 B per record
 constexpr int kQWords = 8;  // norm(2) pos col coef(2) skip, padded
 constexpr int kMWords = 16;  // one 128-byte decision mailbox line per CTA
+// LL words of one CTA's candidate-column buffer: 2 per sketch row + coef (2) + skip (1), padded
+RCP_PG size_t qcol_stride(int P) { return 2 * (size_t)P + 4; }
 
 // One CTA's contribution to a pivot-search exchange (SBKP step).
 struct XRec {
@@ -149,7 +151,7 @@ struct PanelParams {
   // the 32-bit exchange tag, so a reader validates data and arrival with one load.
   unsigned long long* xll;   // SBKP records  [2][G][kXWords]
   unsigned long long* qll;   // QRCP records  [2][G][kQWords]
-  unsigned long long* qcll;  // QRCP candidate columns [2][G][2P]
+  unsigned long long* qcll;  // QRCP candidate columns [2][G][qcol_stride(P)]
   // Decisions are pushed by the reducer CTA into one private mailbox line per CTA, so each CTA
   // polls its own line (no hot line polled by the whole grid).
   unsigned long long* sdll;  // SBKP decision mailboxes [2][G][kMWords]
