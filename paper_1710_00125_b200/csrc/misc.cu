@@ -102,13 +102,14 @@ __global__ void gather_kernel(int64_t n, int k0, int k_end, int t, int tpad, int
     rows_pad = ((mp_ + 127) / 128) * 128;
     snap += d->snap_off;
   }
-  // compact unit-lower panel block L11 (t x t, row-major ld t) in logical order, for ysolve
+  // compact strictly-lower panel block L11 in logical order, stored by columns for ysolve:
+  // L11T[c * t + a] = L11[a][c]
   {
     const int64_t nthreads = (int64_t)gridDim.x * blockDim.x * blockDim.y;
     const int64_t tflat = ((int64_t)blockIdx.x * blockDim.y + threadIdx.y) * blockDim.x + threadIdx.x;
     for (int64_t f = tflat; f < (int64_t)t * t; f += nthreads) {
       const int a = (int)(f / t), c = (int)(f - (int64_t)a * t);
-      L11[f] = (c < a) ? Lbuf[phys_of_log[k0 + a] + (int64_t)(k0 + c) * n] : 0.0;
+      L11[(int64_t)c * t + a] = (c < a) ? Lbuf[phys_of_log[k0 + a] + (int64_t)(k0 + c) * n] : 0.0;
     }
   }
   const int64_t mp = n - k_end;
@@ -139,37 +140,49 @@ __global__ void gather_kernel(int64_t n, int k0, int k_end, int t, int tpad, int
 
 // Y = B1 * L11^{-T}  (P x t), with B1[:, a] = Bin[:, piv[a]] and L11 the panel's
 // unit-lower block in logical order.  Algebraically equal to the reference's
-// B1 @ solve_triangular(L11, L21^T, trans='T') (factor.py:554-561).  16 sketch rows per
-// CTA, 16 lanes per row.
+// B1 @ solve_triangular(L11, L21^T, trans='T') (factor.py:554-561).  One warp per sketch row:
+// column-oriented forward substitution (y[c] -= L11[c][a] y[a] for c > a), the row held in
+// registers (lane owns entries lane + 32u), L11 by columns in shared memory.
+constexpr int kYsolveWarps = 8;
 __global__ void ysolve_kernel(int64_t n, int P, int k0, int t, int tpad, const int* __restrict__ phys_of_log,
-                              const double* __restrict__ Bin, const double* __restrict__ L11g,
+                              const double* __restrict__ Bin, const double* __restrict__ L11T,
                               double* __restrict__ Y, const PanelDesc* __restrict__ d) {
   if (d) {
     if (!d->ok || d->t <= 0 || d->k_end >= n) return;
     k0 = d->k0;
     t = d->t;
   }
-  extern __shared__ double sm[];
-  double* L11 = sm;                 // [t][t]
-  double* yv = sm + (size_t)t * t;  // [16][tpad]
-  const int tid = threadIdx.x;
-  for (int f = tid; f < t * t; f += blockDim.x) L11[f] = L11g[f];  // compact copy made by gather_kernel
-  const int rr = tid >> 4, l16 = tid & 15;
-  const int r = blockIdx.x * 16 + rr;
-  // B1 row prefetched (the substitution below is then smem + shuffles only)
-  for (int a = l16; a < tpad; a += 16)
-    yv[rr * tpad + a] = (r < P && a < t) ? Bin[r + (int64_t)phys_of_log[k0 + a] * P] : 0.0;
-  __syncthreads();
-  for (int a = 0; a < t; ++a) {
-    double part = 0.0;
-    for (int c = l16; c < a; c += 16) part = __fma_rn(L11[a * t + c], yv[rr * tpad + c], part);
+  extern __shared__ double sm[];  // [t][t]: row a = column a of L11
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  for (int f = tid; f < t * t; f += blockDim.x) sm[f] = L11T[f];
+  const int r = blockIdx.x * kYsolveWarps + warp;
+  constexpr int kU = 6;  // t <= tpad <= 192 (L11 in smem limits t to ~170 anyway)
+  double y[kU];
 #pragma unroll
-    for (int off = 8; off > 0; off >>= 1) part = __dadd_rn(part, __shfl_xor_sync(0xffffffffu, part, off, 16));
-    if (l16 == 0) yv[rr * tpad + a] = __dsub_rn(yv[rr * tpad + a], part);
-    __syncwarp();
+  for (int u = 0; u < kU; ++u) {
+    const int a = lane + 32 * u;
+    y[u] = (r < P && a < t) ? Bin[r + (int64_t)phys_of_log[k0 + a] * P] : 0.0;
   }
-  if (r < P) {
-    for (int a = l16; a < tpad; a += 16) Y[(int64_t)r * tpad + a] = yv[rr * tpad + a];
+  __syncthreads();
+  if (r >= P) return;
+  for (int a = 0; a < t; ++a) {
+    const int ua = a >> 5;
+    double src = 0.0;
+#pragma unroll
+    for (int u = 0; u < kU; ++u)
+      if (u == ua) src = y[u];
+    const double ya = __shfl_sync(0xffffffffu, src, a & 31);
+    const double* col = sm + (size_t)a * t;
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int c = lane + 32 * u;
+      if (c > a && c < t) y[u] = __fma_rn(-col[c], ya, y[u]);
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < kU; ++u) {
+    const int a = lane + 32 * u;
+    if (a < tpad) Y[(int64_t)r * tpad + a] = (a < t) ? y[u] : 0.0;
   }
 }
 
@@ -275,10 +288,12 @@ cudaError_t launch_gather(int64_t n, int k0, int k_end, int t, int tpad, int64_t
 
 cudaError_t launch_ysolve(int64_t n, int P, int k0, int t, int tpad, const int* phys_of_log, const double* Bin,
                           const double* L11, double* Y, cudaStream_t st, const PanelDesc* d) {
-  size_t smem = sizeof(double) * ((size_t)t * t + 16 * (size_t)tpad);  // t: an upper bound when d != nullptr
+  if (tpad > 192) return cudaErrorInvalidValue;  // register-resident rows: 6 entries per lane
+  size_t smem = sizeof(double) * (size_t)t * t;  // t: an upper bound when d != nullptr
   cudaError_t e = cudaFuncSetAttribute(ysolve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  ysolve_kernel<<<(unsigned)((P + 15) / 16), 256, smem, st>>>(n, P, k0, t, tpad, phys_of_log, Bin, L11, Y, d);
+  ysolve_kernel<<<(unsigned)((P + kYsolveWarps - 1) / kYsolveWarps), 32 * kYsolveWarps, smem, st>>>(
+      n, P, k0, t, tpad, phys_of_log, Bin, L11, Y, d);
   return cudaGetLastError();
 }
 

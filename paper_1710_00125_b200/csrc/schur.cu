@@ -5,6 +5,7 @@
 #include "schur_kernel.cuh"
 #include "schur_ws.cuh"
 #include <algorithm>
+#include <type_traits>
 
 namespace rcp {
 
@@ -39,7 +40,7 @@ struct SketchCorrEpi {
     mp = n - k;
     K = ((d->t + kBK - 1) / kBK) * kBK;
     B.rows = mp;
-    map.tiles_n = (mp + 127) / 128;
+    map.tiles_n = (mp + map.bn - 1) / map.bn;
     return true;
   }
   RCP_D double* cout_mirror(int64_t, int64_t) const { return nullptr; }
@@ -83,6 +84,15 @@ cudaError_t gemm_init_attributes() {
   if (e != cudaSuccess) return e;
   e = cudaFuncSetAttribute(dmma_gemm_kernel<64, 128, kRectStages, 2, ColMajorRectMap, SketchCorrEpi>,
                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gemm_smem_bytes<64, 128, kRectStages>());
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(dmma_gemm_kernel<48, 64, kRectStages, 2, ColMajorRectMap, SketchCorrEpi>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gemm_smem_bytes<48, 64, kRectStages>());
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(dmma_gemm_kernel<96, 64, kRectStages, 2, ColMajorRectMap, SketchCorrEpi>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gemm_smem_bytes<96, 64, kRectStages>());
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(dmma_gemm_kernel<144, 64, kRectStages, 2, ColMajorRectMap, SketchCorrEpi>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gemm_smem_bytes<144, 64, kRectStages>());
   return e;
 }
 
@@ -148,11 +158,24 @@ cudaError_t launch_sketch_correction(int P, int64_t mp, int64_t k, const double*
                                      cudaStream_t st, const PanelDesc* d, int64_t n) {
   // with d: mp / k / K are upper bounds for the grid; the kernel reads the actual values
   if (mp <= 0 || K <= 0) return cudaSuccess;
-  const int64_t tm = (P + 63) / 64, tn = (mp + 127) / 128;
   const int Kl = ((K + kBK - 1) / kBK) * kBK;
   OperandDesc a{Y, tpad, P, tpad};
   OperandDesc b{Lneg, tpad, mp, tpad};
   SketchCorrEpi epi{d, n, B_in, B_out, phys, P, mp, k};
+  // one tile row covering all P sketch rows when P <= 144 (no padded MMA rows beyond a multiple
+  // of 48); 64-wide column tiles.  SketchCorrEpi::prepare rescales tiles_n for N = 64 below.
+  auto one_row = [&](auto bm_tag) -> cudaError_t {
+    constexpr int BM = decltype(bm_tag)::value;
+    const int64_t tn = (mp + 63) / 64;
+    ColMajorRectMap map{tn, 1, BM, 64};
+    dmma_gemm_kernel<BM, 64, kRectStages, 2, ColMajorRectMap, SketchCorrEpi>
+        <<<(unsigned)tn, kGemmThreads, gemm_smem_bytes<BM, 64, kRectStages>(), st>>>(a, b, Kl, map, epi);
+    return cudaGetLastError();
+  };
+  if (P <= 48) return one_row(std::integral_constant<int, 48>{});
+  if (P <= 96) return one_row(std::integral_constant<int, 96>{});
+  if (P <= 144) return one_row(std::integral_constant<int, 144>{});
+  const int64_t tm = (P + 63) / 64, tn = (mp + 127) / 128;
   ColMajorRectMap map{tn, tm, 64, 128};
   dmma_gemm_kernel<64, 128, kRectStages, 2, ColMajorRectMap, SketchCorrEpi>
       <<<(unsigned)(tm * tn), kGemmThreads, gemm_smem_bytes<64, 128, kRectStages>(), st>>>(a, b, Kl, map, epi);
