@@ -309,69 +309,12 @@ __global__ void __launch_bounds__(kPanelThreads, 1) panel_kernel(PanelParams pin
       }
       myn2x = myn2;
     };
-    // Householder reflector (vv over rows [jj, P), coef, skip) applied to the own column, then the
-    // residual-norm downdate.  Residual norms are downdated (|r|^2 -= y^2) and recomputed exactly
-    // whenever cancellation could cost more than ~1e-10 relative accuracy (LAPACK xLAQP2 policy).
-    auto reflect_own = [&](const double* vv, int jj, double coef, int skip) {
-      double yj;
-      if (!skip) {
-        double d0 = 0.0, d1 = 0.0, d2 = 0.0, d3 = 0.0;
-#pragma unroll
-        for (int r = 0; r < kRegRows; r += 4) {
-          if (r >= jj && r < PRr) d0 = __fma_rn(vv[r], rg[r], d0);
-          if (r + 1 >= jj && r + 1 < PRr) d1 = __fma_rn(vv[r + 1], rg[r + 1], d1);
-          if (r + 2 >= jj && r + 2 < PRr) d2 = __fma_rn(vv[r + 2], rg[r + 2], d2);
-          if (r + 3 >= jj && r + 3 < PRr) d3 = __fma_rn(vv[r + 3], rg[r + 3], d3);
-        }
-        int r = max(jj, PRr);
-        const double* bc = Bs + (size_t)(r - PRr) * Rs + tid;
-#pragma unroll 2
-        for (; r + 4 <= P; r += 4, bc += 4 * Rs) {
-          d0 = __fma_rn(vv[r], bc[0], d0);
-          d1 = __fma_rn(vv[r + 1], bc[Rs], d1);
-          d2 = __fma_rn(vv[r + 2], bc[2 * Rs], d2);
-          d3 = __fma_rn(vv[r + 3], bc[3 * Rs], d3);
-        }
-        for (; r < P; ++r, bc += Rs) d0 = __fma_rn(vv[r], bc[0], d0);
-        const double wv = __dmul_rn(coef, __dadd_rn(__dadd_rn(d0, d1), __dadd_rn(d2, d3)));
-#pragma unroll
-        for (int r2 = 0; r2 < kRegRows; ++r2)
-          if (r2 >= jj && r2 < PRr) rg[r2] = __fma_rn(-vv[r2], wv, rg[r2]);
-        r = max(jj, PRr);
-        double* bw = Bs + (size_t)(r - PRr) * Rs + tid;
-        // batched: all loads of a group before its stores (smem aliasing would
-        // otherwise serialise every element on the load latency)
-        for (; r + 8 <= P; r += 8, bw += 8 * Rs) {
-          double x[8], vl[8];
-#pragma unroll
-          for (int u = 0; u < 8; ++u) {
-            x[u] = bw[u * Rs];
-            vl[u] = vv[r + u];
-          }
-#pragma unroll
-          for (int u = 0; u < 8; ++u) bw[u * Rs] = __fma_rn(-vl[u], wv, x[u]);
-        }
-        for (; r < P; ++r, bw += Rs) *bw = __fma_rn(-vv[r], wv, *bw);
-      }
-      if (jj < PRr) {
-        yj = 0.0;
-#pragma unroll
-        for (int r2 = 0; r2 < kRegRows; ++r2)
-          if (r2 == jj) yj = rg[r2];
-      } else {
-        yj = Bs[(jj - PRr) * Rs + tid];
-      }
-      const double n2 = __fma_rn(-yj, yj, myn2);
-      if (exact_only || !(n2 > 1e-6 * myn2x) || !(n2 > 1e-280)) {
-        exact_norm(jj + 1);
-      } else {
-        myn2 = n2;
-        myn = sqrt(n2);
-      }
-    };
-    // Fused variant (register mode): the pending reflector (vp, wpend) of the previous step is
-    // applied to the smem rows while forming this step's dot, and this step's reflector becomes
-    // the pending one.  Values are bit-identical to reflect_own applied step by step.
+    // Householder reflector (vc over rows [jj, P), coef, skip) applied to the own column, then the
+    // residual-norm downdate (|r|^2 -= y^2, recomputed exactly whenever cancellation could cost
+    // more than ~1e-10 relative accuracy: LAPACK xLAQP2 policy).  Register mode: the pending
+    // reflector (vp, wpend) of the previous step is applied to the smem rows while forming this
+    // step's dot, and this step's reflector becomes the pending one -- one smem pass per step,
+    // values bit-identical to applying each reflector eagerly.
     auto reflect_fused = [&](const double* vc, const double* vp, int jj, double coef, int skip) {
       double d0 = 0.0, d1 = 0.0, d2 = 0.0, d3 = 0.0;
       if (!skip) {
