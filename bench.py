@@ -67,6 +67,21 @@ def workload_name(a):
             f"P=b+{a.p - a.b}={a.p} sketch rows, seed={a.seed}")
 
 
+def ncu_traffic(kernel: str, detail: bool = False):
+    """DRAM bytes (read + write) of one profiled launch of `kernel` from the committed ncu summary
+    (profiles/r01_ncu_traffic.json); with detail, the launch it refers to and its algorithmic bytes."""
+    path = Path(__file__).resolve().parent / "profiles" / "r01_ncu_traffic.json"
+    try:
+        rec = json.loads(path.read_text())[kernel]
+    except (OSError, KeyError, ValueError):
+        return None
+    total = rec["dram_read_bytes"] + rec["dram_write_bytes"]
+    if not detail:
+        return total
+    return {k: rec[k] for k in rec if k not in ("dram_read_bytes", "dram_write_bytes")} | {
+        "dram_bytes": total, "source": "profiles/r01_ncu_traffic.json (ncu --set full, one launch)"}
+
+
 def cfg_dict(a, world: int = 1):
     return {"workload": workload_name(a), "n": a.n, "b": a.b, "q": a.b, "p_sketch": a.p,
             "oversampling": a.p - a.b,
@@ -321,7 +336,8 @@ def run_b200(args, rank: int, world: int, local_rank: int):
         "roofline": {"bound": "tensor", "kernel": "schur_ws_kernel (trailing Schur update, DMMA.8x8x4)",
                      "achieved": achieved, "peak": FP64_PEAK_GFLOPS / 1e3, "unit": "TFLOP/s",
                      "frac": (achieved / (FP64_PEAK_GFLOPS / 1e3)) if achieved else None,
-                     "traffic": None,
+                     "traffic": ncu_traffic("schur_ws_kernel"),
+                     "traffic_launch": ncu_traffic("schur_ws_kernel", detail=True),
                      "algorithmic": "sum over panels of t*m*(m+1) flops (lower-triangle rank-t update)"
                                     + (" (rank 0's share of the tiles; achieved over its Schur time)" if world > 1
                                        else ""),
