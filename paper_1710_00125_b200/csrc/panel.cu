@@ -175,6 +175,12 @@ __global__ void __launch_bounds__(kPanelThreads, 1) panel_kernel(PanelParams pin
   const int64_t n = p.n;
   const int k0 = p.k0, P = p.P, R = p.R, G = p.G, Wn = p.Wn;
   const size_t QS = qcol_stride(P);  // LL words per candidate-column buffer
+#ifndef RCP_REDUCER_LAST
+#define RCP_REDUCER_LAST 1
+#endif
+  // Reducer CTA of every exchange.  The last CTA owns the fewest rows (m - (G-1) R), so it tends
+  // to publish its record first and starts reducing earliest.
+  const int kRed = RCP_REDUCER_LAST ? G - 1 : 0;
   const int m0 = static_cast<int>(n - k0);
   const int r0 = cta * R;
   const int rcnt = max(0, min(R, m0 - r0));
@@ -511,7 +517,7 @@ __global__ void __launch_bounds__(kPanelThreads, 1) panel_kernel(PanelParams pin
       // ---- reducer CTA 0: winner over all records -> a 6-word decision pushed into every CTA's
       //      mailbox (winner CTA, position, column, coef, flags); every CTA then reads v from
       //      the winner's buffer.
-      if (cta == 0) {
+      if (cta == kRed) {
         double gk = -1.0;
         long long gi = LLONG_MAX;
         int gs = -1;
@@ -548,7 +554,7 @@ __global__ void __launch_bounds__(kPanelThreads, 1) panel_kernel(PanelParams pin
         if (s_abort) hw[3] = 4u;
         for (int f = tid; f < G * 4; f += nthr) {
           const int c = f >> 2, u = f & 3;
-          if (c != 0) ll_put(p.qdll + ((size_t)pb * G + c) * kMWords + u, tag, hw[u]);
+          if (c != kRed) ll_put(p.qdll + ((size_t)pb * G + c) * kMWords + u, tag, hw[u]);
         }
         if (tid == 0) {
           s_wcta = static_cast<int>(hw[0]);
@@ -779,7 +785,7 @@ __global__ void __launch_bounds__(kPanelThreads, 1) panel_kernel(PanelParams pin
         }
         seq = nseq1;
         __syncthreads();  // records out before anyone polls
-        if (cta == 0) {
+        if (cta == kRed) {
           double gk = -1.0;
           long long gi = LLONG_MAX;
           int gs = -1, gph = -1;
@@ -821,7 +827,7 @@ __global__ void __launch_bounds__(kPanelThreads, 1) panel_kernel(PanelParams pin
           if (s_abort) hw[3] |= 4u;
           for (int f = tid; f < G * 4; f += nthr) {
             const int c = f >> 2, u = f & 3;
-            if (c != 0) ll_put(p.qdll + ((size_t)pb1 * G + c) * kMWords + u, tag1, hw[u]);
+            if (c != kRed) ll_put(p.qdll + ((size_t)pb1 * G + c) * kMWords + u, tag1, hw[u]);
           }
           if (tid == 0) {
             s_gs1 = static_cast<int>(hw[0]);
@@ -944,7 +950,7 @@ __global__ void __launch_bounds__(kPanelThreads, 1) panel_kernel(PanelParams pin
 
     // ---- reducer CTA 0 reads all records and pushes the decision inputs (12 LL words) into
     //      every CTA's mailbox
-    if (cta == 0) {
+    if (cta == kRed) {
       double gk = -1.0;
       long long gi = LLONG_MAX;
       int gs = -1;
@@ -1001,7 +1007,7 @@ __global__ void __launch_bounds__(kPanelThreads, 1) panel_kernel(PanelParams pin
 #else
         for (int f = tid; f < G * 12; f += nthr) {
           const int c = f / 12, u = f - c * 12;
-          if (c != 0) ll_put(p.sdll + ((size_t)pb * G + c) * kMWords + u, tag, hw[u]);
+          if (c != kRed) ll_put(p.sdll + ((size_t)pb * G + c) * kMWords + u, tag, hw[u]);
         }
 #endif
       }
