@@ -22,8 +22,9 @@ this restatement against them bit-for-bit (perm, pattern, L, D, x).  The
 restatement issues the same NumPy/SciPy primitives in the same order as the
 reference, so OpenBLAS rounding is reproduced exactly on the same machine.
 
-Out of scope here: the BKPP/BBK strategies,
-``track_growth="full"`` snapshots and ``audit_sketch`` drift records.
+The Bunch-Kaufman partial-pivoting (``bkpp``) and rook (``bbk``) strategies run on the
+same engine without a sketch (pivot.py:131-225).
+Out of scope here: ``track_growth="full"`` snapshots and ``audit_sketch`` drift records.
 """
 
 from __future__ import annotations
@@ -36,6 +37,7 @@ from scipy.linalg import solve_triangular
 
 EPS = float(np.finfo(np.float64).eps)          # factor.py:91
 ALPHA = math.sqrt(2.0) / 2.0                   # pivot.py:44 (SBKP_ALPHA)
+BK_ALPHA = (1.0 + math.sqrt(17.0)) / 8.0       # pivot.py:47 (bkpp / bbk)
 
 PAT_SINGLE, PAT_PAIR_START, PAT_PAIR_END, PAT_DEFICIENT = 0, 1, 2, 3   # factor.py:94-97
 
@@ -48,8 +50,9 @@ class OracleNumericalError(RuntimeError):
 
 @dataclass
 class OracleConfig:
-    """Knobs of ``FactorConfig`` used by the rcp path (factor.py:116-149)."""
+    """Knobs of ``FactorConfig`` used by the path (factor.py:116-149)."""
 
+    strategy: str = "rcp"
     p: int = 5
     b: int = 64
     q: int = 1
@@ -61,6 +64,8 @@ class OracleConfig:
             raise ValueError("bad config")
         if self.q not in (1, self.b) or self.p < self.q:
             raise ValueError("bad q/p")
+        if self.strategy not in ("rcp", "bkpp", "bbk"):
+            raise ValueError("bad strategy")
 
 
 @dataclass
@@ -210,7 +215,7 @@ def _multipliers(c0, c1):
 # --------------------------------------------------------------------------- engine
 
 class _State:
-    """Mutable factorization state; mirrors _Engine (factor.py:273-634) for strategy rcp."""
+    """Mutable factorization state; mirrors _Engine (factor.py:273-634)."""
 
     def __init__(self, a: np.ndarray, cfg: OracleConfig, normal_source=None):
         a = np.asarray(a, dtype=np.float64)
@@ -238,11 +243,14 @@ class _State:
         self.t = 0
         self.W = np.zeros((0, 0))
         self.P = cfg.p
+        self.rcp = cfg.strategy == "rcp"
+        self.alpha = ALPHA if self.rcp else BK_ALPHA                       # factor.py:299
         # One generator per factorization, advancing across recomputes (sketch.py:63-84).
         self.gen = normal_source or np.random.Generator(np.random.Philox(cfg.seed))
-        self.B = self.gen.standard_normal((cfg.p, n)) @ self.A            # factor.py:307-309
+        # factor.py:306-310: only rcp draws a sketch
+        self.B = self.gen.standard_normal((cfg.p, n)) @ self.A if self.rcp else np.zeros((cfg.p, 0))
         self.recomputes = 0
-        self.armed = cfg.robust_r >= 1                                     # factor.py:314
+        self.armed = self.rcp and cfg.robust_r >= 1                        # factor.py:314
         self.delta = 1.0 / cfg.robust_r if self.armed else 0.0
         self.thr = EPS ** self.delta if self.armed else 0.0
         self.beta = float(col_norms(self.B).max()) if (self.armed and self.B.size) else 0.0
@@ -259,7 +267,8 @@ class _State:
         if self.W.size:
             a, b = i - self.k0, j - self.k0
             self.W[[a, b], :] = self.W[[b, a], :]
-        self.B[:, [i, j]] = self.B[:, [j, i]]
+        if self.rcp:
+            self.B[:, [i, j]] = self.B[:, [j, i]]
         self.perm[[i, j]] = self.perm[[j, i]]
 
     # -- left-looking column formation ---------------------------------------
@@ -304,6 +313,62 @@ class _State:
             return ONE_SWAP, 1, r
         return TWO, 2, r
 
+    def _scan(self, v: np.ndarray):
+        """Max and its first index, charging the scan's comparisons (pivot.py:80-84)."""
+        self.cnt.comps += max(v.size - 1, 0)
+        j = int(np.argmax(v))
+        return float(v[j]), j
+
+    def bkpp(self):
+        """Classic Bunch-Kaufman partial pivoting on the leading column (pivot.py:146-171)."""
+        k = self.k
+        c = self.column(k)
+        sub = np.abs(c[1:])
+        lam, j = self._scan(sub) if sub.size else (0.0, 0)
+        if sub.size == 0 or lam == 0.0:
+            return SKIP, 1, None, None
+        r = k + 1 + j
+        a_kk = float(c[0])
+        if abs(a_kk) >= self.alpha * lam:
+            return ONE, 1, None, None
+        col_r = self.column(r)
+        absr = np.abs(col_r)
+        mask = np.ones(absr.size, dtype=bool)
+        mask[r - k] = False
+        sigma, _ = self._scan(absr[mask])
+        a_rr = float(col_r[r - k])
+        if abs(a_kk) * sigma >= self.alpha * lam * lam:
+            return ONE, 1, None, None
+        if abs(a_rr) >= self.alpha * sigma:
+            return ONE_SWAP, 1, r, None
+        return TWO, 2, r, None
+
+    def bbk(self):
+        """Rook search (bounded Bunch-Kaufman) on the leading column (pivot.py:189-218)."""
+        k, n = self.k, self.n
+        c = self.column(k)
+        sub = np.abs(c[1:])
+        lam, j = self._scan(sub) if sub.size else (0.0, 0)
+        if sub.size == 0 or lam == 0.0:
+            return SKIP, 1, None, None
+        if abs(float(c[0])) >= self.alpha * lam:
+            return ONE, 1, None, None
+        p_idx, imax, colmax = k, k + 1 + j, lam
+        for _ in range(n - k):
+            col = self.column(imax)
+            absc = np.abs(col)
+            mask = np.ones(absc.size, dtype=bool)
+            mask[imax - k] = False
+            offsets = np.nonzero(mask)[0]
+            rowmax, local = self._scan(absc[mask])
+            jmax = k + int(offsets[local])
+            if abs(float(col[imax - k])) >= self.alpha * rowmax:
+                return ONE_SWAP, 1, imax, None
+            if jmax == p_idx or rowmax <= colmax:
+                return TWO, 2, imax, (None if p_idx == k else p_idx)
+            p_idx, imax, colmax = imax, jmax, rowmax
+        raise AssertionError("rook search failed to terminate")
+
     # -- elimination ----------------------------------------------------------
     def eliminate(self, kind: str, s: int) -> None:
         """Multipliers, checks and writes for one pivot block (factor.py:449-489)."""
@@ -316,7 +381,7 @@ class _State:
         if s == 2:
             d21 = abs(float(dblk[1, 0]))
             det = float(dblk[0, 0]) * float(dblk[1, 1]) - d21 * d21
-            if abs(det) < (1.0 - ALPHA * ALPHA) * d21 * d21 * (1.0 - 1e-12):
+            if abs(det) < (1.0 - self.alpha * self.alpha) * d21 * d21 * (1.0 - 1e-12):
                 raise OracleNumericalError(f"2x2 block at step {k} violates its determinant bound")
         self.L[k + s:, k:k + s] = lc
         self.W[k - self.k0:, self.t] = c0
@@ -335,7 +400,7 @@ class _State:
                 self.cnt.divs += 2 * w
                 self.cnt.mults += 4 * w + 2
                 self.cnt.adds += 2 * w + 1
-        if self.cfg.q == 1 and w > 0:                              # per-step sketch downdate
+        if self.rcp and self.cfg.q == 1 and w > 0:                 # per-step sketch downdate
             self.B[:, k + s:] -= self.B[:, k:k + s] @ lc.T
             self.cnt.mults += s * self.P * w
             self.cnt.adds += s * self.P * w
@@ -410,7 +475,7 @@ class _State:
         """One pivot decision + elimination inside a panel (factor.py:602-634)."""
         k, n, t = self.k, self.n, self.t
         m = n - k
-        if self.cfg.q == 1 and m > 1:
+        if self.rcp and self.cfg.q == 1 and m > 1:
             nr = col_norms(self.B, start=k)
             self.cnt.comps += m - 1
             self.cnt.mults += self.P * (m - 1)
@@ -424,14 +489,23 @@ class _State:
                     return "stop"
                 jl = int(np.argmax(col_norms(self.B, start=k)))
             self.exchange(k, k + jl)
-        kind, s, r = self.sbkp()
+        pre = None
+        if self.rcp:
+            kind, s, r = self.sbkp()
+        elif self.cfg.strategy == "bkpp":
+            kind, s, r, pre = self.bkpp()
+        else:
+            kind, s, r, pre = self.bbk()
         if s == 2 and t > 0 and t + 2 > width:
             return "defer"
         self.trace.append((k, kind, r))
         if kind == ONE_SWAP:
             self.exchange(k, r)
-        elif kind == TWO and r != k + 1:
-            self.exchange(k + 1, r)
+        elif kind == TWO:
+            if pre is not None:                                     # factor.py:628-629
+                self.exchange(k, pre)
+            if r != k + 1:
+                self.exchange(k + 1, r)
         self.eliminate(kind, s)
         self.k += s
         self.t += s
@@ -444,7 +518,7 @@ class _State:
         width = min(self.cfg.b, n - self.k0)
         self.t = 0
         self.W = np.zeros((n - self.k0, min(width + 1, n - self.k0)))
-        if self.cfg.q > 1:
+        if self.rcp and self.cfg.q > 1:
             if self.preselect(width) == "stop":
                 self.W = np.zeros((0, 0))
                 return
@@ -452,7 +526,7 @@ class _State:
             if self.step(width) != "ok":
                 break
         self.flush_panel()
-        if self.cfg.q > 1 and self.t > 0 and self.k < n:
+        if self.rcp and self.cfg.q > 1 and self.t > 0 and self.k < n:
             k0, k = self.k0, self.k
             z = solve_triangular(self.L[k0:k, k0:k], self.L[k:, k0:k].T,
                                  lower=True, unit_diagonal=True, trans="T")
