@@ -72,12 +72,21 @@ enum {
   RCP_NUM_DET_BOUND = 4        /* "2x2 block at step {k} violates its determinant bound" */
 };
 
-/* Mirror of the rcp-relevant FactorConfig fields (factor.py:116-135). */
+/* Pivoting strategy (reference Strategy, factor.py:104-113; pivot.py). */
+enum {
+  RCP_STRATEGY_RCP = 0,   /* randomized complete pivoting: sketch + SBKP rule (the BASELINE path) */
+  RCP_STRATEGY_BKPP = 1,  /* Bunch-Kaufman partial pivoting (pivot.py:146-171), no sketch         */
+  RCP_STRATEGY_BBK = 2    /* rook / bounded Bunch-Kaufman (pivot.py:189-218), no sketch           */
+};
+
+/* Mirror of the engine-relevant FactorConfig fields (factor.py:116-135).  Zero-initialised
+ * trailing fields select the defaults (strategy rcp). */
 typedef struct rcp_config {
   int32_t p;          /* sketch rows (reference FactorConfig.p)                */
   int32_t b;          /* panel width                                            */
   int32_t q;          /* 1 or b                                                 */
   int32_t robust_r;   /* recompute budget exponent; 0 disables the guard        */
+  int32_t strategy;   /* RCP_STRATEGY_*                                         */
 } rcp_config;
 
 /* Mirror of GrowthStats' engine-produced fields (metrics.py:47-65, factor.py:514-527)

@@ -59,7 +59,8 @@ class NativeUnavailable(RuntimeError):
 
 
 class RcpConfig(ctypes.Structure):
-    _fields_ = [("p", ctypes.c_int32), ("b", ctypes.c_int32), ("q", ctypes.c_int32), ("robust_r", ctypes.c_int32)]
+    _fields_ = [("p", ctypes.c_int32), ("b", ctypes.c_int32), ("q", ctypes.c_int32), ("robust_r", ctypes.c_int32),
+                ("strategy", ctypes.c_int32)]
 
 
 class RcpStats(ctypes.Structure):

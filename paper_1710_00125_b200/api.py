@@ -179,9 +179,18 @@ def _require_square(a: np.ndarray, name: str = "A") -> np.ndarray:
     return a
 
 
-def _check_supported(cfg: FactorConfig) -> None:
-    if cfg.strategy is not Strategy.RCP:
-        raise ValueError(f"strategy {cfg.strategy.value!r} is not part of the B200 build (rcp only)")
+_STRATEGY_CODE = {Strategy.RCP: 0, Strategy.BKPP: 1, Strategy.BBK: 2}  # rcp_b200.h RCP_STRATEGY_*
+
+
+def _native_config(cfg: FactorConfig) -> _native.RcpConfig:
+    return _native.RcpConfig(cfg.p, cfg.b, cfg.q, cfg.robust_r, _STRATEGY_CODE[cfg.strategy])
+
+
+def _check_supported(cfg: FactorConfig, batched: bool = False) -> None:
+    if cfg.strategy is Strategy.BBK:
+        raise ValueError("strategy 'bbk' is not part of the B200 build (rcp and bkpp are)")
+    if batched and cfg.strategy is not Strategy.RCP:
+        raise ValueError(f"the batched kernel runs strategy 'rcp' only, got {cfg.strategy.value!r}")
     if cfg.track_growth is GrowthTracking.FULL or cfg.audit_sketch:
         raise ValueError("track_growth='full' / audit_sketch diagnostics are not part of the B200 build")
 
@@ -311,7 +320,7 @@ def _config(cfg: FactorConfig | None, overrides: dict) -> FactorConfig:
 
 def workspace_bytes(n: int, cfg: FactorConfig) -> int:
     lib = _native.load()
-    c = _native.RcpConfig(cfg.p, cfg.b, cfg.q, cfg.robust_r)
+    c = _native_config(cfg)
     return int(lib.rcp_workspace_bytes(n, ctypes.byref(c)))
 
 
@@ -343,12 +352,14 @@ def factor_device(a: torch.Tensor, cfg: FactorConfig | None = None, *, omega: to
     lda = a.stride(0) if a.stride(1) == 1 else a.stride(1)
     dev = a.device
     normals = _NormalStream(cfg.seed)
-    if omega is None:
+    if cfg.strategy is not Strategy.RCP:
+        omega = None  # bkpp / bbk draw no sketch (factor.py:306-310)
+    elif omega is None:
         omega = torch.from_numpy(normals.first(cfg.p, n)).to(dev)
     else:
         normals.skip_first(cfg.p, n)  # advance past the supplied first draw when needed
         omega = omega.contiguous()
-    c = _native.RcpConfig(cfg.p, cfg.b, cfg.q, cfg.robust_r)
+    c = _native_config(cfg)
     need = int(lib.rcp_workspace_bytes(n, ctypes.byref(c)))
     if isinstance(workspace, tuple):
         ws_ptr, ws_bytes = int(workspace[0]), int(workspace[1])
@@ -376,7 +387,7 @@ def factor_device(a: torch.Tensor, cfg: FactorConfig | None = None, *, omega: to
         out.trace_r = torch.empty(n, dtype=torch.int32, device=dev)
     st = _native.RcpStats()
     status = lib.rcp_factor_dist(
-        ctypes.byref(c), n, a.data_ptr(), lda, omega.data_ptr(), normals.cfunc, None,
+        ctypes.byref(c), n, a.data_ptr(), lda, 0 if omega is None else omega.data_ptr(), normals.cfunc, None,
         ws_ptr, ws_bytes, out.perm.data_ptr(), out.L.data_ptr(),
         out.d_diag.data_ptr(), out.d_off.data_ptr(), out.pattern.data_ptr(),
         _ptr(out.trace_kind if trace else None), _ptr(out.trace_r if trace else None),

@@ -80,7 +80,7 @@ class BatchedDeviceFactorization:
 
 
 def _cfg_struct(cfg: FactorConfig) -> _native.RcpConfig:
-    return _native.RcpConfig(cfg.p, cfg.b, cfg.q, cfg.robust_r)
+    return _native.RcpConfig(cfg.p, cfg.b, cfg.q, cfg.robust_r, 0)
 
 
 def batched_workspace_bytes(n: int, cfg: FactorConfig) -> int:
@@ -120,7 +120,7 @@ def factor_batched_device(a: torch.Tensor, cfg: FactorConfig | None = None, *, n
     exhaust the pre-drawn normal stream are re-run through :func:`factor_device`.
     """
     cfg = _config(cfg, overrides)
-    _check_supported(cfg)
+    _check_supported(cfg, batched=True)
     lib = _native.load()
     if a.dim() != 3 or a.shape[1] != a.shape[2]:
         raise ValueError(f"expected a [count, n, n] stack, got shape {tuple(a.shape)}")

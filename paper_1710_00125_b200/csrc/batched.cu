@@ -1057,6 +1057,7 @@ int rcp_factor_batched(const rcp_config* cfg, int64_t count, int64_t n, const do
   if (cfg->p < 1 || cfg->b < 1 || cfg->robust_r < 0 || cfg->p < cfg->q) return RCP_ERR_INVALID_ARG;
   if (!(cfg->q == 1 || cfg->q == cfg->b)) return RCP_ERR_INVALID_ARG;
   if (n > BT || cfg->b > kMaxB || cfg->p > 64 || cfg->q == 1) return RCP_ERR_UNSUPPORTED;
+  if (cfg->strategy != RCP_STRATEGY_RCP) return RCP_ERR_UNSUPPORTED;  // batched kernel: rcp only
   if (count > INT_MAX || normals_len < (int64_t)cfg->p * n) return RCP_ERR_INVALID_ARG;
   if (count == 0) return RCP_OK;
   const size_t need = rcp_batched_workspace_bytes(n, cfg);

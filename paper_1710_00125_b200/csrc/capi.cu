@@ -102,6 +102,7 @@ WorkerBufs carve_worker(unsigned char* b, int64_t n, const Layout& L) {
 int validate_cfg(const rcp_config* c, int64_t n) {
   if (!c || n < 1) return RCP_ERR_INVALID_ARG;
   if (c->p < 1 || c->b < 1 || c->robust_r < 0) return RCP_ERR_INVALID_ARG;
+  if (c->strategy < RCP_STRATEGY_RCP || c->strategy > RCP_STRATEGY_BKPP) return RCP_ERR_INVALID_ARG;
   if (!(c->q == 1 || c->q == c->b)) return RCP_ERR_INVALID_ARG;
   if (c->p < c->q) return RCP_ERR_INVALID_ARG;
   if (n > (int64_t)INT_MAX / 2) return RCP_ERR_INVALID_ARG;
@@ -170,7 +171,9 @@ int rcp_factor_dist(const rcp_config* cfg, int64_t n, const double* a, int64_t l
   }
   int vc = validate_cfg(cfg, n);
   if (vc != RCP_OK) return vc;
-  if (lda < n || !a || !omega_dev || !perm || !Lout || !d_diag || !d_off || !pattern) return RCP_ERR_INVALID_ARG;
+  const bool rcp_strat = cfg->strategy == RCP_STRATEGY_RCP;  // bkpp / bbk: no sketch (factor.py:306)
+  if (lda < n || !a || (rcp_strat && !omega_dev) || !perm || !Lout || !d_diag || !d_off || !pattern)
+    return RCP_ERR_INVALID_ARG;
   const rcp_config c = *cfg;
   const Layout Lay = make_layout(n, c);
   if (!workspace || workspace_bytes < Lay.total) return RCP_ERR_WORKSPACE;
@@ -274,8 +277,8 @@ int rcp_factor_dist(const rcp_config* cfg, int64_t n, const double* a, int64_t l
   const double amax = hscal->amax;
 
   // ---- sketch B = Omega A (factor.py:307-309) and guard setup (factor.py:314-317)
-  RCP_LAUNCH(launch_sketch_gemm(P, n, omega_dev, n, A[0], n, B[0], 0, st));
-  const bool armed = c.robust_r >= 1;
+  if (rcp_strat) RCP_LAUNCH(launch_sketch_gemm(P, n, omega_dev, n, A[0], n, B[0], 0, st));
+  const bool armed = rcp_strat && c.robust_r >= 1;  // factor.py:314
   double delta = armed ? 1.0 / c.robust_r : 0.0;
   double thr = armed ? std::pow(DBL_EPSILON, delta) : 0.0;
   double beta = 0.0;
@@ -306,7 +309,8 @@ int rcp_factor_dist(const rcp_config* cfg, int64_t n, const double* a, int64_t l
   // ---- panel loop, device driven (see PanelDesc): the host enqueues panels back to back
   // and reads their outcome only once per batch; guard events and errors stop the device
   // chain, the host rolls back to that panel and handles them.
-  const bool q1 = (c.q == 1);
+  const bool q1 = rcp_strat && (c.q == 1);
+  const int q_eff = rcp_strat ? c.q : 0;  // no sketch selection outside rcp (factor.py:548, 608)
   const int sms_cap = std::min(num_sms, kMaxSMs);
   // launch grid: the largest G any panel can ask for (G(m0) is not monotone in m0); CTAs
   // beyond a panel's own G return at once
@@ -336,7 +340,8 @@ int rcp_factor_dist(const rcp_config* cfg, int64_t n, const double* a, int64_t l
   PanelParams base{};
   base.n = n;
   base.P = P;
-  base.alpha = std::sqrt(2.0) / 2.0;
+  base.alpha = rcp_strat ? std::sqrt(2.0) / 2.0 : (1.0 + std::sqrt(17.0)) / 8.0;  // factor.py:299
+  base.strategy = c.strategy;
   base.q1 = q1 ? 1 : 0;
   base.qscr = dptr(Lay.qscr);
   base.Lbuf = Lbuf;
@@ -356,7 +361,7 @@ int rcp_factor_dist(const rcp_config* cfg, int64_t n, const double* a, int64_t l
   base.qdll = reinterpret_cast<unsigned long long*>(ws + Lay.qdec);
   base.st = dstate;
   base.b = c.b;
-  base.q = c.q;
+  base.q = q_eff;
   base.num_sms = sms_cap;
   base.smem_budget = smem_budget;
 
@@ -377,7 +382,7 @@ int rcp_factor_dist(const rcp_config* cfg, int64_t n, const double* a, int64_t l
       RCP_CHECK(cudaEventRecord(ep.a, st));
       RCP_LAUNCH(launch_panel(prm, gmax, (size_t)smem_budget, st));
       RCP_CHECK(cudaEventRecord(ep.b, st));
-      RCP_LAUNCH(launch_panel_commit(din, dout, dplog, dstate, n, c.b, c.q, P, (long long)Lay.snap_cap, st));
+      RCP_LAUNCH(launch_panel_commit(din, dout, dplog, dstate, n, c.b, q_eff, P, (long long)Lay.snap_cap, st));
       RCP_LAUNCH(launch_gather(n, 0, 0, 0, tpad, 0, pol, Lbuf, W, permb[pcur], permb[pcur ^ 1], snap, phys, Lneg, Wg,
                                L11c, st, din));
       EventPair& es = new_pair(ev_schur);
@@ -392,7 +397,7 @@ int rcp_factor_dist(const rcp_config* cfg, int64_t n, const double* a, int64_t l
       RCP_LAUNCH(launch_schur_update(n, 0, 0, Lneg, Wg, tpad, 0, A[curA], phys, A[curA ^ 1], st, din, 0, world));
       RCP_CHECK(cudaEventRecord(es.b, st));
       if (world > 1) RCP_LAUNCH(launch_dist_wait_done(dsh, world, dseq, st));
-      if (!q1) {  // sketch correction once per panel (factor.py:554-565)
+      if (rcp_strat && !q1) {  // sketch correction once per panel (factor.py:554-565)
         RCP_LAUNCH(launch_ysolve(n, P, 0, c.b, tpad, pol, B[curB], L11c, Y, st, din));
         RCP_LAUNCH(launch_sketch_correction(P, n, 0, Y, tpad, c.b, Lneg, B[curB], phys, B[curB ^ 1], st, din, n));
       }
@@ -534,7 +539,7 @@ int rcp_factor_dist(const rcp_config* cfg, int64_t n, const double* a, int64_t l
       const int t = lg.k_end - lg.k0;
       const long long mp = n - lg.k_end;
       const int m0 = lg.m0;
-      if (!q1 && m0 > 1) {  // preselect norms (factor.py:576-577)
+      if (rcp_strat && !q1 && m0 > 1) {  // preselect norms (factor.py:576-577)
         h_mul += (long long)P * (m0 - 1);
         h_add += (long long)P * (m0 - 1);
         h_cmp += m0 - 1;
@@ -548,7 +553,7 @@ int rcp_factor_dist(const rcp_config* cfg, int64_t n, const double* a, int64_t l
         schur_flops += (double)t * (double)mp * (double)(mp + 1);
         h_mul += (long long)t * (mp * (mp + 1) / 2);  // _apply_trailing (factor.py:377-378)
         h_add += (long long)t * (mp * (mp + 1) / 2);
-        if (!q1) {
+        if (rcp_strat && !q1) {
           h_mul += (long long)t * P * mp + (long long)(t * (t - 1) / 2) * mp;
           h_add += (long long)t * P * mp + (long long)(t * (t - 1) / 2) * mp;
         }

@@ -220,6 +220,8 @@ __global__ void __launch_bounds__(kPanelThreads, 1) panel_kernel(PanelParams pin
   __shared__ XRec s_win;
   __shared__ unsigned s_qhdr[8], s_dhdr[12];
   __shared__ int s_wpos, s_qflags, s_hascand, s_wcta, s_gs1, s_gs2;
+  __shared__ double s_bkarr;  // bkpp: a_rr of the partner column
+  __shared__ int s_bkhas;
 
   for (int x = tid; x < Wn; x += nthr) win[x] = x;
   for (int i = tid; i < rcnt; i += nthr) lpos[i] = r0 + i;
@@ -1062,15 +1064,121 @@ __global__ void __launch_bounds__(kPanelThreads, 1) panel_kernel(PanelParams pin
       pr = s_win.phys;
     }
 
-    // ---- SBKP decision (pivot.py:111-128): 0 skip, 1 1x1, 2 1x1-swap, 3 2x2
-    int kind, s;
     const double athr = __dmul_rn(alpha, lam);
+    // ---- BKPP (pivot.py:146-171): when the 1x1 test fails, form column r in every CTA and find
+    //      sigma = max_{i != r} |c_r(i)| with a second exchange; a_rr comes from r's owner.
+    bool cr_done = false;
+    double sigma = 0.0;
+    if (p.strategy == 1 && has_cand && lam != 0.0 && !(fabs(akk) >= athr)) {
+      for (int s2 = tid; s2 < t; s2 += nthr) wrrow[s2] = __ldcg(p.W + (k0 + pr) + (int64_t)s2 * n);
+      const double av0 = (tid < rcnt) ? sym_at(A, n, k0 + r0 + tid, k0 + pr) : 0.0;
+      if (tid == 0) s_bkhas = 0;
+      __syncthreads();  // wrrow ready
+      double sk = -1.0;
+      long long si = LLONG_MAX;
+      int ss = -1;
+      for (int i = tid; i < rcnt; i += nthr) {
+        const double a_ip = (i == tid) ? av0 : sym_at(A, n, k0 + r0 + i, k0 + pr);
+        const int lp = lpos[i];
+        if (lp < t) continue;
+        const int64_t row = k0 + r0 + i;
+        const double dot = row_dot4(Lsm + i, R, Ls, p.Lbuf + row + (int64_t)k0 * n, n, wrrow, t);
+        const double c = __dsub_rn(a_ip, dot);
+        cr[i] = c;
+        if (r0 + i == pr) {
+          s_bkarr = c;
+          s_bkhas = 1;
+        } else if (better(fabs(c), lp, sk, si)) {
+          sk = fabs(c);
+          si = lp;
+          ss = i;
+        }
+      }
+      const BlockBest lb2 = block_argmax(sk, si, ss, par);
+      par ^= 1;
+      const long long nseq2 = seq + 1;
+      const int pb2 = static_cast<int>(nseq2 & 1);
+      const unsigned tag2 = static_cast<unsigned>(nseq2);
+      if (tid == 0) {
+        u64* q = p.xll + ((size_t)pb2 * G + cta) * kXWords;
+        ll_put_d(q + 0, tag2, lb2.slot >= 0 ? lb2.key : -1.0);
+        ll_put(q + 2, tag2, lb2.slot >= 0 ? static_cast<unsigned>(lb2.idx) : 0x7fffffffu);
+        ll_put_d(q + 3, tag2, s_bkhas ? s_bkarr : 0.0);
+        ll_put(q + 5, tag2, s_bkhas ? 1u : 0u);
+      }
+      seq = nseq2;
+      __syncthreads();  // record out before anyone polls
+      if (cta == kRed) {
+        double gk = -1.0;
+        long long gi = LLONG_MAX;
+        int gs = -1;
+        for (int c = tid; c < G; c += nthr) {
+          unsigned w[6];
+          if (!ll_read<6>(p.xll + ((size_t)pb2 * G + c) * kXWords, tag2, w)) {
+            s_abort = 1;
+            continue;
+          }
+          const double v = ll_d(w[0], w[1]);
+          if (w[5]) s_bkarr = ll_d(w[3], w[4]);
+          if ((v >= 0.0 || v != v) && better(v, static_cast<int>(w[2]), gk, gi)) {
+            gk = v;
+            gi = static_cast<int>(w[2]);
+            gs = c;
+          }
+        }
+        const BlockBest gb = block_argmax(gk, gi, gs, par);
+        __syncthreads();  // s_bkarr from the owner's record
+        const u64 kb = static_cast<u64>(__double_as_longlong(gb.slot >= 0 ? gb.key : -1.0));
+        const u64 ab = static_cast<u64>(__double_as_longlong(s_bkarr));
+        const unsigned hw[5] = {static_cast<unsigned>(kb), static_cast<unsigned>(kb >> 32), static_cast<unsigned>(ab),
+                                static_cast<unsigned>(ab >> 32), s_abort ? 4u : 0u};
+        for (int f = tid; f < G * 5; f += nthr) {
+          const int c = f / 5, u = f - c * 5;
+          if (c != kRed) ll_put(p.sdll + ((size_t)pb2 * G + c) * kMWords + u, tag2, hw[u]);
+        }
+        if (tid < 5) s_dhdr[tid] = hw[tid];
+      } else {
+        if (tid < 5) {
+          unsigned w[1];
+          if (!ll_read<1>(p.sdll + ((size_t)pb2 * G + cta) * kMWords + tid, tag2, w)) {
+            s_abort = 1;
+            w[0] = 4u;
+          }
+          s_dhdr[tid] = w[0];
+        }
+      }
+      par ^= 1;
+      __syncthreads();
+      if (s_abort || (s_dhdr[4] & 4u)) {
+        if (tid == 0) atomicExch(&p.st->status, 99);
+        s_abort = 1;
+        break;
+      }
+      sigma = ll_d(s_dhdr[0], s_dhdr[1]);
+      dr = ll_d(s_dhdr[2], s_dhdr[3]);  // a_rr = c_r(r): the 1x1-swap pivot / the 2x2 block's d22
+      cr_done = true;
+    }
+
+    // ---- decision: 0 skip, 1 1x1, 2 1x1-swap r, 3 2x2 (k, r)
+    //      SBKP (pivot.py:111-128) or BKPP (pivot.py:146-171)
+    int kind, s;
     if (!has_cand || lam == 0.0) {
       kind = 0;
       s = 1;
     } else if (fabs(akk) >= athr) {
       kind = 1;
       s = 1;
+    } else if (p.strategy == 1) {
+      if (__dmul_rn(fabs(akk), sigma) >= __dmul_rn(athr, lam)) {
+        kind = 1;
+        s = 1;
+      } else if (fabs(dr) >= __dmul_rn(alpha, sigma)) {
+        kind = 2;
+        s = 1;
+      } else {
+        kind = 3;
+        s = 2;
+      }
     } else if (fabs(dr) >= athr) {
       kind = 2;
       s = 1;
@@ -1086,7 +1194,13 @@ __global__ void __launch_bounds__(kPanelThreads, 1) panel_kernel(PanelParams pin
       c_mul += colc;
       c_add += colc;
       c_cmp += mm >= 2 ? mm - 2 : 0;
-      if (kind >= 2 && t > 0) {
+      if (p.strategy == 1) {
+        if (cr_done) {  // _form_column(r) + the scan for sigma (pivot.py:162-166)
+          c_mul += colc;
+          c_add += colc;
+          c_cmp += mm >= 2 ? mm - 2 : 0;
+        }
+      } else if (kind >= 2 && t > 0) {  // _diag_entry(r)
         c_mul += t;
         c_add += t;
       }
@@ -1137,7 +1251,7 @@ __global__ void __launch_bounds__(kPanelThreads, 1) panel_kernel(PanelParams pin
 
     // ---- phase B: partner column when needed, multipliers, writes
     const int64_t kglob = k0 + t;
-    if (kind >= 2) {
+    if (kind >= 2 && !cr_done) {
       for (int s2 = tid; s2 < t; s2 += nthr) wrrow[s2] = __ldcg(p.W + (k0 + pr) + (int64_t)s2 * n);
       if (q1) {  // partner's sketch column (per-step downdate, factor.py:486-489)
         const u64* src = p.qcll + ((size_t)pb * G + s_gs2) * QS;

