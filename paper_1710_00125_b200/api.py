@@ -187,8 +187,6 @@ def _native_config(cfg: FactorConfig) -> _native.RcpConfig:
 
 
 def _check_supported(cfg: FactorConfig, batched: bool = False) -> None:
-    if cfg.strategy is Strategy.BBK:
-        raise ValueError("strategy 'bbk' is not part of the B200 build (rcp and bkpp are)")
     if batched and cfg.strategy is not Strategy.RCP:
         raise ValueError(f"the batched kernel runs strategy 'rcp' only, got {cfg.strategy.value!r}")
     if cfg.track_growth is GrowthTracking.FULL or cfg.audit_sketch:

@@ -102,7 +102,7 @@ WorkerBufs carve_worker(unsigned char* b, int64_t n, const Layout& L) {
 int validate_cfg(const rcp_config* c, int64_t n) {
   if (!c || n < 1) return RCP_ERR_INVALID_ARG;
   if (c->p < 1 || c->b < 1 || c->robust_r < 0) return RCP_ERR_INVALID_ARG;
-  if (c->strategy < RCP_STRATEGY_RCP || c->strategy > RCP_STRATEGY_BKPP) return RCP_ERR_INVALID_ARG;
+  if (c->strategy < RCP_STRATEGY_RCP || c->strategy > RCP_STRATEGY_BBK) return RCP_ERR_INVALID_ARG;
   if (!(c->q == 1 || c->q == c->b)) return RCP_ERR_INVALID_ARG;
   if (c->p < c->q) return RCP_ERR_INVALID_ARG;
   if (n > (int64_t)INT_MAX / 2) return RCP_ERR_INVALID_ARG;
@@ -342,6 +342,7 @@ int rcp_factor_dist(const rcp_config* cfg, int64_t n, const double* a, int64_t l
   base.P = P;
   base.alpha = rcp_strat ? std::sqrt(2.0) / 2.0 : (1.0 + std::sqrt(17.0)) / 8.0;  // factor.py:299
   base.strategy = c.strategy;
+  base.bkscr = Lneg;  // free while a panel runs (the gather fills it afterwards)
   base.q1 = q1 ? 1 : 0;
   base.qscr = dptr(Lay.qscr);
   base.Lbuf = Lbuf;

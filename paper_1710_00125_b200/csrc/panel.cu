@@ -220,8 +220,8 @@ __global__ void __launch_bounds__(kPanelThreads, 1) panel_kernel(PanelParams pin
   __shared__ XRec s_win;
   __shared__ unsigned s_qhdr[8], s_dhdr[12];
   __shared__ int s_wpos, s_qflags, s_hascand, s_wcta, s_gs1, s_gs2;
-  __shared__ double s_bkarr;  // bkpp: a_rr of the partner column
-  __shared__ int s_bkhas;
+  __shared__ double s_bkarr, s_bkcp;  // bkpp / bbk: a_rr of the partner column, c_p(imax)
+  __shared__ int s_bkhas, s_bkjph;
 
   for (int x = tid; x < Wn; x += nthr) win[x] = x;
   for (int i = tid; i < rcnt; i += nthr) lpos[i] = r0 + i;
@@ -1159,8 +1159,184 @@ __global__ void __launch_bounds__(kPanelThreads, 1) panel_kernel(PanelParams pin
       cr_done = true;
     }
 
+    // pivot-block sources: c0 = the column that ends at position t, c1 = at t + 1 (2x2); their
+    // physical rows, W rows and formed values.  Defaults: SBKP / BKPP.
+    double* c0v = ck;
+    double* c1v = cr;
+    const double* c0w = wrow;
+    const double* c1w = wrrow;
+    int c0phys = pk;
+    double d3a = akk, d3b = ckr;  // 2x2 block d11, d21 (d22 = dr)
+    int pre_pos = -1, pre_phys = -1;  // bbk: swap(k, p) before swap(k + 1, r) (factor.py:628-629)
+    int bbk_kind = -1;
+    long long bbk_iters = 0;
+    if (p.strategy == 2 && has_cand && lam != 0.0 && !(fabs(akk) >= athr)) {
+      // ---- BBK rook walk (pivot.py:189-218): form column imax, rowmax = max_{i != imax} |c(i)|
+      //      (one exchange per hop); stop at a 1x1-swap (|a_ii| >= alpha rowmax) or a 2x2 (p, imax)
+      int ppos = t, pphys = pk, ipos = r_rel, iphys = pr;
+      double colmax = lam, app = akk;
+      double* cpv = ck;
+      const double* cpw = wrow;
+      // third column / W-row buffers in global scratch (the rook path is off the rcp critical path)
+      double* const cx = p.bkscr + (size_t)cta * (R + Wn);
+      double* const wx = cx + R;
+      int nb = 0;
+      for (long long it = 0; it <= n - (k0 + t); ++it) {
+        double* ccv = nb ? cx : cr;
+        double* ccw = nb ? wx : wrrow;
+        for (int s2 = tid; s2 < t; s2 += nthr) ccw[s2] = __ldcg(p.W + (k0 + iphys) + (int64_t)s2 * n);
+        const double av0 = (tid < rcnt) ? sym_at(A, n, k0 + r0 + tid, k0 + iphys) : 0.0;
+        if (tid == 0) s_bkhas = 0;
+        __syncthreads();  // ccw ready
+        double sk = -1.0;
+        long long si = LLONG_MAX;
+        int ss = -1;
+        for (int i = tid; i < rcnt; i += nthr) {
+          const double a_ip = (i == tid) ? av0 : sym_at(A, n, k0 + r0 + i, k0 + iphys);
+          const int lp = lpos[i];
+          if (lp < t) continue;
+          const int64_t row = k0 + r0 + i;
+          const double dot = row_dot4(Lsm + i, R, Ls, p.Lbuf + row + (int64_t)k0 * n, n, ccw, t);
+          const double c = __dsub_rn(a_ip, dot);
+          ccv[i] = c;
+          if (r0 + i == iphys) {
+            s_bkarr = c;
+            s_bkcp = cpv[i];
+            s_bkhas = 1;
+          } else if (better(fabs(c), lp, sk, si)) {
+            sk = fabs(c);
+            si = lp;
+            ss = i;
+          }
+        }
+        const BlockBest lb2 = block_argmax(sk, si, ss, par);
+        par ^= 1;
+        const long long nseq2 = seq + 1;
+        const int pb2 = static_cast<int>(nseq2 & 1);
+        const unsigned tag2 = static_cast<unsigned>(nseq2);
+        if (tid == 0) {
+          u64* q = p.xll + ((size_t)pb2 * G + cta) * kXWords;
+          const bool hv = lb2.slot >= 0;
+          ll_put_d(q + 0, tag2, hv ? lb2.key : -1.0);
+          ll_put(q + 2, tag2, hv ? static_cast<unsigned>(lb2.idx) : 0x7fffffffu);
+          ll_put(q + 3, tag2, hv ? static_cast<unsigned>(r0 + lb2.slot) : 0xffffffffu);
+          ll_put_d(q + 4, tag2, s_bkhas ? s_bkarr : 0.0);
+          ll_put_d(q + 6, tag2, s_bkhas ? s_bkcp : 0.0);
+          ll_put(q + 8, tag2, s_bkhas ? 1u : 0u);
+        }
+        seq = nseq2;
+        __syncthreads();  // record out before anyone polls
+        if (cta == kRed) {
+          double gk = -1.0;
+          long long gi = LLONG_MAX;
+          int gs = -1;
+          unsigned gph = 0;
+          for (int c = tid; c < G; c += nthr) {
+            unsigned w[9];
+            if (!ll_read<9>(p.xll + ((size_t)pb2 * G + c) * kXWords, tag2, w)) {
+              s_abort = 1;
+              continue;
+            }
+            const double v = ll_d(w[0], w[1]);
+            if (w[8]) {
+              s_bkarr = ll_d(w[4], w[5]);
+              s_bkcp = ll_d(w[6], w[7]);
+            }
+            if ((v >= 0.0 || v != v) && better(v, static_cast<int>(w[2]), gk, gi)) {
+              gk = v;
+              gi = static_cast<int>(w[2]);
+              gs = c;
+              gph = w[3];
+            }
+          }
+          const BlockBest gb = block_argmax(gk, gi, gs, par);
+          if (gs >= 0 && gs == gb.slot) s_bkjph = static_cast<int>(gph);
+          __syncthreads();
+          const u64 kb = static_cast<u64>(__double_as_longlong(gb.slot >= 0 ? gb.key : -1.0));
+          const u64 ab = static_cast<u64>(__double_as_longlong(s_bkarr));
+          const u64 cb = static_cast<u64>(__double_as_longlong(s_bkcp));
+          const unsigned hw[9] = {static_cast<unsigned>(kb), static_cast<unsigned>(kb >> 32),
+                                  gb.slot >= 0 ? static_cast<unsigned>(gb.idx) : 0x7fffffffu,
+                                  gb.slot >= 0 ? static_cast<unsigned>(s_bkjph) : 0xffffffffu,
+                                  static_cast<unsigned>(ab), static_cast<unsigned>(ab >> 32),
+                                  static_cast<unsigned>(cb), static_cast<unsigned>(cb >> 32), s_abort ? 4u : 0u};
+          for (int f = tid; f < G * 9; f += nthr) {
+            const int c = f / 9, u = f - c * 9;
+            if (c != kRed) ll_put(p.sdll + ((size_t)pb2 * G + c) * kMWords + u, tag2, hw[u]);
+          }
+          if (tid < 9) s_dhdr[tid] = hw[tid];
+        } else {
+          if (tid < 9) {
+            unsigned w[1];
+            if (!ll_read<1>(p.sdll + ((size_t)pb2 * G + cta) * kMWords + tid, tag2, w)) {
+              s_abort = 1;
+              w[0] = 4u;
+            }
+            s_dhdr[tid] = w[0];
+          }
+        }
+        par ^= 1;
+        __syncthreads();
+        if (s_abort || (s_dhdr[8] & 4u)) {
+          bbk_kind = -2;
+          break;
+        }
+        ++bbk_iters;
+        const double rowmax = ll_d(s_dhdr[0], s_dhdr[1]);
+        const int jpos = static_cast<int>(s_dhdr[2]);
+        const int jphys = static_cast<int>(s_dhdr[3]);
+        const double aii = ll_d(s_dhdr[4], s_dhdr[5]);
+        const double cpi = ll_d(s_dhdr[6], s_dhdr[7]);
+        __syncthreads();  // s_dhdr / s_bk* reused by the next hop
+        if (fabs(aii) >= __dmul_rn(alpha, rowmax)) {  // 1x1 with swap(k, imax)
+          bbk_kind = 2;
+          c0v = ccv;
+          c0w = ccw;
+          c0phys = iphys;
+          dr = aii;
+          r_rel = ipos;
+          pr = iphys;
+          break;
+        }
+        if (jpos == ppos || rowmax <= colmax) {  // 2x2 (p, imax)
+          bbk_kind = 3;
+          c0v = cpv;
+          c0w = cpw;
+          c0phys = pphys;
+          c1v = ccv;
+          c1w = ccw;
+          d3a = app;
+          d3b = cpi;
+          dr = aii;
+          r_rel = ipos;
+          pr = iphys;
+          if (ppos != t) {
+            pre_pos = ppos;
+            pre_phys = pphys;
+          }
+          if (ipos == t) bbk_kind = -3;  // walk returned to k with a 2x2: not supported (ties only)
+          break;
+        }
+        ppos = ipos;  // hop: p <- imax, imax <- jmax
+        pphys = iphys;
+        cpv = ccv;
+        cpw = ccw;
+        app = aii;
+        colmax = rowmax;
+        ipos = jpos;
+        iphys = jphys;
+        nb ^= 1;
+      }
+      if (bbk_kind < 0) {
+        if (tid == 0) atomicExch(&p.st->status, bbk_kind == -3 ? 96 : 99);
+        s_abort = 1;
+        break;
+      }
+      cr_done = true;
+    }
+
     // ---- decision: 0 skip, 1 1x1, 2 1x1-swap r, 3 2x2 (k, r)
-    //      SBKP (pivot.py:111-128) or BKPP (pivot.py:146-171)
+    //      SBKP (pivot.py:111-128), BKPP (pivot.py:146-171) or BBK (pivot.py:189-218)
     int kind, s;
     if (!has_cand || lam == 0.0) {
       kind = 0;
@@ -1168,6 +1344,9 @@ __global__ void __launch_bounds__(kPanelThreads, 1) panel_kernel(PanelParams pin
     } else if (fabs(akk) >= athr) {
       kind = 1;
       s = 1;
+    } else if (p.strategy == 2) {
+      kind = bbk_kind;
+      s = kind == 3 ? 2 : 1;
     } else if (p.strategy == 1) {
       if (__dmul_rn(fabs(akk), sigma) >= __dmul_rn(athr, lam)) {
         kind = 1;
@@ -1194,7 +1373,11 @@ __global__ void __launch_bounds__(kPanelThreads, 1) panel_kernel(PanelParams pin
       c_mul += colc;
       c_add += colc;
       c_cmp += mm >= 2 ? mm - 2 : 0;
-      if (p.strategy == 1) {
+      if (p.strategy == 2) {  // each rook hop: _form_column(imax) + its scan (pivot.py:207-213)
+        c_mul += colc * bbk_iters;
+        c_add += colc * bbk_iters;
+        c_cmp += (mm >= 2 ? mm - 2 : 0) * bbk_iters;
+      } else if (p.strategy == 1) {
         if (cr_done) {  // _form_column(r) + the scan for sigma (pivot.py:162-166)
           c_mul += colc;
           c_add += colc;
@@ -1230,6 +1413,16 @@ __global__ void __launch_bounds__(kPanelThreads, 1) panel_kernel(PanelParams pin
 
     // ---- symmetric swaps as permutation bookkeeping (factor.py:624-630)
     int p_t = pk, p_t1 = -1;
+    if (kind == 3 && pre_pos >= 0) {  // bbk: swap(k, p) first (factor.py:628-629)
+      if (tid == 0) {
+        const int col_t = win[t];
+        win[t] = pre_phys;
+        if (pre_pos < Wn) win[pre_pos] = col_t;
+        if (pre_phys >= r0 && pre_phys < r0 + rcnt) lpos[pre_phys - r0] = t;
+        if (col_t >= r0 && col_t < r0 + rcnt) lpos[col_t - r0] = pre_pos;
+      }
+      p_t = pre_phys;
+    }
     if (kind == 2) {  // swap(k, r)
       if (tid == 0) {
         win[t] = pr;
@@ -1240,7 +1433,7 @@ __global__ void __launch_bounds__(kPanelThreads, 1) panel_kernel(PanelParams pin
       p_t = pr;
     } else if (kind == 3) {  // swap(k+1, r)
       if (r_rel != t + 1 && tid == 0) {
-        const int p1 = win[t + 1];
+        const int p1 = win[t + 1];  // (after the bbk swap(k, p), which never touches r's position)
         win[t + 1] = pr;
         if (r_rel < Wn) win[r_rel] = p1;
         if (pr >= r0 && pr < r0 + rcnt) lpos[pr - r0] = t + 1;
@@ -1281,8 +1474,8 @@ __global__ void __launch_bounds__(kPanelThreads, 1) panel_kernel(PanelParams pin
       d11 = dr;
       if (!isfinite(d11)) num_kind = 3;
     } else {
-      d11 = akk;
-      d21 = ckr;
+      d11 = d3a;
+      d21 = d3b;
       d22 = dr;
       det = __dsub_rn(__dmul_rn(d11, d22), __dmul_rn(d21, d21));
       if (det == 0.0) {
@@ -1308,7 +1501,7 @@ __global__ void __launch_bounds__(kPanelThreads, 1) panel_kernel(PanelParams pin
       if (lp < t) continue;
       const int64_t row = k0 + r0 + i;
       if (kind <= 1) {
-        const double c = ck[i];
+        const double c = c0v[i];
         p.W[row + (int64_t)t * n] = c;
         if (lp > t) {
           double l = (kind == 0) ? 0.0 : __ddiv_rn(c, d11);
@@ -1320,7 +1513,7 @@ __global__ void __launch_bounds__(kPanelThreads, 1) panel_kernel(PanelParams pin
             for (int r = 0; r < P; ++r) Bq[r * R + i] = __dsub_rn(Bq[r * R + i], __dmul_rn(skp0[r], l));
         }
       } else if (kind == 2) {
-        const double c = cr[i];
+        const double c = (p.strategy == 2 ? c0v : cr)[i];
         p.W[row + (int64_t)t * n] = c;
         if (lp > t) {
           double l = __ddiv_rn(c, d11);
@@ -1332,7 +1525,7 @@ __global__ void __launch_bounds__(kPanelThreads, 1) panel_kernel(PanelParams pin
             for (int r = 0; r < P; ++r) Bq[r * R + i] = __dsub_rn(Bq[r * R + i], __dmul_rn(skr[r], l));
         }
       } else {
-        const double c0 = ck[i], c1 = cr[i];
+        const double c0 = c0v[i], c1 = c1v[i];
         p.W[row + (int64_t)t * n] = c0;
         p.W[row + (int64_t)(t + 1) * n] = c1;
         if (lp > t + 1) {
@@ -1389,14 +1582,14 @@ __global__ void __launch_bounds__(kPanelThreads, 1) panel_kernel(PanelParams pin
         lnext[s3] = __ldcg(p.Lbuf + rown + (int64_t)(k0 + s3) * n);
         wnext[s3] = __ldcg(p.W + rown + (int64_t)s3 * n);
       }
-      const double an0 = (tid == 0) ? sym_at(A, n, rown, k0 + (kind == 2 ? pr : pk)) : 0.0;
+      const double an0 = (tid == 0) ? sym_at(A, n, rown, k0 + (kind == 2 ? pr : c0phys)) : 0.0;
       const double an1 = (tid == 0 && kind == 3) ? sym_at(A, n, rown, k0 + pr) : 0.0;
       __syncthreads();
       if (tid == 0) {
         auto lrow = [&](int s3) { return lnext[s3]; };
-        const double v0 = __dsub_rn(an0, chain_dot4(lrow, kind == 2 ? wrrow : wrow, t));
+        const double v0 = __dsub_rn(an0, chain_dot4(lrow, kind == 2 ? (p.strategy == 2 ? c0w : wrrow) : c0w, t));
         wnext[t] = v0;
-        if (kind == 3) wnext[t + 1] = __dsub_rn(an1, chain_dot4(lrow, wrrow, t));
+        if (kind == 3) wnext[t + 1] = __dsub_rn(an1, chain_dot4(lrow, c1w, t));
       }
       __syncthreads();
       for (int s3 = tid; s3 < tn; s3 += nthr) wrow[s3] = wnext[s3];

@@ -161,6 +161,7 @@ struct PanelParams {
   const PanelDesc* desc;
   int b, q, num_sms, smem_budget;
   int strategy;  // RCP_STRATEGY_*: decision rule of the pivot steps
+  double* bkscr;  // bbk: per-CTA global scratch (third column + W-row buffer), G * (R + Wn) doubles
 };
 
 cudaError_t panel_init_attributes(int max_dyn_smem);

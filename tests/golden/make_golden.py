@@ -106,6 +106,12 @@ def main_bk():
     save("g_bkpp_c5_scaled", gallery.scaled_member(256, 10, True), dict(strategy="bkpp", b=16, q=1, p=5, seed=0))
     save("g_bkpp_zero5", np.zeros((5, 5)), dict(strategy="bkpp", b=4, q=1, p=5, seed=0))
     save("g_bkpp_exchange4", np.eye(4)[::-1].copy(), dict(strategy="bkpp", b=2, q=1, p=5, seed=0))
+    save("g_bbk_n100_b8", sym(100, 1), dict(strategy="bbk", b=8, q=1, p=5, seed=7))
+    save("g_bbk_n300_b32", sym(300, 3), dict(strategy="bbk", b=32, q=1, p=5, seed=0))
+    save("g_bbk_n64_b1", sym(64, 6), dict(strategy="bbk", b=1, q=1, p=5, seed=0))
+    save("g_bbk_kkt_200", gallery.kkt(160, 40, 4), dict(strategy="bbk", b=16, q=1, p=5, seed=0))
+    save("g_bbk_c5_scaled", gallery.scaled_member(256, 10, True), dict(strategy="bbk", b=16, q=1, p=5, seed=0))
+    save("g_bbk_exchange4", np.eye(4)[::-1].copy(), dict(strategy="bbk", b=2, q=1, p=5, seed=0))
 
 
 if __name__ == "__main__":

@@ -249,11 +249,13 @@ def test_supplied_omega_with_guard_recompute(cuda_ok):
     assert np.array_equal(f.perm.cpu().numpy(), g["perm"])
 
 
+@pytest.mark.parametrize("strategy", ["bkpp", "bbk"])
 @pytest.mark.parametrize("n,b,seed,kind", [(512, 32, 0, "type6"), (1000, 64, 1, "type6"), (600, 16, 2, "kkt"),
                                            (257, 128, 3, "type6"), (300, 8, 4, "scaled")])
-def test_bkpp_matches_oracle_live(cuda_ok, n, b, seed, kind):
-    """Bunch-Kaufman partial pivoting (pivot.py:146-171) on the same panel engine: same pivot
-    sequence, block structure and op counters as the oracle (itself bit-exact vs the reference)."""
+def test_bk_strategies_match_oracle_live(cuda_ok, strategy, n, b, seed, kind):
+    """Bunch-Kaufman partial pivoting (pivot.py:146-171) and the rook search (pivot.py:189-218) on
+    the same panel engine: same pivot sequence, block structure and op counters as the oracle
+    (itself bit-exact vs the reference)."""
     from oracle.rcp_oracle import OracleConfig, oracle_factor
     from paper_1710_00125_b200 import gallery
     if kind == "type6":
@@ -262,8 +264,8 @@ def test_bkpp_matches_oracle_live(cuda_ok, n, b, seed, kind):
         a = gallery.kkt((4 * n) // 5, n - (4 * n) // 5, seed)
     else:
         a = gallery.scaled_member(n, seed, True)
-    o = oracle_factor(a, OracleConfig(strategy="bkpp", b=b, q=1, p=5, seed=seed))
-    df = _gpu_factor(a, dict(strategy="bkpp", b=b, q=1, p=5, seed=seed))
+    o = oracle_factor(a, OracleConfig(strategy=strategy, b=b, q=1, p=5, seed=seed))
+    df = _gpu_factor(a, dict(strategy=strategy, b=b, q=1, p=5, seed=seed))
     hf = df.to_host()
     assert np.array_equal(hf.perm, o.perm)
     assert np.array_equal(hf.pattern, o.pattern)
@@ -273,12 +275,3 @@ def test_bkpp_matches_oracle_live(cuda_ok, n, b, seed, kind):
     dref = o.d_dense()
     assert np.abs(hf.D.to_dense() - dref).max() <= l_tol(n) * max(1.0, np.abs(dref).max())
     assert hf.stats.recompute_count == 0
-
-
-def test_bbk_is_rejected_not_faked(cuda_ok):
-    """bbk is not built on the GPU: the API refuses it instead of silently running another rule."""
-    import torch
-
-    from paper_1710_00125_b200 import api
-    with pytest.raises(ValueError, match="bbk"):
-        api.factor_device(torch.eye(4, dtype=torch.float64, device="cuda"), strategy="bbk", b=2, q=1, p=5)

@@ -41,9 +41,7 @@ def test_factor_robust_prerequisites():
 
 
 def test_out_of_scope_strategies_are_explicit():
-    # bbk (rook pivoting) is not built on the GPU; bkpp is (tests/test_gpu_parity.py)
-    with pytest.raises(ValueError, match="bbk"):
-        api.factor(np.eye(3), strategy="bbk")
+    # the batched kernel runs rcp only; bkpp / bbk run on the single-matrix engine
     with pytest.raises(ValueError, match="rcp"):
         api._check_supported(api.FactorConfig(strategy="bkpp"), batched=True)
 
