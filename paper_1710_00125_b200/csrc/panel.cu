@@ -152,6 +152,8 @@ RCP_D long long prof_now() { return clock64(); }
 
 }  // namespace
 
+// STRAT: RCP_STRATEGY_* as a template argument, so the rcp kernel carries no bkpp / bbk code.
+template <int STRAT>
 __global__ void __launch_bounds__(kPanelThreads, 1) panel_kernel(PanelParams pin) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int cta = blockIdx.x, tid = threadIdx.x, nthr = blockDim.x;
@@ -1069,7 +1071,7 @@ __global__ void __launch_bounds__(kPanelThreads, 1) panel_kernel(PanelParams pin
     //      sigma = max_{i != r} |c_r(i)| with a second exchange; a_rr comes from r's owner.
     bool cr_done = false;
     double sigma = 0.0;
-    if (p.strategy == 1 && has_cand && lam != 0.0 && !(fabs(akk) >= athr)) {
+    if (STRAT == 1 && has_cand && lam != 0.0 && !(fabs(akk) >= athr)) {
       for (int s2 = tid; s2 < t; s2 += nthr) wrrow[s2] = __ldcg(p.W + (k0 + pr) + (int64_t)s2 * n);
       const double av0 = (tid < rcnt) ? sym_at(A, n, k0 + r0 + tid, k0 + pr) : 0.0;
       if (tid == 0) s_bkhas = 0;
@@ -1170,7 +1172,7 @@ __global__ void __launch_bounds__(kPanelThreads, 1) panel_kernel(PanelParams pin
     int pre_pos = -1, pre_phys = -1;  // bbk: swap(k, p) before swap(k + 1, r) (factor.py:628-629)
     int bbk_kind = -1;
     long long bbk_iters = 0;
-    if (p.strategy == 2 && has_cand && lam != 0.0 && !(fabs(akk) >= athr)) {
+    if (STRAT == 2 && has_cand && lam != 0.0 && !(fabs(akk) >= athr)) {
       // ---- BBK rook walk (pivot.py:189-218): form column imax, rowmax = max_{i != imax} |c(i)|
       //      (one exchange per hop); stop at a 1x1-swap (|a_ii| >= alpha rowmax) or a 2x2 (p, imax)
       int ppos = t, pphys = pk, ipos = r_rel, iphys = pr;
@@ -1344,10 +1346,10 @@ __global__ void __launch_bounds__(kPanelThreads, 1) panel_kernel(PanelParams pin
     } else if (fabs(akk) >= athr) {
       kind = 1;
       s = 1;
-    } else if (p.strategy == 2) {
+    } else if (STRAT == 2) {
       kind = bbk_kind;
       s = kind == 3 ? 2 : 1;
-    } else if (p.strategy == 1) {
+    } else if (STRAT == 1) {
       if (__dmul_rn(fabs(akk), sigma) >= __dmul_rn(athr, lam)) {
         kind = 1;
         s = 1;
@@ -1373,11 +1375,11 @@ __global__ void __launch_bounds__(kPanelThreads, 1) panel_kernel(PanelParams pin
       c_mul += colc;
       c_add += colc;
       c_cmp += mm >= 2 ? mm - 2 : 0;
-      if (p.strategy == 2) {  // each rook hop: _form_column(imax) + its scan (pivot.py:207-213)
+      if (STRAT == 2) {  // each rook hop: _form_column(imax) + its scan (pivot.py:207-213)
         c_mul += colc * bbk_iters;
         c_add += colc * bbk_iters;
         c_cmp += (mm >= 2 ? mm - 2 : 0) * bbk_iters;
-      } else if (p.strategy == 1) {
+      } else if (STRAT == 1) {
         if (cr_done) {  // _form_column(r) + the scan for sigma (pivot.py:162-166)
           c_mul += colc;
           c_add += colc;
@@ -1513,7 +1515,7 @@ __global__ void __launch_bounds__(kPanelThreads, 1) panel_kernel(PanelParams pin
             for (int r = 0; r < P; ++r) Bq[r * R + i] = __dsub_rn(Bq[r * R + i], __dmul_rn(skp0[r], l));
         }
       } else if (kind == 2) {
-        const double c = (p.strategy == 2 ? c0v : cr)[i];
+        const double c = (STRAT == 2 ? c0v : cr)[i];
         p.W[row + (int64_t)t * n] = c;
         if (lp > t) {
           double l = __ddiv_rn(c, d11);
@@ -1587,7 +1589,7 @@ __global__ void __launch_bounds__(kPanelThreads, 1) panel_kernel(PanelParams pin
       __syncthreads();
       if (tid == 0) {
         auto lrow = [&](int s3) { return lnext[s3]; };
-        const double v0 = __dsub_rn(an0, chain_dot4(lrow, kind == 2 ? (p.strategy == 2 ? c0w : wrrow) : c0w, t));
+        const double v0 = __dsub_rn(an0, chain_dot4(lrow, kind == 2 ? (STRAT == 2 ? c0w : wrrow) : c0w, t));
         wnext[t] = v0;
         if (kind == 3) wnext[t + 1] = __dsub_rn(an1, chain_dot4(lrow, c1w, t));
       }
@@ -1682,20 +1684,31 @@ cudaError_t launch_panel_commit(PanelDesc* din, PanelDesc* dout, PanelLog* plog,
 }
 
 cudaError_t panel_init_attributes(int max_dyn_smem) {
-  return cudaFuncSetAttribute(panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, max_dyn_smem);
+  cudaError_t e = cudaFuncSetAttribute(panel_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_dyn_smem);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(panel_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_dyn_smem);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(panel_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_dyn_smem);
+  return e;
 }
 
 int panel_static_smem_bytes() {
   cudaFuncAttributes attr;
-  if (cudaFuncGetAttributes(&attr, panel_kernel) != cudaSuccess) return 4096;
-  return static_cast<int>(attr.sharedSizeBytes);
+  int mx = 0;
+  if (cudaFuncGetAttributes(&attr, panel_kernel<0>) != cudaSuccess) return 4096;
+  mx = static_cast<int>(attr.sharedSizeBytes);
+  if (cudaFuncGetAttributes(&attr, panel_kernel<1>) != cudaSuccess) return 4096;
+  mx = mx > static_cast<int>(attr.sharedSizeBytes) ? mx : static_cast<int>(attr.sharedSizeBytes);
+  if (cudaFuncGetAttributes(&attr, panel_kernel<2>) != cudaSuccess) return 4096;
+  mx = mx > static_cast<int>(attr.sharedSizeBytes) ? mx : static_cast<int>(attr.sharedSizeBytes);
+  return mx;
 }
 
 cudaError_t launch_panel(const PanelParams& prm, int G, size_t smem, cudaStream_t st) {
   PanelParams copy = prm;
   void* args[] = {&copy};
-  return cudaLaunchCooperativeKernel(reinterpret_cast<void*>(panel_kernel), dim3(G), dim3(kPanelThreads), args,
-                                     smem, st);
+  const void* fn = prm.strategy == 2   ? reinterpret_cast<const void*>(panel_kernel<2>)
+                   : prm.strategy == 1 ? reinterpret_cast<const void*>(panel_kernel<1>)
+                                       : reinterpret_cast<const void*>(panel_kernel<0>);
+  return cudaLaunchCooperativeKernel(fn, dim3(G), dim3(kPanelThreads), args, smem, st);
 }
 
 }  // namespace rcp
