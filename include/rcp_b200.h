@@ -124,7 +124,9 @@ typedef int (*rcp_draw_fn)(void* ctx, int64_t rows, int64_t cols, double* out);
 /* Bytes of device workspace rcp_factor needs for this (n, cfg). */
 size_t rcp_workspace_bytes(int64_t n, const rcp_config* cfg);
 
-/* Factor A[perm][:, perm] = L D L^T (randldl.factor, factor.py:637-647).
+/* Factor A[perm][:, perm] = L D L^T (randldl.factor, factor.py:637-647) with the strategy in
+ * cfg->strategy.  omega (p x n, device, row-major: the first draw of the factorization's
+ * generator) is required for RCP_STRATEGY_RCP and ignored (may be NULL) for bkpp / bbk.
  * Optional per-step trace (device, may be NULL): trace_kind[k] in {0 skip, 1 1x1,
  * 2 1x1-swap, 3 2x2} at each decision position k, trace_r[k] = partner r or -1. */
 int rcp_factor(const rcp_config* cfg, int64_t n, const double* a, int64_t lda,
