@@ -31,9 +31,6 @@ constexpr int kPanelThreads = 256;
 constexpr int kWarps = kPanelThreads / 32;
 constexpr int kRegRows = 32;  // QRCP register mode: sketch rows [0, 32) of each column live in registers
 constexpr long long kWatchdogCycles = 8000000000LL;
-#ifndef RCP_SBKP_SHARED
-#define RCP_SBKP_SHARED 0  // 1: SBKP decision on one shared line polled by every CTA (A/B switch)
-#endif
 
 struct BlockBest {
   double key;
@@ -1006,14 +1003,10 @@ __global__ void __launch_bounds__(kPanelThreads, 1) panel_kernel(PanelParams pin
         hw[9] = static_cast<unsigned>(s_win.phys);
         hw[10] = (s_hascand ? 1u : 0u) | (s_gerr ? 2u : 0u) | (s_abort ? 4u : 0u);
         hw[11] = static_cast<unsigned>(gb.slot);
-#if RCP_SBKP_SHARED
-        if (tid < 12) ll_put(p.sdll + (size_t)pb * G * kMWords + tid, tag, hw[tid]);
-#else
         for (int f = tid; f < G * 12; f += nthr) {
           const int c = f / 12, u = f - c * 12;
           if (c != kRed) ll_put(p.sdll + ((size_t)pb * G + c) * kMWords + u, tag, hw[u]);
         }
-#endif
       }
       if (tid == 0) s_gs2 = gb.slot;
       // The decision will need the partner column r unless the 1x1 test passes: start pulling it
@@ -1025,7 +1018,7 @@ __global__ void __launch_bounds__(kPanelThreads, 1) panel_kernel(PanelParams pin
     } else {
       if (tid < 12) {
         unsigned w[1];
-        if (!ll_read<1>(p.sdll + ((size_t)pb * G + (RCP_SBKP_SHARED ? 0 : cta)) * kMWords + tid, tag, w)) {
+        if (!ll_read<1>(p.sdll + ((size_t)pb * G + cta) * kMWords + tid, tag, w)) {
           s_abort = 1;
           w[0] = 0;
         }
