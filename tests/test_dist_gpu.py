@@ -29,7 +29,8 @@ def _same(f1, f2):
         assert f1.stats[k] == f2.stats[k], k
 
 
-@pytest.mark.parametrize("name", ["g_n300_b32", "g_c5_scaled", "g_zero_tail", "g_n100_q1_b64", "g_kkt_200"])
+@pytest.mark.parametrize("name", ["g_n300_b32", "g_c5_scaled", "g_zero_tail", "g_n100_q1_b64", "g_kkt_200",
+                                  "g_bkpp_n300_b32", "g_bbk_n300_b32"])
 @pytest.mark.parametrize("world", [2, 3, 4])
 def test_emulated_world_is_bit_identical(cuda_ok, name, world):
     g = load_golden(name)
