@@ -249,32 +249,53 @@ class DeviceFactorization:
                                    self.pattern.cpu().numpy())
 
     def to_host(self) -> Factorization:
+        lh = None
+        if self.n >= 2048:  # D2H of the dense L into (cached) pinned memory, overlapped with the
+            lh = torch.empty(tuple(self.L.shape), dtype=torch.float64, pin_memory=True)  # host work below
+            lh.copy_(self.L, non_blocking=True)
         pattern = self.pattern.cpu().numpy().astype(np.int8)
         blocks = _blocks_from_arrays(self.d_diag.cpu().numpy(), self.d_off.cpu().numpy(), pattern)
         s = self.stats
         stats = GrowthStats(rho_cheap=s["rho_cheap"], max_multiplier=s["max_multiplier"],
                             counters=OpCounters(*s["counters"]), recompute_count=s["recompute_count"])
-        if self.n >= 2048:  # D2H into (cached) pinned memory: full PCIe bandwidth for the dense L
-            lh = torch.empty(tuple(self.L.shape), dtype=torch.float64, pin_memory=True)
-            lh.copy_(self.L)
+        perm = self.perm.cpu().numpy().astype(np.int64)
+        if lh is not None:
+            torch.cuda.current_stream(self.L.device).synchronize()
             L = lh.numpy()
         else:
             L = self.L.cpu().numpy()
-        return Factorization(perm=self.perm.cpu().numpy().astype(np.int64), L=L,
-                             D=BlockDiag(blocks), pattern=pattern, stats=stats)
+        return Factorization(perm=perm, L=L, D=BlockDiag(blocks), pattern=pattern, stats=stats)
 
 
 def _blocks_from_arrays(dd: np.ndarray, doff: np.ndarray, pattern: np.ndarray) -> list:
-    blocks = []
+    """The reference's list of (1,1)/(2,2) D blocks (factor.py:153-199) from the flat arrays.
+    The blocks are views of two stacked arrays built vectorised (a Python-level np.array per
+    block costs ~40 ms at n = 32768)."""
     n = pattern.size
-    i = 0
-    while i < n:
-        if pattern[i] == PAT_PAIR_START and i + 1 < n:
-            blocks.append(np.array([[dd[i], doff[i]], [doff[i], dd[i + 1]]]))
-            i += 2
+    is2 = pattern == PAT_PAIR_START
+    if n:
+        is2[-1] = False
+    consumed = np.zeros(n, dtype=bool)
+    consumed[1:] = is2[:-1]
+    starts = np.flatnonzero(~consumed)
+    s2 = starts[is2[starts]]
+    s1 = starts[~is2[starts]]
+    two = np.empty((s2.size, 2, 2))
+    two[:, 0, 0] = dd[s2]
+    two[:, 0, 1] = doff[s2]
+    two[:, 1, 0] = doff[s2]
+    two[:, 1, 1] = dd[s2 + 1]
+    one = np.ascontiguousarray(dd[s1], dtype=np.float64).reshape(-1, 1, 1)
+    kind = is2[starts].tolist()
+    blocks = []
+    i1 = i2 = 0
+    for k2 in kind:
+        if k2:
+            blocks.append(two[i2])
+            i2 += 1
         else:
-            blocks.append(np.array([[dd[i]]]))
-            i += 1
+            blocks.append(one[i1])
+            i1 += 1
     return blocks
 
 
@@ -460,8 +481,14 @@ def factor(a: np.ndarray, cfg: FactorConfig | None = None, **overrides) -> Facto
     _check_supported(cfg)
     _native.load()
     dev = _device()
-    ad = torch.from_numpy(np.ascontiguousarray(a)).to(dev)
-    return factor_device(ad, cfg).to_host()
+    at = torch.from_numpy(np.ascontiguousarray(a))
+    # the H2D copy of A (asynchronous from pinned memory) overlaps the host draw of Omega
+    ad = at.to(dev, non_blocking=at.is_pinned())
+    omega = None
+    if cfg.strategy is Strategy.RCP:
+        omega = torch.from_numpy(np.random.Generator(np.random.Philox(cfg.seed)).standard_normal((cfg.p, a.shape[0])))
+        omega = omega.to(dev)
+    return factor_device(ad, cfg, omega=omega).to_host()
 
 
 def factor_robust(a: np.ndarray, cfg: FactorConfig | None = None, **overrides) -> Factorization:
