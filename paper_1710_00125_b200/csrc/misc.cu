@@ -154,7 +154,22 @@ __global__ void ysolve_kernel(int64_t n, int P, int k0, int t, int tpad, const i
   }
   extern __shared__ double sm[];  // [t][t]: row a = column a of L11
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  for (int f = tid; f < t * t; f += blockDim.x) sm[f] = L11T[f];
+  {  // stage L11 (t*t doubles, L2-resident): 16-byte loads, 8 in flight per thread
+    const int tt = t * t, t2 = tt >> 1;
+    const double2* src2 = reinterpret_cast<const double2*>(L11T);
+    double2* dst2 = reinterpret_cast<double2*>(sm);
+    const int nth = blockDim.x;
+    int f = tid;
+    for (; f + 7 * nth < t2; f += 8 * nth) {
+      double2 v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = __ldcg(src2 + f + u * nth);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) dst2[f + u * nth] = v[u];
+    }
+    for (; f < t2; f += nth) dst2[f] = __ldcg(src2 + f);
+    if ((tt & 1) && tid == 0) sm[tt - 1] = L11T[tt - 1];
+  }
   const int r = blockIdx.x * kYsolveWarps + warp;
   constexpr int kU = 6;  // t <= tpad <= 192 (L11 in smem limits t to ~170 anyway)
   double y[kU];
