@@ -269,9 +269,26 @@ __global__ void __launch_bounds__(kPanelThreads, 1) panel_kernel(PanelParams pin
 #pragma unroll
       for (int r = 0; r < kRegRows; ++r) rg[r] = (r < PRr) ? src[r] : 0.0;
     }
-    for (int f = tid; f < Ps * rcnt; f += nthr) {
-      int c = f / Ps, r = f - c * Ps;
-      bsm(PRr + r, c) = p.B[(size_t)(k0 + r0 + c) * P + PRr + r];
+    {  // sketch rows >= PRr of the owned columns: 8 independent loads in flight per thread
+      const int tot = Ps * rcnt;
+      int f = tid;
+      for (; f + 7 * nthr < tot; f += 8 * nthr) {
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int e = f + u * nthr, c = e / Ps, r = e - c * Ps;
+          v[u] = __ldcg(p.B + (size_t)(k0 + r0 + c) * P + PRr + r);
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int e = f + u * nthr, c = e / Ps, r = e - c * Ps;
+          bsm(PRr + r, c) = v[u];
+        }
+      }
+      for (; f < tot; f += nthr) {
+        const int c = f / Ps, r = f - c * Ps;
+        bsm(PRr + r, c) = p.B[(size_t)(k0 + r0 + c) * P + PRr + r];
+      }
     }
     if (!regmode)
       for (int c = tid; c < rcnt; c += nthr) qsel[c] = 0;
