@@ -35,7 +35,12 @@ constexpr int NBUF = RCP_WS_NBUF;  // C tile buffers (1: the epilogue drains til
 constexpr int kMmaWarps = RCP_WS_MMA_WARPS;  // 4: 64x32 warp tiles, 8: 32x32 warp tiles
 constexpr int kThreads = 32 * kMmaWarps + 128;
 constexpr int kProdThreads = 64, kEpiThreads = 64;
-constexpr int kCStride = BM + 1;
+#ifndef RCP_WS_CSTRIDE
+#define RCP_WS_CSTRIDE (BM + 2)
+#endif
+// C tile column stride: BM + 2 makes the MMA warps' accumulate (lanes g + 4q) bank-conflict free; the
+// epilogue's mirror reads then see 2-way conflicts (BM + 1 is the other way round)
+constexpr int kCStride = RCP_WS_CSTRIDE;
 
 struct Smem {
   double a[STAGES][BM][kBK + kPad];
