@@ -2,7 +2,6 @@
 // sketch projection and sketch correction.
 #include "gemm_dmma.cuh"
 #include "misc.cuh"
-#include "schur_kernel.cuh"
 #include "schur_ws.cuh"
 #include <algorithm>
 #include <type_traits>
@@ -67,9 +66,6 @@ bool aligned16(const void* p, int64_t ld) {
 
 cudaError_t gemm_init_attributes() {
   cudaError_t e;
-  e = cudaFuncSetAttribute(schur_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)schur_smem_bytes());
-  if (e != cudaSuccess) return e;
   e = cudaFuncSetAttribute(schur_ws_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)schur_ws_smem_bytes());
   if (e != cudaSuccess) return e;
@@ -112,7 +108,7 @@ cudaError_t launch_schur_update(int64_t n, int64_t k, int64_t mp, const double* 
     return cudaGetLastError();
   }
   if (mp <= 0 || K <= 0) return cudaSuccess;
-  const int64_t nbi = (mp + kSchurBM - 1) / kSchurBM;
+  const int64_t nbi = (mp + ws::BM - 1) / ws::BM;
   const long long tiles = nbi * (nbi + 1);  // row block I has 2I+2 column blocks of 64
   const int Kl = ((K + kBK - 1) / kBK) * kBK;  // operands are zero padded to tpad along K
   int dev = 0, sms = 148;

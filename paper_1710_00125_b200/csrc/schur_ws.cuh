@@ -84,16 +84,7 @@ RCP_D void mbar_wait(unsigned long long* b, unsigned parity) {
 #ifndef RCP_WS_ORDER
 #define RCP_WS_ORDER 2  // DMMA issue order inside a k-step: 2 = B fragment outer (measured -1.3 % at C3)
 #endif
-#ifndef RCP_SCHUR_STCS
-#define RCP_SCHUR_STCS 0
-#endif
-RCP_D void st_c(double* p, double v) {
-#if RCP_SCHUR_STCS
-  __stcs(p, v);
-#else
-  *p = v;
-#endif
-}
+RCP_D void st_c(double* p, double v) { *p = v; }  // (streaming stores measured: no difference)
 RCP_D void named_sync(int id, int nthreads) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory"); }
 
 RCP_D void tile_of(long long x, int64_t& m0, int64_t& n0) {
