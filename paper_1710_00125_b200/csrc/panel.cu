@@ -341,7 +341,8 @@ __global__ void __launch_bounds__(kPanelThreads, 1) panel_kernel(PanelParams pin
     // values bit-identical to applying each reflector eagerly.
     auto reflect_fused = [&](const double* vc, const double* vp, int jj, double coef, int skip) {
       double d0 = 0.0, d1 = 0.0, d2 = 0.0, d3 = 0.0;
-      if (!skip) {
+      const bool regs_live = jj < PRr;  // uniform: register rows are all finished once jj >= PRr
+      if (!skip && regs_live) {
 #pragma unroll
         for (int r = 0; r < kRegRows; r += 4) {
           if (r >= jj && r < PRr) d0 = __fma_rn(vc[r], rg[r], d0);
@@ -402,9 +403,11 @@ __global__ void __launch_bounds__(kPanelThreads, 1) panel_kernel(PanelParams pin
       double wv = 0.0;
       if (!skip) {
         wv = __dmul_rn(coef, __dadd_rn(__dadd_rn(d0, d1), __dadd_rn(d2, d3)));
+        if (regs_live) {
 #pragma unroll
-        for (int r2 = 0; r2 < kRegRows; ++r2)
-          if (r2 >= jj && r2 < PRr) rg[r2] = __fma_rn(-vc[r2], wv, rg[r2]);
+          for (int r2 = 0; r2 < kRegRows; ++r2)
+            if (r2 >= jj && r2 < PRr) rg[r2] = __fma_rn(-vc[r2], wv, rg[r2]);
+        }
       }
       double yj;
       if (jj < PRr) {
