@@ -498,7 +498,7 @@ __global__ void __launch_bounds__(kPanelThreads, 1) panel_kernel(PanelParams pin
         const int lane = tid & 31;
         const int hwarp = lb.slot < 0 ? -1 : (regmode ? (lb.slot >> 5) : 0);
         if ((tid >> 5) == hwarp) {
-          if (regmode && lane == (lb.slot & 31)) {
+          if (regmode && j < PRr && lane == (lb.slot & 31)) {
 #pragma unroll
             for (int r = 0; r < kRegRows; ++r)
               if (r >= j && r < PRr) vcur[r] = rg[r];
