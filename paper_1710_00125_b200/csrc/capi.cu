@@ -99,6 +99,10 @@ WorkerBufs carve_worker(unsigned char* b, int64_t n, const Layout& L) {
   return w;
 }
 
+#ifndef RCP_FUSED_SKETCH
+#define RCP_FUSED_SKETCH 1  // single GPU: the sketch correction runs as extra Schur tiles
+#endif
+
 int validate_cfg(const rcp_config* c, int64_t n) {
   if (!c || n < 1) return RCP_ERR_INVALID_ARG;
   if (c->p < 1 || c->b < 1 || c->robust_r < 0) return RCP_ERR_INVALID_ARG;
@@ -386,6 +390,11 @@ int rcp_factor_dist(const rcp_config* cfg, int64_t n, const double* a, int64_t l
       RCP_LAUNCH(launch_panel_commit(din, dout, dplog, dstate, n, c.b, q_eff, P, (long long)Lay.snap_cap, st));
       RCP_LAUNCH(launch_gather(n, 0, 0, 0, tpad, 0, pol, Lbuf, W, permb[pcur], permb[pcur ^ 1], snap, phys, Lneg, Wg,
                                L11c, st, din));
+      // sketch correction once per panel (factor.py:554-565): Y = B1 L11^-T, then B2 -= Y L21^T as
+      // extra tiles of the Schur kernel (single GPU) or as its own GEMM (multi-GPU)
+      const bool sketch_corr = rcp_strat && !q1;
+      const bool fused_sk = sketch_corr && world == 1 && RCP_FUSED_SKETCH;
+      if (fused_sk) RCP_LAUNCH(launch_ysolve(n, P, 0, c.b, tpad, pol, B[curB], L11c, Y, st, din));
       EventPair& es = new_pair(ev_schur);
       RCP_CHECK(cudaEventRecord(es.a, st));
       if (world > 1) {  // hand the panel to the other devices (dist.cuh)
@@ -395,10 +404,11 @@ int rcp_factor_dist(const rcp_config* cfg, int64_t n, const double* a, int64_t l
           RCP_LAUNCH(launch_worker_panel(dsh, r, world, dseq, A[0], A[1], ddesc, Lneg, Wg, phys, n, tpad,
                                          vworkers[r - 1], st));
       }
-      RCP_LAUNCH(launch_schur_update(n, 0, 0, Lneg, Wg, tpad, 0, A[curA], phys, A[curA ^ 1], st, din, 0, world));
+      RCP_LAUNCH(launch_schur_update(n, 0, 0, Lneg, Wg, tpad, 0, A[curA], phys, A[curA ^ 1], st, din, 0, world,
+                                     fused_sk ? Y : nullptr, B[curB], B[curB ^ 1], P));
       RCP_CHECK(cudaEventRecord(es.b, st));
       if (world > 1) RCP_LAUNCH(launch_dist_wait_done(dsh, world, dseq, st));
-      if (rcp_strat && !q1) {  // sketch correction once per panel (factor.py:554-565)
+      if (sketch_corr && !fused_sk) {
         RCP_LAUNCH(launch_ysolve(n, P, 0, c.b, tpad, pol, B[curB], L11c, Y, st, din));
         RCP_LAUNCH(launch_sketch_correction(P, n, 0, Y, tpad, c.b, Lneg, B[curB], phys, B[curB ^ 1], st, din, n));
       }
@@ -552,6 +562,8 @@ int rcp_factor_dist(const rcp_config* cfg, int64_t n, const double* a, int64_t l
       }
       if (mp > 0 && t > 0) {
         schur_flops += (double)t * (double)mp * (double)(mp + 1);
+        if (rcp_strat && !q1 && world == 1 && RCP_FUSED_SKETCH)  // sketch tiles in the same kernel
+          schur_flops += 2.0 * (double)P * (double)t * (double)mp;
         h_mul += (long long)t * (mp * (mp + 1) / 2);  // _apply_trailing (factor.py:377-378)
         h_add += (long long)t * (mp * (mp + 1) / 2);
         if (rcp_strat && !q1) {

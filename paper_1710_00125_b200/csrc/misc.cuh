@@ -31,7 +31,9 @@ cudaError_t launch_iota(int64_t n, int* p, cudaStream_t st);
 // A_out[k+i, k+j] = A_in(phys[i], phys[j]) - sum_s L[i,s] W[j,s]   for i >= j (lower tiles)
 cudaError_t launch_schur_update(int64_t n, int64_t k, int64_t mp, const double* Lneg, const double* Wg, int tpad,
                                 int K, const double* A_in, const int* phys, double* A_out, cudaStream_t st,
-                                const PanelDesc* d = nullptr, int part = 0, int nparts = 1);
+                                const PanelDesc* d = nullptr, int part = 0, int nparts = 1,
+                                const double* ysk = nullptr, const double* bin = nullptr, double* bout = nullptr,
+                                int P = 0);
 // multi-GPU worker: buffers / panel outcome resolved on the device (dist.cuh)
 cudaError_t launch_schur_update_dyn(int64_t n, const double* Lneg, const double* Wg, int tpad, const int* phys,
                                     const SchurDyn* dyn, int part, int nparts, cudaStream_t st);

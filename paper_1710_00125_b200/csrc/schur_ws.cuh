@@ -102,7 +102,12 @@ __global__ void __launch_bounds__(ws::kThreads, 1)
 schur_ws_kernel(const double* __restrict__ Lneg, const double* __restrict__ Wg, int tpad, int Kl,
                 const double* __restrict__ ain, double* __restrict__ aout, const int* __restrict__ phys, int64_t n,
                 int64_t k, int64_t mp, long long tiles, const PanelDesc* __restrict__ d, int part, int nparts,
-                const SchurDyn* __restrict__ dyn) {
+                const SchurDyn* __restrict__ dyn, const double* __restrict__ ysk = nullptr,
+                const double* __restrict__ bin = nullptr, double* __restrict__ bout = nullptr, int P = 0) {
+  // With ysk != nullptr (device-driven, single GPU) the sketch correction B2^T -= L21 Y^T
+  // (factor.py:554-565, Y = B1 L11^-T from ysolve) rides along as extra tiles after the lower
+  // triangle: A operand = the same -L21 rows, B operand = Y rows, C = the sketch columns
+  // gathered through the panel permutation (no mirror).
   using namespace ws;
   if (kMulti && dyn) {  // multi-GPU worker: buffers resolved on the device from rank 0's signal
     if (!dyn->go) return;
@@ -110,14 +115,29 @@ schur_ws_kernel(const double* __restrict__ Lneg, const double* __restrict__ Wg, 
     aout = dyn->aout;
     d = dyn->d;
   }
+  long long tiles_tri = tiles;
+  const int nbp = ysk ? (P + BN - 1) / BN : 0;  // sketch tiles per 128-row block
   if (d) {  // device-driven: the panel outcome comes from the committed descriptor
     if (!d->ok || d->t <= 0 || d->k_end >= n) return;
     k = d->k_end;
     mp = n - k;
     Kl = ((d->t + kBK - 1) / kBK) * kBK;
     const long long nbi = (mp + BM - 1) / BM;
-    tiles = nbi * (nbi + 1);
+    tiles_tri = nbi * (nbi + 1);
+    tiles = tiles_tri + nbi * nbp;
   }
+  // tile x: lower-triangle tile (returns false) or sketch tile (true): rows m0 of -L21, sketch
+  // rows n0 (of Y and B)
+  auto tile_at = [&](long long x, int64_t& m0, int64_t& n0) -> bool {
+    if (x < tiles_tri) {
+      tile_of(x, m0, n0);
+      return false;
+    }
+    const long long sx = x - tiles_tri;
+    m0 = (sx / nbp) * BM;
+    n0 = (sx % nbp) * BN;
+    return true;
+  };
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -217,9 +237,11 @@ schur_ws_kernel(const double* __restrict__ Lneg, const double* __restrict__ Wg, 
     unsigned stage = 0, ephase = 1;  // fresh "empty" barriers count as released
     for (long long x = x0; x < tiles; x += xs) {
       int64_t m0, n0;
-      tile_of(x, m0, n0);
+      const bool skt = tile_at(x, m0, n0);
       const double* ab = Lneg + (m0 + srow) * (int64_t)tpad + soff;
-      const double* bb = Wg + (n0 + srow) * (int64_t)tpad + soff;
+      const double* bsrc = skt ? ysk : Wg;
+      const int64_t blim = skt ? P : mp;
+      const double* bb = bsrc + (n0 + srow) * (int64_t)tpad + soff;
       const int64_t step = 8 * (int64_t)tpad;
       for (int kt = 0; kt < KT; ++kt) {
         mbar_wait(&sm.empty[stage], ephase);
@@ -231,8 +253,8 @@ schur_ws_kernel(const double* __restrict__ Lneg, const double* __restrict__ Wg, 
         }
 #pragma unroll
         for (int u = 0; u < BN / 8; ++u) {
-          const bool ok = n0 + srow + 8 * u < mp;
-          cp_async16(&sm.b[stage][srow + 8 * u][soff], ok ? bb + u * step + k0 : Wg, ok);
+          const bool ok = n0 + srow + 8 * u < blim;
+          cp_async16(&sm.b[stage][srow + 8 * u][soff], ok ? bb + u * step + k0 : Lneg, ok);
         }
         mbar_arrive_cpasync(&sm.full[stage]);
         if (++stage == STAGES) {
@@ -246,7 +268,16 @@ schur_ws_kernel(const double* __restrict__ Lneg, const double* __restrict__ Wg, 
     const int et = tid - 32 * kMmaWarps - 64;  // 0..63
     auto gather = [&](long long x, int b) {
       int64_t m0, n0;
-      tile_of(x, m0, n0);
+      if (tile_at(x, m0, n0)) {  // sketch tile: C(i, j) = B[n0 + j, phys[m0 + i]] (threads along j)
+        const bool col_ok = n0 + et < P;
+        for (int i = 0; i < BM; ++i) {
+          const int64_t gi = m0 + i;
+          const bool ok = col_ok && gi < mp;
+          cp_async8(&sm.c[b][et][i], ok ? bin + (n0 + et) + (int64_t)phys[gi] * P : bin, ok);
+        }
+        mbar_arrive_cpasync(&sm.cin[b]);
+        return;
+      }
       sm.colmap[b][et] = (n0 + et < mp) ? phys[n0 + et] : 0;
       named_sync(1, kEpiThreads);
 #pragma unroll
@@ -268,8 +299,18 @@ schur_ws_kernel(const double* __restrict__ Lneg, const double* __restrict__ Wg, 
     for (long long x = x0; x < tiles; x += xs, ++it) {
       const int b = it % NBUF;
       int64_t m0, n0;
-      tile_of(x, m0, n0);
+      const bool skt = tile_at(x, m0, n0);
       mbar_wait(&sm.accd[b], (it / NBUF) & 1);
+      if (skt) {  // corrected sketch columns k + m0 + i, rows n0 + j (threads along j)
+        if (n0 + et < P) {
+          const int imax = (int)(mp - m0 < BM ? mp - m0 : BM);
+          double* dst = bout + (n0 + et) + (k + m0) * (int64_t)P;
+          for (int i = 0; i < imax; ++i, dst += P) st_c(dst, sm.c[b][et][i]);
+        }
+        named_sync(1, kEpiThreads);
+        if (x + (long long)NBUF * xs < tiles) gather(x + (long long)NBUF * xs, b);
+        continue;
+      }
       // lower part: column n0+j, rows m0..m0+127 (threads along rows)
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
