@@ -134,10 +134,28 @@ cudaError_t launch_schur_update_dyn(int64_t n, const double* Lneg, const double*
 cudaError_t launch_sketch_gemm(int P, int64_t m, const double* omega, int64_t ldo, const double* A, int64_t lda,
                                double* B, int64_t col0, cudaStream_t st) {
   if (m <= 0) return cudaSuccess;
-  const int64_t tm = (P + 63) / 64, tn = (m + 127) / 128;
   OperandDesc a{omega, ldo, P, m};
   OperandDesc b{A, lda, m, m};
   SketchEpi epi{B, P, m, col0};
+  if (P <= 144 && aligned16(omega, ldo) && aligned16(A, lda) && (m % 2 == 0)) {
+    // one tile row over all P sketch rows (48 / 96 / 144), 64-column tiles: no padded MMA rows
+    auto one_row = [&](auto bm_tag) -> cudaError_t {
+      constexpr int BM = decltype(bm_tag)::value;
+      const int64_t tn = (m + 63) / 64;
+      RectMap map{tn, BM, 64};
+      cudaError_t e = cudaFuncSetAttribute(dmma_gemm_kernel<BM, 64, kRectStages, 2, RectMap, SketchEpi>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)gemm_smem_bytes<BM, 64, kRectStages>());
+      if (e != cudaSuccess) return e;
+      dmma_gemm_kernel<BM, 64, kRectStages, 2, RectMap, SketchEpi>
+          <<<(unsigned)tn, kGemmThreads, gemm_smem_bytes<BM, 64, kRectStages>(), st>>>(a, b, m, map, epi);
+      return cudaGetLastError();
+    };
+    if (P <= 48) return one_row(std::integral_constant<int, 48>{});
+    if (P <= 96) return one_row(std::integral_constant<int, 96>{});
+    return one_row(std::integral_constant<int, 144>{});
+  }
+  const int64_t tm = (P + 63) / 64, tn = (m + 127) / 128;
   RectMap map{tn, 64, 128};
   const size_t smem = gemm_smem_bytes<64, 128, kRectStages>();
   if (aligned16(omega, ldo) && aligned16(A, lda) && (m % 2 == 0)) {
