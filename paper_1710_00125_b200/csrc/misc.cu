@@ -30,28 +30,51 @@ __device__ double block_max(double v) {
 
 // Exact-symmetry / finiteness check (core.py:48-53, factor.py:278-281), max|A|
 // (factor.py:286) and copy into the workspace, 32x32 tiles.
+// One 32x32 tile pair per block: tile (I, J) with I >= J and its mirror (J, I), each read once
+// from the input and written once to the workspace; the exact-symmetry check compares the two in
+// shared memory (core.py:48-53), finiteness and max|A| on the way (factor.py:280-286).
 __global__ void validate_copy_kernel(const double* __restrict__ a, int64_t lda, int64_t n,
                                      double* __restrict__ out, int* flags, double* amax) {
-  __shared__ double tile[32][33];
-  const int64_t bi = (int64_t)blockIdx.y * 32, bj = (int64_t)blockIdx.x * 32;
+  __shared__ double tl[32][33];  // tile (I, J): tl[x][y] = a(bi + y, bj + x)  (x = column offset)
+  __shared__ double tu[32][33];  // tile (J, I): tu[x][y] = a(bj + y, bi + x)
+  const long long pid = blockIdx.x;
+  long long I = static_cast<long long>((sqrt(8.0 * (double)pid + 1.0) - 1.0) * 0.5);
+  while (I * (I + 1) / 2 > pid) --I;
+  while ((I + 1) * (I + 2) / 2 <= pid) ++I;
+  const long long J = pid - I * (I + 1) / 2;
+  const int64_t bi = I * 32, bj = J * 32;
   const int tx = threadIdx.x, ty = threadIdx.y;  // 32 x 8
-  // tile[x][y] = a(bj + x, bi + y): the mirrored block, loaded coalesced
-  for (int r = ty; r < 32; r += 8) {
-    int64_t i = bj + tx, j = bi + r;
-    tile[tx][r] = (i < n && j < n) ? a[i + j * lda] : 0.0;
-  }
-  __syncthreads();
   int asym = 0, nonfin = 0;
   double mx = 0.0;
-  for (int r = ty; r < 32; r += 8) {
-    int64_t i = bi + tx, j = bj + r;  // element (i, j), column-major index i + j*lda
-    if (i < n && j < n) {
-      double v = a[i + j * lda];
-      double m = tile[r][tx];  // a(j, i)
-      if (!(v == m)) asym = 1;
-      if (!isfinite(v)) nonfin = 1;
+  for (int r = ty; r < 32; r += 8) {  // coalesced along rows (tx) of column bj + r / bi + r
+    const int64_t il = bi + tx, jl = bj + r;
+    double v = 0.0;
+    if (il < n && jl < n) {
+      v = a[il + jl * lda];
+      out[il + jl * n] = v;
+      nonfin |= !isfinite(v);
       mx = fmax(mx, fabs(v));
-      out[i + j * n] = v;
+    }
+    tl[r][tx] = v;
+    if (I != J) {
+      const int64_t iu = bj + tx, ju = bi + r;
+      double w = 0.0;
+      if (iu < n && ju < n) {
+        w = a[iu + ju * lda];
+        out[iu + ju * n] = w;
+        nonfin |= !isfinite(w);
+        mx = fmax(mx, fabs(w));
+      }
+      tu[r][tx] = w;
+    }
+  }
+  __syncthreads();
+  for (int r = ty; r < 32; r += 8) {  // a(bi + tx, bj + r) vs a(bj + r, bi + tx)
+    const int64_t il = bi + tx, jl = bj + r;
+    if (il < n && jl < n) {
+      const double v = tl[r][tx];
+      const double m = (I != J) ? tu[tx][r] : tl[tx][r];
+      if (!(v == m)) asym = 1;
     }
   }
   if (asym) atomicOr(flags + 0, 1);
@@ -280,8 +303,9 @@ __global__ void iota_kernel(int64_t n, int* p) {
 // ------------------------------------------------------------------ launchers
 cudaError_t launch_validate_copy(const double* a, int64_t lda, int64_t n, double* out, int* flags, double* amax,
                                  cudaStream_t st) {
-  dim3 grid((unsigned)((n + 31) / 32), (unsigned)((n + 31) / 32)), block(32, 8);
-  validate_copy_kernel<<<grid, block, 0, st>>>(a, lda, n, out, flags, amax);
+  const long long nb = (n + 31) / 32;
+  dim3 block(32, 8);
+  validate_copy_kernel<<<(unsigned)(nb * (nb + 1) / 2), block, 0, st>>>(a, lda, n, out, flags, amax);
   return cudaGetLastError();
 }
 
