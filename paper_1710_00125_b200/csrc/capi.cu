@@ -226,6 +226,7 @@ int rcp_factor_dist(const rcp_config* cfg, int64_t n, const double* a, int64_t l
   int* poso = iptr(Lay.poso);
   int* snap = iptr(Lay.snap);
   PanelState* dstate = reinterpret_cast<PanelState*>(ws + Lay.state);
+  unsigned long long* tstamp = reinterpret_cast<unsigned long long*>(ws + Lay.tstamp);
   Scal* dscal = reinterpret_cast<Scal*>(ws + Lay.scal);
   const int P = c.p;
   const int tpad = Lay.tpad;
@@ -233,11 +234,20 @@ int rcp_factor_dist(const rcp_config* cfg, int64_t n, const double* a, int64_t l
   int dev = 0;
   RCP_CHECK(cudaGetDevice(&dev));
   int num_sms = 0, max_optin = 0;
-  RCP_CHECK(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev));
-  RCP_CHECK(cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
-  RCP_CHECK(panel_init_attributes(max_optin - panel_static_smem_bytes()));
-  RCP_CHECK(gemm_init_attributes());
-  const int smem_budget = max_optin - panel_static_smem_bytes() - 1024;
+  // device attributes and kernel smem limits once per device and thread (driver calls here can
+  // queue behind an NVML client such as a running nvidia-smi)
+  static thread_local int attr_dev = -1, attr_sms = 0, attr_optin = 0, attr_static = 0;
+  if (attr_dev != dev) {
+    RCP_CHECK(cudaDeviceGetAttribute(&attr_sms, cudaDevAttrMultiProcessorCount, dev));
+    RCP_CHECK(cudaDeviceGetAttribute(&attr_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    attr_static = panel_static_smem_bytes();
+    RCP_CHECK(panel_init_attributes(attr_optin - attr_static));
+    RCP_CHECK(gemm_init_attributes());
+    attr_dev = dev;
+  }
+  num_sms = attr_sms;
+  max_optin = attr_optin;
+  const int smem_budget = max_optin - attr_static - 1024;
 
   // pinned snapshots and CUDA events come from a per-thread cache (cudaMallocHost /
   // cudaFreeHost and event creation per call cost milliseconds of GPU idle time)
@@ -250,11 +260,6 @@ int rcp_factor_dist(const rcp_config* cfg, int64_t n, const double* a, int64_t l
   PanelState* hstate = hc.hstate;
   Scal* hscal = hc.hscal;
   cudaEvent_t ev_start = hc.event(), ev_stop = hc.event();
-  std::vector<EventPair> ev_panel, ev_schur;
-  auto new_pair = [&](std::vector<EventPair>& v) -> EventPair& {
-    v.push_back(EventPair{hc.event(), hc.event()});
-    return v.back();
-  };
 
   int64_t launches = 0;
   double schur_flops = 0.0;
@@ -266,6 +271,8 @@ int rcp_factor_dist(const rcp_config* cfg, int64_t n, const double* a, int64_t l
   init.err = LLONG_MAX;
   RCP_CHECK(cudaMemcpyAsync(dstate, &init, sizeof(init), cudaMemcpyHostToDevice, st));
   RCP_CHECK(cudaMemsetAsync(ws + Lay.xrec, 0, Lay.state - Lay.xrec, st));  // LL exchange buffers: no stale tags
+  RCP_CHECK(cudaMemsetAsync(ws + Lay.tstamp, 0, 8 * 4 * (size_t)(n + 2), st));
+  RCP_LAUNCH(launch_tstamp_init(reinterpret_cast<unsigned long long*>(ws + Lay.tstamp), 2 * (n + 2), st));
   RCP_CHECK(cudaMemsetAsync(dscal, 0, sizeof(Scal), st));
   if (world > 1 && emulate) RCP_CHECK(cudaMemsetAsync(dsh, 0, sizeof(DistShared), st));
   RCP_CHECK(cudaMemsetAsync(d_off, 0, sizeof(double) * n, st));
@@ -346,7 +353,8 @@ int rcp_factor_dist(const rcp_config* cfg, int64_t n, const double* a, int64_t l
   base.P = P;
   base.alpha = rcp_strat ? std::sqrt(2.0) / 2.0 : (1.0 + std::sqrt(17.0)) / 8.0;  // factor.py:299
   base.strategy = c.strategy;
-  base.bkscr = Lneg;  // free while a panel runs (the gather fills it afterwards)
+  base.bkscr = Lneg;
+  base.tstamp = tstamp;  // free while a panel runs (the gather fills it afterwards)
   base.q1 = q1 ? 1 : 0;
   base.qscr = dptr(Lay.qscr);
   base.Lbuf = Lbuf;
@@ -383,10 +391,7 @@ int rcp_factor_dist(const rcp_config* cfg, int64_t n, const double* a, int64_t l
       prm.B = B[curB];
       prm.Bout = B[curB ^ 1];
       prm.perm_cur = permb[pcur];
-      EventPair& ep = new_pair(ev_panel);
-      RCP_CHECK(cudaEventRecord(ep.a, st));
       RCP_LAUNCH(launch_panel(prm, gmax, (size_t)smem_budget, st));
-      RCP_CHECK(cudaEventRecord(ep.b, st));
       RCP_LAUNCH(launch_panel_commit(din, dout, dplog, dstate, n, c.b, q_eff, P, (long long)Lay.snap_cap, st));
       RCP_LAUNCH(launch_gather(n, 0, 0, 0, tpad, 0, pol, Lbuf, W, permb[pcur], permb[pcur ^ 1], snap, phys, Lneg, Wg,
                                L11c, st, din));
@@ -395,8 +400,6 @@ int rcp_factor_dist(const rcp_config* cfg, int64_t n, const double* a, int64_t l
       const bool sketch_corr = rcp_strat && !q1;
       const bool fused_sk = sketch_corr && world == 1 && RCP_FUSED_SKETCH;
       if (fused_sk) RCP_LAUNCH(launch_ysolve(n, P, 0, c.b, tpad, pol, B[curB], L11c, Y, st, din));
-      EventPair& es = new_pair(ev_schur);
-      RCP_CHECK(cudaEventRecord(es.a, st));
       if (world > 1) {  // hand the panel to the other devices (dist.cuh)
         ++dseq;
         RCP_LAUNCH(launch_dist_signal(dsh, dseq, curA, pidx & 1, st));
@@ -405,8 +408,7 @@ int rcp_factor_dist(const rcp_config* cfg, int64_t n, const double* a, int64_t l
                                          vworkers[r - 1], st));
       }
       RCP_LAUNCH(launch_schur_update(n, 0, 0, Lneg, Wg, tpad, 0, A[curA], phys, A[curA ^ 1], st, din, 0, world,
-                                     fused_sk ? Y : nullptr, B[curB], B[curB ^ 1], P));
-      RCP_CHECK(cudaEventRecord(es.b, st));
+                                     fused_sk ? Y : nullptr, B[curB], B[curB ^ 1], P, tstamp));
       if (world > 1) RCP_LAUNCH(launch_dist_wait_done(dsh, world, dseq, st));
       if (sketch_corr && !fused_sk) {
         RCP_LAUNCH(launch_ysolve(n, P, 0, c.b, tpad, pol, B[curB], L11c, Y, st, din));
@@ -605,22 +607,26 @@ int rcp_factor_dist(const rcp_config* cfg, int64_t n, const double* a, int64_t l
     float ms = 0.f;
     cudaEventElapsedTime(&ms, ev_start, ev_stop);
     stats->t_factor_ms = ms;
-    double tp = 0, ts = 0;
-    for (auto& e : ev_panel) {
-      float x = 0.f;
-      cudaEventElapsedTime(&x, e.a, e.b);
-      tp += x;
-    }
-    for (auto& e : ev_schur) {
-      float x = 0.f;
-      cudaEventElapsedTime(&x, e.a, e.b);
-      ts += x;
+    double tp = 0, ts = 0;  // kernel durations from the device timestamps (one copy)
+    {
+      const int np = hstate->panels_done + 2 < (int)n + 2 ? hstate->panels_done + 2 : (int)n + 2;
+      std::vector<unsigned long long> h(4 * (size_t)np);
+      if (cudaMemcpy(h.data(), tstamp, sizeof(unsigned long long) * h.size(), cudaMemcpyDeviceToHost) == cudaSuccess) {
+        for (int i = 0; i < np; ++i) {
+          const unsigned long long* q = &h[4 * (size_t)i];
+          if (q[0] != ~0ULL && q[1] > q[0]) tp += (double)(q[1] - q[0]) * 1e-6;
+          if (q[2] != ~0ULL && q[3] > q[2]) ts += (double)(q[3] - q[2]) * 1e-6;
+        }
+      }
     }
     stats->t_panel_ms = tp;
     stats->t_schur_ms = ts;
     stats->schur_flops = schur_flops;
-    int clk_khz = 0;
-    cudaDeviceGetAttribute(&clk_khz, cudaDevAttrClockRate, dev);
+    static thread_local int clk_khz = 0, clk_dev = -1;
+    if (clk_dev != dev) {
+      cudaDeviceGetAttribute(&clk_khz, cudaDevAttrClockRate, dev);
+      clk_dev = dev;
+    }
     for (int i = 0; i < 16; ++i) stats->panel_prof_ms[i] = clk_khz > 0 ? (double)hstate->cyc[i] / clk_khz : 0.0;
     stats->n_launches = launches;
     stats->mults = h_mul + hstate->cnt[0];

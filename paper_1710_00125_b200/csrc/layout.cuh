@@ -17,7 +17,7 @@ constexpr size_t kAlign = 256;
 inline size_t align_up(size_t x) { return (x + kAlign - 1) & ~(kAlign - 1); }
 
 struct Layout {
-  size_t A0, A1, Lbuf, W, Lneg, Wg, B0, B1, qscr, Y, L11, omega, phys, lop, pol, perm0, perm1, poso, snap, flags, xrec, qrec,
+  size_t A0, A1, Lbuf, W, Lneg, Wg, B0, B1, qscr, Y, L11, omega, phys, lop, pol, perm0, perm1, poso, snap, tstamp, flags, xrec, qrec,
       qcol, sdec, qdec, state, scal, desc, plog, dist, total;
   int64_t rows_pad, snap_cap;
   int tpad;
@@ -57,6 +57,7 @@ inline Layout make_layout(int64_t n, const rcp_config& c) {
   L.perm1 = take((size_t)n * 4);
   L.poso = take((size_t)n * 4);
   L.snap = take((size_t)L.snap_cap * 4);
+  L.tstamp = take(8 * 4 * (size_t)(n + 2));  // per panel: panel start/end, Schur start/end (ns)
   L.flags = take(0);
   L.xrec = take(8 * 2 * kMaxSMs * (size_t)kXWords);
   L.qrec = take(8 * 2 * kMaxSMs * (size_t)kQWords);

@@ -293,6 +293,11 @@ __global__ void mirror_lower_kernel(int64_t n, int64_t k, double* A) {
   }
 }
 
+__global__ void tstamp_init_kernel(unsigned long long* ts, int64_t count) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < count) ts[2 * i] = ~0ULL;  // start slots (atomicMin); end slots stay 0 (atomicMax)
+}
+
 __global__ void iota_kernel(int64_t n, int* p) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) p[i] = static_cast<int>(i);
@@ -306,6 +311,11 @@ cudaError_t launch_validate_copy(const double* a, int64_t lda, int64_t n, double
   const long long nb = (n + 31) / 32;
   dim3 block(32, 8);
   validate_copy_kernel<<<(unsigned)(nb * (nb + 1) / 2), block, 0, st>>>(a, lda, n, out, flags, amax);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_tstamp_init(unsigned long long* ts, int64_t count, cudaStream_t st) {
+  tstamp_init_kernel<<<(unsigned)((count + 255) / 256), 256, 0, st>>>(ts, count);
   return cudaGetLastError();
 }
 
@@ -329,8 +339,19 @@ cudaError_t launch_ysolve(int64_t n, int P, int k0, int t, int tpad, const int* 
                           const double* L11, double* Y, cudaStream_t st, const PanelDesc* d) {
   if (tpad > 192) return cudaErrorInvalidValue;  // register-resident rows: 6 entries per lane
   size_t smem = sizeof(double) * (size_t)t * t;  // t: an upper bound when d != nullptr
-  cudaError_t e = cudaFuncSetAttribute(ysolve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
+  static thread_local size_t smem_set = 0;  // raise the limit only when it grows (one driver call)
+  static thread_local int smem_dev = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev != smem_dev) {
+    smem_set = 0;
+    smem_dev = dev;
+  }
+  if (smem > smem_set) {
+    cudaError_t e = cudaFuncSetAttribute(ysolve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    smem_set = smem;
+  }
   ysolve_kernel<<<(unsigned)((P + kYsolveWarps - 1) / kYsolveWarps), 32 * kYsolveWarps, smem, st>>>(
       n, P, k0, t, tpad, phys_of_log, Bin, L11, Y, d);
   return cudaGetLastError();

@@ -10,6 +10,7 @@ struct SchurDyn;
 
 cudaError_t launch_validate_copy(const double* a, int64_t lda, int64_t n, double* out, int* flags, double* amax,
                                  cudaStream_t st);
+cudaError_t launch_tstamp_init(unsigned long long* ts, int64_t count, cudaStream_t st);
 cudaError_t launch_sketch_norm_max(const double* B, int P, int64_t ncols, double* out, cudaStream_t st);
 cudaError_t launch_gather(int64_t n, int k0, int k_end, int t, int tpad, int64_t rows_pad, const int* phys_of_log,
                           const double* Lbuf, const double* W, const int* perm_cur, int* perm_next, int* snap,
@@ -33,7 +34,7 @@ cudaError_t launch_schur_update(int64_t n, int64_t k, int64_t mp, const double* 
                                 int K, const double* A_in, const int* phys, double* A_out, cudaStream_t st,
                                 const PanelDesc* d = nullptr, int part = 0, int nparts = 1,
                                 const double* ysk = nullptr, const double* bin = nullptr, double* bout = nullptr,
-                                int P = 0);
+                                int P = 0, unsigned long long* tstamp = nullptr);
 // multi-GPU worker: buffers / panel outcome resolved on the device (dist.cuh)
 cudaError_t launch_schur_update_dyn(int64_t n, const double* Lneg, const double* Wg, int tpad, const int* phys,
                                     const SchurDyn* dyn, int part, int nparts, cudaStream_t st);

@@ -171,6 +171,8 @@ __global__ void __launch_bounds__(kPanelThreads, 1) panel_kernel(PanelParams pin
     if (!(g.qn > 0 || p.q1)) p.guard_mode = 0;
     if (cta >= g.G) return;
   }
+  unsigned long long* const ts_panel = (p.tstamp && p.desc) ? p.tstamp + 4 * (size_t)p.desc->pidx : nullptr;
+  stamp_start(ts_panel);
   const int64_t n = p.n;
   const int k0 = p.k0, P = p.P, R = p.R, G = p.G, Wn = p.Wn;
   const size_t QS = qcol_stride(P);  // LL words per candidate-column buffer
@@ -1640,6 +1642,8 @@ __global__ void __launch_bounds__(kPanelThreads, 1) panel_kernel(PanelParams pin
     }
   }
   if (prof) atomicAdd(reinterpret_cast<unsigned long long*>(&p.st->cyc[7]), (unsigned long long)(prof_now() - c_kernel0));
+  __syncthreads();
+  stamp_end(ts_panel ? ts_panel + 1 : nullptr);
 #undef PROF_BEGIN
 #undef PROF_END
 }

@@ -162,6 +162,7 @@ struct PanelParams {
   int b, q, num_sms, smem_budget;
   int strategy;  // RCP_STRATEGY_*: decision rule of the pivot steps
   double* bkscr;  // bbk: per-CTA global scratch (third column + W-row buffer), G * (R + Wn) doubles
+  unsigned long long* tstamp;  // [panel][4] timestamps (panel start/end, Schur start/end), or null
 };
 
 cudaError_t panel_init_attributes(int max_dyn_smem);

@@ -90,6 +90,21 @@ RCP_D double row_dot4(const double* __restrict__ lsm, int ldsm, int ls, const do
   return __dadd_rn(__dadd_rn(c0, c1), __dadd_rn(c2, c3));
 }
 
+// ---------------------------------------------------------------- device timestamps
+// Kernel durations are stamped on the device (%globaltimer, ns): the host then reads one array per
+// factorization instead of issuing a driver call per launch (which can queue behind NVML clients).
+RCP_D unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+RCP_D void stamp_start(unsigned long long* s) {
+  if (s && threadIdx.x == 0 && blockIdx.x == 0) atomicMin(s, gtimer());
+}
+RCP_D void stamp_end(unsigned long long* s) {
+  if (s && threadIdx.x == 0) atomicMax(s, gtimer());
+}
+
 // ---------------------------------------------------------------- argmax comparators
 // numpy argmax semantics: NaN wins (first NaN), otherwise largest value, ties to the
 // lowest index.

@@ -95,17 +95,18 @@ cudaError_t gemm_init_attributes() {
 cudaError_t launch_schur_update(int64_t n, int64_t k, int64_t mp, const double* Lneg, const double* Wg, int tpad,
                                 int K, const double* A_in, const int* phys, double* A_out, cudaStream_t st,
                                 const PanelDesc* d, int part, int nparts, const double* ysk, const double* bin,
-                                double* bout, int P) {
+                                double* bout, int P, unsigned long long* tstamp) {
   if (d) {  // persistent grid; the kernel reads the panel outcome
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (nparts > 1)
       schur_ws_kernel<true><<<(unsigned)sms, ws::kThreads, schur_ws_smem_bytes(), st>>>(
-          Lneg, Wg, tpad, 0, A_in, A_out, phys, n, 0, 0, 0, d, part, nparts, nullptr);
+          Lneg, Wg, tpad, 0, A_in, A_out, phys, n, 0, 0, 0, d, part, nparts, nullptr, nullptr, nullptr, nullptr, 0,
+          tstamp);
     else
       schur_ws_kernel<false><<<(unsigned)sms, ws::kThreads, schur_ws_smem_bytes(), st>>>(
-          Lneg, Wg, tpad, 0, A_in, A_out, phys, n, 0, 0, 0, d, part, nparts, nullptr, ysk, bin, bout, P);
+          Lneg, Wg, tpad, 0, A_in, A_out, phys, n, 0, 0, 0, d, part, nparts, nullptr, ysk, bin, bout, P, tstamp);
     return cudaGetLastError();
   }
   if (mp <= 0 || K <= 0) return cudaSuccess;

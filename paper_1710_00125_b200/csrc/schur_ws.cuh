@@ -103,7 +103,8 @@ schur_ws_kernel(const double* __restrict__ Lneg, const double* __restrict__ Wg, 
                 const double* __restrict__ ain, double* __restrict__ aout, const int* __restrict__ phys, int64_t n,
                 int64_t k, int64_t mp, long long tiles, const PanelDesc* __restrict__ d, int part, int nparts,
                 const SchurDyn* __restrict__ dyn, const double* __restrict__ ysk = nullptr,
-                const double* __restrict__ bin = nullptr, double* __restrict__ bout = nullptr, int P = 0) {
+                const double* __restrict__ bin = nullptr, double* __restrict__ bout = nullptr, int P = 0,
+                unsigned long long* __restrict__ tstamp = nullptr) {
   // With ysk != nullptr (device-driven, single GPU) the sketch correction B2^T -= L21 Y^T
   // (factor.py:554-565, Y = B1 L11^-T from ysolve) rides along as extra tiles after the lower
   // triangle: A operand = the same -L21 rows, B operand = Y rows, C = the sketch columns
@@ -138,6 +139,8 @@ schur_ws_kernel(const double* __restrict__ Lneg, const double* __restrict__ Wg, 
     n0 = (sx % nbp) * BN;
     return true;
   };
+  unsigned long long* const ts_schur = (tstamp && d) ? tstamp + 4 * (size_t)d->pidx + 2 : nullptr;
+  stamp_start(ts_schur);
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -337,6 +340,8 @@ schur_ws_kernel(const double* __restrict__ Lneg, const double* __restrict__ Wg, 
       if (x + (long long)NBUF * xs < tiles) gather(x + (long long)NBUF * xs, b);
     }
   }
+  __syncthreads();
+  stamp_end(ts_schur ? ts_schur + 1 : nullptr);
 }
 
 inline size_t schur_ws_smem_bytes() { return sizeof(ws::Smem); }
