@@ -338,7 +338,8 @@ def run_b200(args, rank: int, world: int, local_rank: int):
                      "frac": (achieved / (FP64_PEAK_GFLOPS / 1e3)) if achieved else None,
                      "traffic": ncu_traffic("schur_ws_kernel"),
                      "traffic_launch": ncu_traffic("schur_ws_kernel", detail=True),
-                     "algorithmic": "sum over panels of t*m*(m+1) flops (lower-triangle rank-t update)"
+                     "algorithmic": "sum over panels of t*m*(m+1) flops (lower-triangle rank-t update) + 2*P*t*m "
+                                    "for the sketch-correction tiles the same kernel runs (single GPU)"
                                     + (" (rank 0's share of the tiles; achieved over its Schur time)" if world > 1
                                        else ""),
                      "share_of_step": schur_ms / (ms * args.steps) if ms > 0 else None,
