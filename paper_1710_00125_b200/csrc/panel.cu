@@ -1600,13 +1600,20 @@ __global__ void __launch_bounds__(kPanelThreads, 1) panel_kernel(PanelParams pin
         wnext[s3] = __ldcg(p.W + rown + (int64_t)s3 * n);
       }
       const double an0 = (tid == 0) ? sym_at(A, n, rown, k0 + (kind == 2 ? pr : c0phys)) : 0.0;
-      const double an1 = (tid == 0 && kind == 3) ? sym_at(A, n, rown, k0 + pr) : 0.0;
+      const double an1 = (tid == 4 && kind == 3) ? sym_at(A, n, rown, k0 + pr) : 0.0;
       __syncthreads();
-      if (tid == 0) {
-        auto lrow = [&](int s3) { return lnext[s3]; };
-        const double v0 = __dsub_rn(an0, chain_dot4(lrow, kind == 2 ? (STRAT == 2 ? c0w : wrrow) : c0w, t));
-        wnext[t] = v0;
-        if (kind == 3) wnext[t + 1] = __dsub_rn(an1, chain_dot4(lrow, c1w, t));
+      if (tid < 32) {
+        // chain_dot4 split over lanes: lane q (q < 4) accumulates chain q of the c0 dot, lanes 4..7
+        // the c1 dot (2x2); same terms, same order, same ((c0+c1)+(c2+c3)) combination
+        const int q = tid & 3;
+        const double* wsel = (tid >= 4) ? c1w : (kind == 2 ? (STRAT == 2 ? c0w : wrrow) : c0w);
+        double c = 0.0;
+        if (tid < 8)
+          for (int s3 = q; s3 < t; s3 += 4) c = __fma_rn(lnext[s3], wsel[s3], c);
+        const double pr1 = __dadd_rn(c, __shfl_xor_sync(0xffffffffu, c, 1));
+        const double tot = __dadd_rn(pr1, __shfl_xor_sync(0xffffffffu, pr1, 2));
+        if (tid == 0) wnext[t] = __dsub_rn(an0, tot);
+        if (tid == 4 && kind == 3) wnext[t + 1] = __dsub_rn(an1, tot);
       }
       __syncthreads();
       for (int s3 = tid; s3 < tn; s3 += nthr) wrow[s3] = wnext[s3];
