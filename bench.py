@@ -286,7 +286,8 @@ def run_b200(args, rank: int, world: int, local_rank: int):
 
     # end to end through the public API: numpy in (pinned) -> Factorization out
     h2d = n * n * 8 + P * n * 8
-    d2h = n * n * 8 + n * (8 + 8 + 8 + 1)
+    # L: the 256-row block rows of its lower trapezoid (rcp_lower_to_host), then perm/D/pattern
+    d2h = sum((min(n, i0 + 256) - i0) * min(n, i0 + 256) for i0 in range(0, n, 256)) * 8 + n * (8 + 8 + 8 + 1)
     e2e_times = []
     for it in range(1 + max(1, args.e2e_steps)):  # first call untimed: pinned host buffers get allocated
         torch.cuda.synchronize()

@@ -170,6 +170,10 @@ size_t rcp_worker_workspace_bytes(int64_t n, const rcp_config* cfg);
 int rcp_dist_prepare(int64_t n, const rcp_config* cfg, void* workspace, void* cuda_stream);
 int rcp_schur_worker(const rcp_config* cfg, int64_t n, int rank, int world, void* rank0_workspace,
                      void* worker_ws, size_t worker_ws_bytes, void* cuda_stream);
+/* Dense host copy of a device unit-lower L (row-major n x n): the lower trapezoid is copied,
+ * the strictly upper part is written as zeros on the host; synchronises cuda_stream.
+ * Replaces the dense L transfer of the reference's result (factor.py:637-647 returns L dense). */
+int rcp_lower_to_host(int64_t n, const double* dL, double* hL, void* cuda_stream);
 int rcp_device_alloc(size_t bytes, void** ptr);
 int rcp_device_free(void* ptr);
 /* handle_out: 64 bytes (cudaIpcMemHandle_t); base must come from rcp_device_alloc. */

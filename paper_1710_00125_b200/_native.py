@@ -39,6 +39,7 @@ EXPORTED_SYMBOLS = (
     "rcp_solve_workspace_bytes",
     "rcp_reconstruct",
     "rcp_version",
+    "rcp_lower_to_host",
     "rcp_batched_workspace_bytes",
     "rcp_factor_batched",
     "rcp_solve_batched",
@@ -171,6 +172,8 @@ def load(path: str | os.PathLike | None = None):
     lib.rcp_dist_prepare.restype = ctypes.c_int
     lib.rcp_schur_worker.argtypes = [ctypes.POINTER(RcpConfig), i64, ctypes.c_int, ctypes.c_int, vp, vp, sz, vp]
     lib.rcp_schur_worker.restype = ctypes.c_int
+    lib.rcp_lower_to_host.argtypes = [i64, vp, vp, vp]
+    lib.rcp_lower_to_host.restype = ctypes.c_int
     lib.rcp_device_alloc.argtypes = [sz, ctypes.POINTER(ctypes.c_void_p)]
     lib.rcp_device_alloc.restype = ctypes.c_int
     lib.rcp_device_free.argtypes = [vp]

@@ -250,9 +250,14 @@ class DeviceFactorization:
 
     def to_host(self) -> Factorization:
         lh = None
-        if self.n >= 2048:  # D2H of the dense L into (cached) pinned memory, overlapped with the
-            lh = torch.empty(tuple(self.L.shape), dtype=torch.float64, pin_memory=True)  # host work below
-            lh.copy_(self.L, non_blocking=True)
+        if self.n >= 2048 and self.L.is_contiguous():
+            # L into (cached) pinned memory: only its lower trapezoid crosses PCIe, the host zeroes
+            # the strictly upper part meanwhile (rcp_lower_to_host)
+            lh = torch.empty(tuple(self.L.shape), dtype=torch.float64, pin_memory=True)
+            with torch.cuda.device(self.L.device):
+                status = _native.load().rcp_lower_to_host(self.n, self.L.data_ptr(), lh.data_ptr(), _stream())
+            if status != _native.RCP_OK:
+                raise RuntimeError(f"rcp_lower_to_host failed (status {status})")
         pattern = self.pattern.cpu().numpy().astype(np.int8)
         blocks = _blocks_from_arrays(self.d_diag.cpu().numpy(), self.d_off.cpu().numpy(), pattern)
         s = self.stats
@@ -260,7 +265,6 @@ class DeviceFactorization:
                             counters=OpCounters(*s["counters"]), recompute_count=s["recompute_count"])
         perm = self.perm.cpu().numpy().astype(np.int64)
         if lh is not None:
-            torch.cuda.current_stream(self.L.device).synchronize()
             L = lh.numpy()
         else:
             L = self.L.cpu().numpy()

@@ -13,6 +13,7 @@
 #include <cstdio>
 #include <cstring>
 #include <cstdlib>
+#include <thread>
 #include <vector>
 
 #include "../../include/rcp_b200.h"
@@ -679,6 +680,38 @@ int rcp_schur_worker(const rcp_config* cfg, int64_t n, int rank, int world, void
     if (hflags[1]) return RCP_ERR_CUDA;  // watchdog
     if (!hd.go) return RCP_OK;            // rank 0 finished
   }
+}
+
+int rcp_lower_to_host(int64_t n, const double* dL, double* hL, void* cuda_stream) {
+  // The unit-lower L (row-major n x n on the device) into a dense host array: block rows of the
+  // lower trapezoid go over PCIe as 2D copies (half the bytes of the dense matrix) while host
+  // threads zero the strictly upper part the copies do not cover (disjoint regions).
+  if (n < 0 || (n > 0 && (dL == nullptr || hL == nullptr))) return RCP_ERR_INVALID_ARG;
+  if (n == 0) return RCP_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
+  const int64_t blk = 256;
+  const size_t pitch = static_cast<size_t>(n) * sizeof(double);
+  for (int64_t i0 = 0; i0 < n; i0 += blk) {
+    const int64_t i1 = std::min(n, i0 + blk);
+    if (cudaMemcpy2DAsync(hL + i0 * n, pitch, dL + i0 * n, pitch, static_cast<size_t>(i1) * sizeof(double),
+                          static_cast<size_t>(i1 - i0), cudaMemcpyDeviceToHost, st) != cudaSuccess)
+      return RCP_ERR_CUDA;
+  }
+  const int64_t nb = (n + blk - 1) / blk;
+  unsigned hw = std::thread::hardware_concurrency();
+  const int nt = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>({(int64_t)(hw ? hw : 1), 16, nb})));
+  auto zero = [&](int tt) {
+    for (int64_t b = tt; b < nb; b += nt) {
+      const int64_t i0 = b * blk, i1 = std::min(n, i0 + blk);
+      if (i1 < n)
+        for (int64_t i = i0; i < i1; ++i) memset(hL + i * n + i1, 0, static_cast<size_t>(n - i1) * sizeof(double));
+    }
+  };
+  std::vector<std::thread> th;
+  for (int tt = 1; tt < nt; ++tt) th.emplace_back(zero, tt);
+  zero(0);
+  for (auto& x : th) x.join();
+  return cudaStreamSynchronize(st) == cudaSuccess ? RCP_OK : RCP_ERR_CUDA;
 }
 
 int rcp_device_alloc(size_t bytes, void** ptr) {

@@ -233,6 +233,29 @@ def test_large_panel_grid_reconstructs(cuda_ok):
     assert r <= 1e-13
 
 
+@pytest.mark.parametrize("n", [2048, 3001])
+def test_lower_to_host_is_exact(cuda_ok, n):
+    """to_host(): only L's lower trapezoid crosses PCIe, the host writes the upper zeros; the
+    result equals the device L exactly (including a ragged last block row)."""
+    import torch
+
+    from paper_1710_00125_b200 import api
+    g = torch.Generator(device="cuda").manual_seed(n)
+    lt = torch.tril(torch.randn(n, n, dtype=torch.float64, device="cuda", generator=g), -1)
+    lt += torch.eye(n, dtype=torch.float64, device="cuda")
+    dev = api.DeviceFactorization(perm=torch.arange(n, device="cuda"), L=lt,
+                                  d_diag=torch.ones(n, dtype=torch.float64, device="cuda"),
+                                  d_off=torch.zeros(n, dtype=torch.float64, device="cuda"),
+                                  pattern=torch.zeros(n, dtype=torch.int8, device="cuda"),
+                                  stats={"rho_cheap": 1.0, "max_multiplier": 1.0, "counters": (0, 0, 0, 0),
+                                         "recompute_count": 0})
+    # poison a pinned block of the same size so stale host contents would show
+    junk = torch.full((n, n), float("nan"), dtype=torch.float64, pin_memory=True)
+    del junk
+    f = dev.to_host()
+    assert np.array_equal(f.L, lt.cpu().numpy())
+
+
 def test_supplied_omega_with_guard_recompute(cuda_ok):
     """Omega passed in (its draw is skipped lazily): a guard recompute must still continue the
     same normal stream (g_c5_scaled recomputes once)."""
