@@ -136,6 +136,17 @@ int rcp_factor(const rcp_config* cfg, int64_t n, const double* a, int64_t lda,
                int8_t* trace_kind, int32_t* trace_r,
                rcp_stats* stats, void* cuda_stream);
 
+/* rcp_factor with L also delivered to L_host (pinned host memory, dense row-major n x n): block
+ * rows of L's lower trapezoid are copied while later panels still run, the strictly-upper part is
+ * zeroed on host threads; returns once L_host is complete.  The device outputs are as rcp_factor's.
+ * Serves randldl.factor's host result (factor.py:637-647: L is returned dense). */
+int rcp_factor_host_l(const rcp_config* cfg, int64_t n, const double* a, int64_t lda,
+                      const double* omega, rcp_draw_fn draw, void* draw_ctx,
+                      void* workspace, size_t workspace_bytes,
+                      int64_t* perm, double* L, double* d_diag, double* d_off, int8_t* pattern,
+                      int8_t* trace_kind, int32_t* trace_r,
+                      rcp_stats* stats, double* L_host, void* cuda_stream);
+
 /* x = P^T L^-T D^-1 L^-1 P b for nrhs right-hand sides (solve.py:69-92).
  * b and x are device, column-major n x nrhs (ld = n); may alias.  *singular is
  * set to 1 if an exact-zero block was met (solve.py:47-58). */

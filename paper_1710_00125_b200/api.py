@@ -239,6 +239,7 @@ class DeviceFactorization:
     stats: dict
     trace_kind: torch.Tensor | None = None
     trace_r: torch.Tensor | None = None
+    host_L: torch.Tensor | None = None  # pinned copy of L streamed during the factorization
 
     @property
     def n(self) -> int:
@@ -249,8 +250,8 @@ class DeviceFactorization:
                                    self.pattern.cpu().numpy())
 
     def to_host(self) -> Factorization:
-        lh = None
-        if self.n >= 2048 and self.L.is_contiguous():
+        lh = self.host_L
+        if lh is None and self.n >= 2048 and self.L.is_contiguous():
             # L into (cached) pinned memory: only its lower trapezoid crosses PCIe, the host zeroes
             # the strictly upper part meanwhile (rcp_lower_to_host)
             lh = torch.empty(tuple(self.L.shape), dtype=torch.float64, pin_memory=True)
@@ -350,7 +351,7 @@ def workspace_bytes(n: int, cfg: FactorConfig) -> int:
 def factor_device(a: torch.Tensor, cfg: FactorConfig | None = None, *, omega: torch.Tensor | None = None,
                   trace: bool = False, workspace: torch.Tensor | tuple | None = None,
                   out: DeviceFactorization | None = None, world: int = 1, emulate: bool = False,
-                  **overrides) -> DeviceFactorization:
+                  l_host: torch.Tensor | None = None, **overrides) -> DeviceFactorization:
     """Factor a CUDA float64 symmetric matrix; results stay on the device.
 
     ``omega`` (p x n, CUDA float64) may be passed pre-drawn; it must then be the
@@ -359,6 +360,8 @@ def factor_device(a: torch.Tensor, cfg: FactorConfig | None = None, *, omega: to
     raw ``(device_pointer, nbytes)`` pair).  ``world > 1`` shares every trailing update with
     ``world - 1`` other GPUs running :func:`paper_1710_00125_b200.dist.schur_worker`
     (``emulate=True``: their parts run on this device, for testing; results are identical).
+    ``l_host`` (pinned CPU float64 n x n, single GPU): L is also streamed into it while the
+    factorization runs (``rcp_factor_host_l``); :meth:`DeviceFactorization.to_host` then uses it.
     """
     cfg = _config(cfg, overrides)
     _check_supported(cfg)
@@ -409,13 +412,28 @@ def factor_device(a: torch.Tensor, cfg: FactorConfig | None = None, *, omega: to
         out.trace_kind = torch.empty(n, dtype=torch.int8, device=dev)
         out.trace_r = torch.empty(n, dtype=torch.int32, device=dev)
     st = _native.RcpStats()
-    status = lib.rcp_factor_dist(
-        ctypes.byref(c), n, a.data_ptr(), lda, 0 if omega is None else omega.data_ptr(), normals.cfunc, None,
-        ws_ptr, ws_bytes, out.perm.data_ptr(), out.L.data_ptr(),
-        out.d_diag.data_ptr(), out.d_off.data_ptr(), out.pattern.data_ptr(),
-        _ptr(out.trace_kind if trace else None), _ptr(out.trace_r if trace else None),
-        ctypes.byref(st), int(world), 1 if emulate else 0, _ptr(wws), 0 if wws is None else wws.numel(), _stream())
-    _raise_status(status, st)
+    if l_host is not None:
+        if world != 1 or l_host.dtype != torch.float64 or tuple(l_host.shape) != (n, n) \
+                or not l_host.is_pinned() or not l_host.is_contiguous():
+            raise ValueError("l_host must be a contiguous pinned float64 (n, n) tensor (single GPU)")
+        status = lib.rcp_factor_host_l(
+            ctypes.byref(c), n, a.data_ptr(), lda, 0 if omega is None else omega.data_ptr(), normals.cfunc, None,
+            ws_ptr, ws_bytes, out.perm.data_ptr(), out.L.data_ptr(),
+            out.d_diag.data_ptr(), out.d_off.data_ptr(), out.pattern.data_ptr(),
+            _ptr(out.trace_kind if trace else None), _ptr(out.trace_r if trace else None),
+            ctypes.byref(st), l_host.data_ptr(), _stream())
+        _raise_status(status, st)
+        out.host_L = l_host
+    else:
+        out.host_L = None
+        status = lib.rcp_factor_dist(
+            ctypes.byref(c), n, a.data_ptr(), lda, 0 if omega is None else omega.data_ptr(), normals.cfunc, None,
+            ws_ptr, ws_bytes, out.perm.data_ptr(), out.L.data_ptr(),
+            out.d_diag.data_ptr(), out.d_off.data_ptr(), out.pattern.data_ptr(),
+            _ptr(out.trace_kind if trace else None), _ptr(out.trace_r if trace else None),
+            ctypes.byref(st), int(world), 1 if emulate else 0, _ptr(wws), 0 if wws is None else wws.numel(),
+            _stream())
+        _raise_status(status, st)
     out.stats = {
         "rho_cheap": float(st.rho_cheap), "max_multiplier": float(st.max_multiplier),
         "amax": float(st.amax), "dmax": float(st.dmax), "recompute_count": int(st.recompute_count),
@@ -492,7 +510,10 @@ def factor(a: np.ndarray, cfg: FactorConfig | None = None, **overrides) -> Facto
     if cfg.strategy is Strategy.RCP:
         omega = torch.from_numpy(np.random.Generator(np.random.Philox(cfg.seed)).standard_normal((cfg.p, a.shape[0])))
         omega = omega.to(dev)
-    return factor_device(ad, cfg, omega=omega).to_host()
+    n = a.shape[0]
+    # L streams into pinned host memory while the factorization runs (rcp_factor_host_l)
+    lh = torch.empty((n, n), dtype=torch.float64, pin_memory=True) if n >= 2048 else None
+    return factor_device(ad, cfg, omega=omega, l_host=lh).to_host()
 
 
 def factor_robust(a: np.ndarray, cfg: FactorConfig | None = None, **overrides) -> Factorization:

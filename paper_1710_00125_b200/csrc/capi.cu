@@ -41,6 +41,7 @@ struct HostCache {
   Scal* hscal = nullptr;
   PanelDesc* hdesc = nullptr;   // 2 slots x 2 descriptors
   cudaEvent_t bev[2] = {nullptr, nullptr};
+  cudaStream_t cst = nullptr;  // copy stream of the host L sink (created on first use)
   std::vector<cudaEvent_t> pool;
   size_t used = 0;
   void reset() { used = 0; }
@@ -58,6 +59,8 @@ struct HostCache {
     used = 0;
     for (int i = 0; i < 2; ++i)
       if (bev[i]) cudaEventDestroy(bev[i]);
+    if (cst) cudaStreamDestroy(cst);
+    cst = nullptr;
     if (hstate) cudaFreeHost(hstate);
     if (hsnap) cudaFreeHost(hsnap);
     if (hscal) cudaFreeHost(hscal);
@@ -157,6 +160,61 @@ size_t rcp_worker_workspace_bytes(int64_t n, const rcp_config* cfg) {
   return align_up((size_t)L.rows_pad * L.tpad * 8) * 2 + align_up((size_t)n * 4) + align_up(sizeof(SchurDyn)) + kAlign;
 }
 
+// Host sink for L (pinned, dense row-major n x n): 256-row block rows of L's lower trapezoid go
+// over PCIe on a copy stream as soon as their rows are final, overlapping the rest of the
+// factorization; host threads zero the strictly-upper part the copies do not cover meanwhile.
+// The destructor joins the threads and drains the copy stream on every exit path.
+struct HostLSink {
+  static constexpr int64_t kBlk = 256;
+  double* h = nullptr;
+  const double* d = nullptr;
+  int64_t n = 0, sent = 0;
+  cudaStream_t cs = nullptr;
+  std::vector<std::thread> th;
+  bool failed = false;
+  void start(double* host, const double* dev, int64_t n_, cudaStream_t copy_stream) {
+    h = host;
+    d = dev;
+    n = n_;
+    cs = copy_stream;
+    const int64_t nb = (n + kBlk - 1) / kBlk;
+    unsigned hw = std::thread::hardware_concurrency();
+    const int nt = (int)std::max<int64_t>(1, std::min<int64_t>({(int64_t)(hw ? hw : 1) / 2, 8, nb}));
+    for (int tt = 0; tt < nt; ++tt)
+      th.emplace_back([this, tt, nt, nb]() {
+        for (int64_t b = tt; b < nb; b += nt) {
+          const int64_t i0 = b * kBlk, i1 = std::min(n, i0 + kBlk);
+          if (i1 < n)
+            for (int64_t i = i0; i < i1; ++i) memset(h + i * n + i1, 0, (size_t)(n - i1) * sizeof(double));
+        }
+      });
+  }
+  // copy the complete block rows below row `upto` (all rows when upto == n) once `ready` is done
+  void flush(int64_t upto, cudaEvent_t ready) {
+    if (!h || failed) return;
+    const int64_t lim = (upto >= n) ? n : (upto / kBlk) * kBlk;
+    if (lim <= sent) return;
+    if (cudaStreamWaitEvent(cs, ready, 0) != cudaSuccess) failed = true;
+    const size_t pitch = (size_t)n * sizeof(double);
+    while (!failed && sent < lim) {
+      const int64_t i0 = sent, i1 = std::min(n, i0 + kBlk);
+      if (cudaMemcpy2DAsync(h + i0 * n, pitch, d + i0 * n, pitch, (size_t)i1 * sizeof(double), (size_t)(i1 - i0),
+                            cudaMemcpyDeviceToHost, cs) != cudaSuccess)
+        failed = true;
+      sent = i1;
+    }
+  }
+  bool finish() {  // true when every block row arrived
+    for (auto& x : th) x.join();
+    th.clear();
+    if (!h) return true;
+    const bool ok = cudaStreamSynchronize(cs) == cudaSuccess && !failed && sent >= n;
+    h = nullptr;
+    return ok;
+  }
+  ~HostLSink() { finish(); }
+};
+
 int rcp_factor(const rcp_config* cfg, int64_t n, const double* a, int64_t lda, const double* omega_dev,
                rcp_draw_fn draw, void* draw_ctx, void* workspace, size_t workspace_bytes, int64_t* perm,
                double* Lout, double* d_diag, double* d_off, int8_t* pattern, int8_t* trace_kind, int32_t* trace_r,
@@ -165,11 +223,36 @@ int rcp_factor(const rcp_config* cfg, int64_t n, const double* a, int64_t lda, c
                          d_off, pattern, trace_kind, trace_r, stats, 1, 0, nullptr, 0, cuda_stream);
 }
 
+static int factor_core(const rcp_config* cfg, int64_t n, const double* a, int64_t lda, const double* omega_dev,
+                       rcp_draw_fn draw, void* draw_ctx, void* workspace, size_t workspace_bytes, int64_t* perm,
+                       double* Lout, double* d_diag, double* d_off, int8_t* pattern, int8_t* trace_kind,
+                       int32_t* trace_r, rcp_stats* stats, int world, int emulate, void* worker_ws,
+                       size_t worker_ws_bytes, void* cuda_stream, double* L_host);
+
 int rcp_factor_dist(const rcp_config* cfg, int64_t n, const double* a, int64_t lda, const double* omega_dev,
                     rcp_draw_fn draw, void* draw_ctx, void* workspace, size_t workspace_bytes, int64_t* perm,
                     double* Lout, double* d_diag, double* d_off, int8_t* pattern, int8_t* trace_kind,
                     int32_t* trace_r, rcp_stats* stats, int world, int emulate, void* worker_ws,
                     size_t worker_ws_bytes, void* cuda_stream) {
+  return factor_core(cfg, n, a, lda, omega_dev, draw, draw_ctx, workspace, workspace_bytes, perm, Lout, d_diag, d_off,
+                     pattern, trace_kind, trace_r, stats, world, emulate, worker_ws, worker_ws_bytes, cuda_stream,
+                     nullptr);
+}
+
+int rcp_factor_host_l(const rcp_config* cfg, int64_t n, const double* a, int64_t lda, const double* omega_dev,
+                      rcp_draw_fn draw, void* draw_ctx, void* workspace, size_t workspace_bytes, int64_t* perm,
+                      double* Lout, double* d_diag, double* d_off, int8_t* pattern, int8_t* trace_kind,
+                      int32_t* trace_r, rcp_stats* stats, double* L_host, void* cuda_stream) {
+  if (!L_host) return RCP_ERR_INVALID_ARG;
+  return factor_core(cfg, n, a, lda, omega_dev, draw, draw_ctx, workspace, workspace_bytes, perm, Lout, d_diag, d_off,
+                     pattern, trace_kind, trace_r, stats, 1, 0, nullptr, 0, cuda_stream, L_host);
+}
+
+static int factor_core(const rcp_config* cfg, int64_t n, const double* a, int64_t lda, const double* omega_dev,
+                       rcp_draw_fn draw, void* draw_ctx, void* workspace, size_t workspace_bytes, int64_t* perm,
+                       double* Lout, double* d_diag, double* d_off, int8_t* pattern, int8_t* trace_kind,
+                       int32_t* trace_r, rcp_stats* stats, int world, int emulate, void* worker_ws,
+                       size_t worker_ws_bytes, void* cuda_stream, double* L_host) {
   if (stats) {
     memset(stats, 0, sizeof(*stats));
     stats->deficient_from = -1;
@@ -379,6 +462,17 @@ int rcp_factor_dist(const rcp_config* cfg, int64_t n, const double* a, int64_t l
   base.num_sms = sms_cap;
   base.smem_budget = smem_budget;
 
+  // L in final order is written row block by row block as panels commit (finalize_rows after
+  // each gather); its strictly-upper part stays zero
+  double* lorig = dptr(Lay.lorig);
+  RCP_CHECK(cudaMemsetAsync(Lout, 0, sizeof(double) * (size_t)n * n, st));
+  RCP_LAUNCH(launch_unit_diag(n, Lout, st));
+  HostLSink hsink;
+  if (L_host) {
+    if (!hc.cst) RCP_CHECK(cudaStreamCreateWithFlags(&hc.cst, cudaStreamNonBlocking));
+    hsink.start(L_host, Lout, n, hc.cst);
+  }
+
   while (!chain_done) {
     for (int bi = 0; bi < batch; ++bi) {
       hist.push_back(Hist{curA, curB, pcur});
@@ -395,7 +489,8 @@ int rcp_factor_dist(const rcp_config* cfg, int64_t n, const double* a, int64_t l
       RCP_LAUNCH(launch_panel(prm, gmax, (size_t)smem_budget, st));
       RCP_LAUNCH(launch_panel_commit(din, dout, dplog, dstate, n, c.b, q_eff, P, (long long)Lay.snap_cap, st));
       RCP_LAUNCH(launch_gather(n, 0, 0, 0, tpad, 0, pol, Lbuf, W, permb[pcur], permb[pcur ^ 1], snap, phys, Lneg, Wg,
-                               L11c, st, din));
+                               L11c, st, din, lorig));
+      RCP_LAUNCH(launch_finalize_rows(n, 0, 0, 0, 0, perm, lorig, L11c, Lout, &dscal->maxmult, c.b + 2, st, din));
       // sketch correction once per panel (factor.py:554-565): Y = B1 L11^-T, then B2 -= Y L21^T as
       // extra tiles of the Schur kernel (single GPU) or as its own GEMM (multi-GPU)
       const bool sketch_corr = rcp_strat && !q1;
@@ -441,6 +536,7 @@ int rcp_factor_dist(const rcp_config* cfg, int64_t n, const double* a, int64_t l
     RCP_CHECK(cudaEventSynchronize(hc.bev[chk]));
     *hstate = hsnap[chk];
     if (hstate->status == 0 && hstate->err == LLONG_MAX) {
+      hsink.flush(hstate->k_end, hc.bev[chk]);  // rows before k_end are final in Lout
       // the descriptor after that batch's last panel decides whether the chain went on
       if (!hdesc[2 * chk + (batch_end[chk] & 1)].run) {
         chain_done = true;  // k == n; the newer batch is all no-ops
@@ -578,18 +674,19 @@ int rcp_factor_dist(const rcp_config* cfg, int64_t n, const double* a, int64_t l
   }
 
   // ---- assemble L in final order + statistics (factor.py:514-538)
-  RCP_CHECK(cudaMemsetAsync(Lout, 0, sizeof(double) * (size_t)n * n, st));
-  RCP_LAUNCH(launch_unit_diag(n, Lout, st));
-  for (const PanelRecord& pr : panels) {
-    RCP_LAUNCH(launch_assemble_panel(n, pr.k0, pr.k_end, snap + pr.snap_off, poso, perm, Lbuf, Lout,
-                                    &dscal->maxmult, st));
-    ++launches;  // assemble = invert + gather kernels
+  if (stop_k0 > 0) {  // rows of a deficient tail: the committed columns (factor.py:405-410)
+    RCP_LAUNCH(launch_finalize_rows(n, stop_k0, n, stop_k0, 0, perm, lorig, nullptr, Lout, &dscal->maxmult, 0, st));
   }
   RCP_LAUNCH(launch_dmax(n, d_diag, d_off, &dscal->dmax, st));
   RCP_CHECK(cudaEventRecord(ev_stop, st));
+  hsink.flush(n, ev_stop);  // the remaining block rows (tail included)
   RCP_CHECK(cudaMemcpyAsync(hscal, dscal, sizeof(Scal), cudaMemcpyDeviceToHost, st));
   RCP_CHECK(cudaMemcpyAsync(hstate, dstate, sizeof(PanelState), cudaMemcpyDeviceToHost, st));
   RCP_CHECK(cudaStreamSynchronize(st));
+  if (!hsink.finish()) {
+    if (stats) snprintf(stats->message, sizeof(stats->message), "host L copy failed");
+    return RCP_ERR_CUDA;
+  }
 
   if (stats) {
     stats->amax = amax;

@@ -17,7 +17,7 @@ constexpr size_t kAlign = 256;
 inline size_t align_up(size_t x) { return (x + kAlign - 1) & ~(kAlign - 1); }
 
 struct Layout {
-  size_t A0, A1, Lbuf, W, Lneg, Wg, B0, B1, qscr, Y, L11, omega, phys, lop, pol, perm0, perm1, poso, snap, tstamp, flags, xrec, qrec,
+  size_t A0, A1, Lbuf, lorig, W, Lneg, Wg, B0, B1, qscr, Y, L11, omega, phys, lop, pol, perm0, perm1, poso, snap, tstamp, flags, xrec, qrec,
       qcol, sdec, qdec, state, scal, desc, plog, dist, total;
   int64_t rows_pad, snap_cap;
   int tpad;
@@ -41,6 +41,7 @@ inline Layout make_layout(int64_t n, const rcp_config& c) {
   L.A0 = take(nn * 8);
   L.A1 = take(nn * 8);
   L.Lbuf = take(nn * 8);
+  L.lorig = take(nn * 8);  // L rows by original index, filled panel by panel (final-row assembly)
   L.W = take((size_t)n * (c.b + 2) * 8);
   L.Lneg = take((size_t)L.rows_pad * L.tpad * 8);
   L.Wg = take((size_t)L.rows_pad * L.tpad * 8);

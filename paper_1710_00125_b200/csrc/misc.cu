@@ -109,13 +109,15 @@ __global__ void sketch_norm_max_kernel(const double* __restrict__ B, int P, int6
 //   Lneg[j][s]     = -L(panel col s) at that row   (K-contiguous, ld tpad, zero padded)
 //   Wg[j][s]       =  W(panel col s) at that row
 //   perm_next      = original index per new logical position
-//   snap[x]        = perm at the panel start (for the final L assembly)
+//   snap[x]        = perm at the panel start
+//   lorig[o][k0+s] =  L(panel col s) of the still-active row with original index o (row-major by
+//                     original index; finalize_rows_kernel reads a row once it is pivoted)
 __global__ void gather_kernel(int64_t n, int k0, int k_end, int t, int tpad, int64_t rows_pad,
                               const int* __restrict__ phys_of_log, const double* __restrict__ Lbuf,
                               const double* __restrict__ W, const int* __restrict__ perm_cur,
                               int* __restrict__ perm_next, int* __restrict__ snap,
                               int* __restrict__ phys, double* __restrict__ Lneg, double* __restrict__ Wg,
-                              double* __restrict__ L11, const PanelDesc* __restrict__ d) {
+                              double* __restrict__ L11, const PanelDesc* __restrict__ d, double* __restrict__ lorig) {
   if (d) {  // device-driven: panel geometry from the committed descriptor
     if (!d->ok) return;
     k0 = d->k0;
@@ -142,11 +144,14 @@ __global__ void gather_kernel(int64_t n, int k0, int k_end, int t, int tpad, int
   for (int64_t j = (int64_t)blockIdx.x * blockDim.y + threadIdx.y; j < jend; j += stride) {
     const bool live = j < mp;
     const int pj = live ? phys_of_log[k_end + j] : 0;
+    double* lo = (live && lorig) ? lorig + (int64_t)perm_cur[pj] * n + k0 : nullptr;
     if (j < rows_pad) for (int s = threadIdx.x; s < tpad; s += blockDim.x) {
       double lv = 0.0, wv = 0.0;
       if (live && s < t) {
-        lv = -Lbuf[pj + (int64_t)(k0 + s) * n];
+        const double lb = Lbuf[pj + (int64_t)(k0 + s) * n];
+        lv = -lb;
         wv = W[pj + (int64_t)s * n];
+        if (lo) lo[s] = lb;
       }
       Lneg[j * tpad + s] = lv;
       Wg[j * tpad + s] = wv;
@@ -251,6 +256,37 @@ __global__ void assemble_panel_kernel(int64_t n, int k0, int k_end, const int64_
   if (threadIdx.x == 0) atomic_max_nonneg(maxmult, bm);
 }
 
+// Final rows [ra, rb) of L (row-major, final order), written once each row's position is decided:
+// L[i, c] = lorig[perm[i]][c] for c < min(i, kp) (the columns of earlier panels, scattered by their
+// gathers while the row was active) and, with L11T (the panel [kp, rb) that pivoted these rows),
+// the panel's own strictly-lower block for c in [kp, i).  Device-driven (d): the committed panel.
+// Same values as the reference's L (factor.py:339-340, 514-538); max |L| for the statistics.
+__global__ void finalize_rows_kernel(int64_t n, int64_t ra, int64_t rb, int64_t kp, int t, const int64_t* __restrict__ perm,
+                                     const double* __restrict__ lorig, const double* __restrict__ L11T,
+                                     double* __restrict__ L, double* maxmult, const PanelDesc* __restrict__ d) {
+  if (d) {
+    if (!d->ok) return;
+    ra = kp = d->k0;
+    rb = d->k_end;
+    t = d->t;
+  }
+  double mx = 0.0;
+  const int64_t cstep = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = ra + blockIdx.y; i < rb; i += gridDim.y) {
+    const double* src = lorig + perm[i] * n;
+    double* dst = L + i * n;
+    const int64_t cl = i < kp ? i : kp;
+    const int64_t ce = L11T ? i : cl;
+    for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < ce; c += cstep) {
+      const double v = (c < cl) ? __ldcs(src + c) : L11T[(c - kp) * t + (i - kp)];
+      dst[c] = v;
+      mx = fmax(mx, fabs(v));
+    }
+  }
+  const double bm = block_max(mx);
+  if (threadIdx.x == 0) atomic_max_nonneg(maxmult, bm);
+}
+
 __global__ void unit_diag_kernel(int64_t n, double* L) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) L[i * n + i] = 1.0;
@@ -326,12 +362,23 @@ cudaError_t launch_sketch_norm_max(const double* B, int P, int64_t ncols, double
 
 cudaError_t launch_gather(int64_t n, int k0, int k_end, int t, int tpad, int64_t rows_pad, const int* phys_of_log,
                           const double* Lbuf, const double* W, const int* perm_cur, int* perm_next, int* snap,
-                          int* phys, double* Lneg, double* Wg, double* L11, cudaStream_t st, const PanelDesc* d) {
+                          int* phys, double* Lneg, double* Wg, double* L11, cudaStream_t st, const PanelDesc* d,
+                          double* lorig) {
   dim3 block(32, 8);
   int64_t rows = rows_pad > (n - k0) ? rows_pad : (n - k0);
   unsigned grid = (unsigned)std::min<int64_t>((rows + 7) / 8, 148 * 16);
   gather_kernel<<<grid, block, 0, st>>>(n, k0, k_end, t, tpad, rows_pad, phys_of_log, Lbuf, W, perm_cur,
-                                        perm_next, snap, phys, Lneg, Wg, L11, d);
+                                        perm_next, snap, phys, Lneg, Wg, L11, d, lorig);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_finalize_rows(int64_t n, int64_t ra, int64_t rb, int64_t kp, int t, const int64_t* perm,
+                                 const double* lorig, const double* L11T, double* L, double* maxmult,
+                                 int max_rows, cudaStream_t st, const PanelDesc* d) {
+  if (!d && rb <= ra) return cudaSuccess;
+  const int64_t rows = d ? max_rows : rb - ra;
+  dim3 grid((unsigned)std::min<int64_t>((n + 255) / 256, 16), (unsigned)std::min<int64_t>(std::max<int64_t>(rows, 1), 1024));
+  finalize_rows_kernel<<<grid, 256, 0, st>>>(n, ra, rb, kp, t, perm, lorig, L11T, L, maxmult, d);
   return cudaGetLastError();
 }
 

@@ -15,7 +15,10 @@ cudaError_t launch_sketch_norm_max(const double* B, int P, int64_t ncols, double
 cudaError_t launch_gather(int64_t n, int k0, int k_end, int t, int tpad, int64_t rows_pad, const int* phys_of_log,
                           const double* Lbuf, const double* W, const int* perm_cur, int* perm_next, int* snap,
                           int* phys, double* Lneg, double* Wg, double* L11, cudaStream_t st,
-                          const PanelDesc* d = nullptr);
+                          const PanelDesc* d = nullptr, double* lorig = nullptr);
+cudaError_t launch_finalize_rows(int64_t n, int64_t ra, int64_t rb, int64_t kp, int t, const int64_t* perm,
+                                 const double* lorig, const double* L11T, double* L, double* maxmult,
+                                 int max_rows, cudaStream_t st, const PanelDesc* d = nullptr);
 cudaError_t launch_ysolve(int64_t n, int P, int k0, int t, int tpad, const int* phys_of_log, const double* Bin,
                           const double* L11, double* Y, cudaStream_t st, const PanelDesc* d = nullptr);
 cudaError_t launch_assemble_panel(int64_t n, int k0, int k_end, const int* snap, int* pos_of_orig,

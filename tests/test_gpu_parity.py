@@ -256,6 +256,29 @@ def test_lower_to_host_is_exact(cuda_ok, n):
     assert np.array_equal(f.L, lt.cpu().numpy())
 
 
+@pytest.mark.parametrize("n,rank,robust", [(2500, 2500, False), (2300, 1500, True)])
+def test_streamed_host_l_matches_device(cuda_ok, n, rank, robust):
+    """factor(numpy) at n >= 2048 streams L into pinned memory while later panels run
+    (rcp_factor_host_l): bit-identical to the device L, incl. a ragged last block row and the
+    rows of a deficient tail (guarded, rank-deficient input)."""
+    import torch
+
+    from paper_1710_00125_b200 import api, gallery
+    a = np.zeros((n, n))
+    a[:rank, :rank] = gallery.type6(rank, 7)
+    cfg = api.FactorConfig(strategy="rcp", b=64, q=64, p=80, seed=3, robust_r=1 if robust else 0)
+    f = api.factor(a, cfg)
+    d = api.factor_device(torch.from_numpy(a).cuda(), cfg)
+    assert np.array_equal(f.perm, d.perm.cpu().numpy())
+    assert np.array_equal(f.L, d.L.cpu().numpy())
+    assert np.array_equal(np.triu(f.L, 1), np.zeros((n, n)))
+    assert np.all(np.diag(f.L) == 1.0)
+    if robust:
+        assert f.deficient_from is not None and 0 < f.deficient_from < n
+    rec = f.L @ f.D.to_dense() @ f.L.T
+    assert float(np.abs(rec - a[np.ix_(f.perm, f.perm)]).max()) / float(np.abs(a).max()) <= 1e-11
+
+
 def test_supplied_omega_with_guard_recompute(cuda_ok):
     """Omega passed in (its draw is skipped lazily): a guard recompute must still continue the
     same normal stream (g_c5_scaled recomputes once)."""
