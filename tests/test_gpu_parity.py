@@ -256,8 +256,11 @@ def test_lower_to_host_is_exact(cuda_ok, n):
     assert np.array_equal(f.L, lt.cpu().numpy())
 
 
-@pytest.mark.parametrize("n,rank,robust", [(2500, 2500, False), (2300, 1500, True)])
-def test_streamed_host_l_matches_device(cuda_ok, n, rank, robust):
+@pytest.mark.parametrize("n,rank,robust,kw", [(2500, 2500, False, {}), (2300, 1500, True, {}),
+                                              (2200, 2200, False, {"q": 1, "p": 12}),
+                                              (2100, 2100, False, {"strategy": "bkpp", "q": 1, "p": 5}),
+                                              (2049, 2049, False, {"strategy": "bbk", "q": 1, "p": 5})])
+def test_streamed_host_l_matches_device(cuda_ok, n, rank, robust, kw):
     """factor(numpy) at n >= 2048 streams L into pinned memory while later panels run
     (rcp_factor_host_l): bit-identical to the device L, incl. a ragged last block row and the
     rows of a deficient tail (guarded, rank-deficient input)."""
@@ -266,7 +269,8 @@ def test_streamed_host_l_matches_device(cuda_ok, n, rank, robust):
     from paper_1710_00125_b200 import api, gallery
     a = np.zeros((n, n))
     a[:rank, :rank] = gallery.type6(rank, 7)
-    cfg = api.FactorConfig(strategy="rcp", b=64, q=64, p=80, seed=3, robust_r=1 if robust else 0)
+    cfg = api.FactorConfig(**{"strategy": "rcp", "b": 64, "q": 64, "p": 80, "seed": 3,
+                              "robust_r": 1 if robust else 0, **kw})
     f = api.factor(a, cfg)
     d = api.factor_device(torch.from_numpy(a).cuda(), cfg)
     assert np.array_equal(f.perm, d.perm.cpu().numpy())
