@@ -285,9 +285,11 @@ def run_b200(args, rank: int, world: int, local_rank: int):
         bwd = resid / (float(a_dev.abs().sum(dim=1).max()) * float(x.abs().max()))
 
     # end to end through the public API: numpy in (pinned) -> Factorization out
-    h2d = n * n * 8 + P * n * 8
-    # L: the 256-row block rows of its lower trapezoid (rcp_lower_to_host), then perm/D/pattern
-    d2h = sum((min(n, i0 + 256) - i0) * min(n, i0 + 256) for i0 in range(0, n, 256)) * 8 + n * (8 + 8 + 8 + 1)
+    # A (single GPU: the 256-row block rows of its lower trapezoid, rcp_factor_host) + Omega;
+    # L: the block rows of its lower trapezoid, then perm/D/pattern
+    trap = sum((min(n, i0 + 256) - i0) * min(n, i0 + 256) for i0 in range(0, n, 256)) * 8
+    h2d = (trap if world == 1 else n * n * 8) + P * n * 8
+    d2h = trap + n * (8 + 8 + 8 + 1)
     e2e_times = []
     for it in range(1 + max(1, args.e2e_steps)):  # first call untimed: pinned host buffers get allocated
         torch.cuda.synchronize()

@@ -147,6 +147,19 @@ int rcp_factor_host_l(const rcp_config* cfg, int64_t n, const double* a, int64_t
                       int8_t* trace_kind, int32_t* trace_r,
                       rcp_stats* stats, double* L_host, void* cuda_stream);
 
+/* rcp_factor from a HOST matrix (row-major n x n, ld lda; pinned for full PCIe speed): only its
+ * lower trapezoid is copied to the device (the kernel mirrors it) while host threads check the
+ * exact symmetry of the whole matrix (core.py:48-53; reported first, as the reference does).
+ * omega may be NULL for RCP_STRATEGY_RCP: Omega is then the first draw of `draw`, taken while
+ * the copies run.  L_host (optional, pinned, dense n x n) receives L as in rcp_factor_host_l.
+ * Serves randldl.factor(a) on a host array (factor.py:637-647). */
+int rcp_factor_host(const rcp_config* cfg, int64_t n, const double* a_host, int64_t lda,
+                    const double* omega, rcp_draw_fn draw, void* draw_ctx,
+                    void* workspace, size_t workspace_bytes,
+                    int64_t* perm, double* L, double* d_diag, double* d_off, int8_t* pattern,
+                    int8_t* trace_kind, int32_t* trace_r,
+                    rcp_stats* stats, double* L_host, void* cuda_stream);
+
 /* x = P^T L^-T D^-1 L^-1 P b for nrhs right-hand sides (solve.py:69-92).
  * b and x are device, column-major n x nrhs (ld = n); may alias.  *singular is
  * set to 1 if an exact-zero block was met (solve.py:47-58). */

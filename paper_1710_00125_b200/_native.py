@@ -36,6 +36,7 @@ EXPORTED_SYMBOLS = (
     "rcp_workspace_bytes",
     "rcp_factor",
     "rcp_factor_host_l",
+    "rcp_factor_host",
     "rcp_solve",
     "rcp_solve_workspace_bytes",
     "rcp_reconstruct",
@@ -153,6 +154,9 @@ def load(path: str | os.PathLike | None = None):
     lib.rcp_factor_host_l.argtypes = [ctypes.POINTER(RcpConfig), i64, vp, i64, vp, DRAW_FN, vp, vp, sz,
                                       vp, vp, vp, vp, vp, vp, vp, ctypes.POINTER(RcpStats), vp, vp]
     lib.rcp_factor_host_l.restype = ctypes.c_int
+    lib.rcp_factor_host.argtypes = [ctypes.POINTER(RcpConfig), i64, vp, i64, vp, DRAW_FN, vp, vp, sz,
+                                    vp, vp, vp, vp, vp, vp, vp, ctypes.POINTER(RcpStats), vp, vp]
+    lib.rcp_factor_host.restype = ctypes.c_int
     lib.rcp_solve.argtypes = [i64, vp, vp, vp, vp, vp, i64, vp, vp, vp, sz, ctypes.POINTER(ctypes.c_int32), vp]
     lib.rcp_solve.restype = ctypes.c_int
     lib.rcp_solve_workspace_bytes.argtypes = [i64, i64]

@@ -170,7 +170,7 @@ class SolveReport:
 # --------------------------------------------------------------------------- helpers
 
 def _require_square(a: np.ndarray, name: str = "A") -> np.ndarray:
-    """core.py:33-45 (shape part; symmetry/finiteness are checked on the device)."""
+    """core.py:33-45 (shape part; symmetry / finiteness: rcp_factor_host / the device)."""
     a = np.asarray(a, dtype=np.float64)
     if a.ndim != 2 or a.shape[0] != a.shape[1]:
         raise ValueError(f"{name} must be square, got shape {a.shape}")
@@ -434,7 +434,12 @@ def factor_device(a: torch.Tensor, cfg: FactorConfig | None = None, *, omega: to
             ctypes.byref(st), int(world), 1 if emulate else 0, _ptr(wws), 0 if wws is None else wws.numel(),
             _stream())
         _raise_status(status, st)
-    out.stats = {
+    out.stats = _stats_dict(st)
+    return out
+
+
+def _stats_dict(st) -> dict:
+    return {
         "rho_cheap": float(st.rho_cheap), "max_multiplier": float(st.max_multiplier),
         "amax": float(st.amax), "dmax": float(st.dmax), "recompute_count": int(st.recompute_count),
         "n_panels": int(st.n_panels), "n_steps": int(st.n_steps), "n_2x2": int(st.n_2x2),
@@ -447,7 +452,6 @@ def factor_device(a: torch.Tensor, cfg: FactorConfig | None = None, *, omega: to
                                    "qrcp_local_argmax", "qrcp_householder"),
                                   [round(float(x), 3) for x in st.panel_prof_ms])),
     }
-    return out
 
 
 def solve_device(f: DeviceFactorization, b: torch.Tensor, x: torch.Tensor | None = None,
@@ -502,18 +506,41 @@ def factor(a: np.ndarray, cfg: FactorConfig | None = None, **overrides) -> Facto
     a = _require_square(a)
     _check_supported(cfg)
     _native.load()
-    dev = _device()
-    at = torch.from_numpy(np.ascontiguousarray(a))
-    # the H2D copy of A (asynchronous from pinned memory) overlaps the host draw of Omega
-    ad = at.to(dev, non_blocking=at.is_pinned())
-    omega = None
-    if cfg.strategy is Strategy.RCP:
-        omega = torch.from_numpy(np.random.Generator(np.random.Philox(cfg.seed)).standard_normal((cfg.p, a.shape[0])))
-        omega = omega.to(dev)
-    n = a.shape[0]
-    # L streams into pinned host memory while the factorization runs (rcp_factor_host_l)
+    return _factor_host(np.ascontiguousarray(a), cfg, _device()).to_host()
+
+
+def _factor_host(a: np.ndarray, cfg: FactorConfig, dev: torch.device) -> DeviceFactorization:
+    """factor() on a C-contiguous float64 host array through ``rcp_factor_host``: the lower
+    trapezoid goes to the device, exact symmetry is checked on host threads meanwhile, Omega is
+    the first draw of the stream (drawn during the copies) and, for n >= 2048, L streams back into
+    pinned memory while later panels run."""
+    lib = _native.load()
+    n = int(a.shape[0])
+    if n == 0:
+        raise ValueError("A must have at least one row")
+    c = _native_config(cfg)
+    workspace = torch.empty(int(lib.rcp_workspace_bytes(n, ctypes.byref(c))), dtype=torch.uint8, device=dev)
+    out = DeviceFactorization(
+        perm=torch.empty(n, dtype=torch.int64, device=dev),
+        L=torch.empty((n, n), dtype=torch.float64, device=dev),
+        d_diag=torch.empty(n, dtype=torch.float64, device=dev),
+        d_off=torch.empty(n, dtype=torch.float64, device=dev),
+        pattern=torch.empty(n, dtype=torch.int8, device=dev),
+        stats={},
+    )
     lh = torch.empty((n, n), dtype=torch.float64, pin_memory=True) if n >= 2048 else None
-    return factor_device(ad, cfg, omega=omega, l_host=lh).to_host()
+    normals = _NormalStream(cfg.seed)
+    st = _native.RcpStats()
+    with torch.cuda.device(dev):
+        status = lib.rcp_factor_host(
+            ctypes.byref(c), n, a.ctypes.data, n, None, normals.cfunc, None,
+            workspace.data_ptr(), workspace.numel(), out.perm.data_ptr(), out.L.data_ptr(),
+            out.d_diag.data_ptr(), out.d_off.data_ptr(), out.pattern.data_ptr(), None, None,
+            ctypes.byref(st), _ptr(lh), _stream())
+    _raise_status(status, st)
+    out.host_L = lh
+    out.stats = _stats_dict(st)
+    return out
 
 
 def factor_robust(a: np.ndarray, cfg: FactorConfig | None = None, **overrides) -> Factorization:

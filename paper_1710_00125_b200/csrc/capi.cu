@@ -13,6 +13,7 @@
 #include <cstdio>
 #include <cstring>
 #include <cstdlib>
+#include <atomic>
 #include <thread>
 #include <vector>
 
@@ -227,7 +228,7 @@ static int factor_core(const rcp_config* cfg, int64_t n, const double* a, int64_
                        rcp_draw_fn draw, void* draw_ctx, void* workspace, size_t workspace_bytes, int64_t* perm,
                        double* Lout, double* d_diag, double* d_off, int8_t* pattern, int8_t* trace_kind,
                        int32_t* trace_r, rcp_stats* stats, int world, int emulate, void* worker_ws,
-                       size_t worker_ws_bytes, void* cuda_stream, double* L_host);
+                       size_t worker_ws_bytes, void* cuda_stream, double* L_host, const double* a_host);
 
 int rcp_factor_dist(const rcp_config* cfg, int64_t n, const double* a, int64_t lda, const double* omega_dev,
                     rcp_draw_fn draw, void* draw_ctx, void* workspace, size_t workspace_bytes, int64_t* perm,
@@ -236,7 +237,7 @@ int rcp_factor_dist(const rcp_config* cfg, int64_t n, const double* a, int64_t l
                     size_t worker_ws_bytes, void* cuda_stream) {
   return factor_core(cfg, n, a, lda, omega_dev, draw, draw_ctx, workspace, workspace_bytes, perm, Lout, d_diag, d_off,
                      pattern, trace_kind, trace_r, stats, world, emulate, worker_ws, worker_ws_bytes, cuda_stream,
-                     nullptr);
+                     nullptr, nullptr);
 }
 
 int rcp_factor_host_l(const rcp_config* cfg, int64_t n, const double* a, int64_t lda, const double* omega_dev,
@@ -245,14 +246,69 @@ int rcp_factor_host_l(const rcp_config* cfg, int64_t n, const double* a, int64_t
                       int32_t* trace_r, rcp_stats* stats, double* L_host, void* cuda_stream) {
   if (!L_host) return RCP_ERR_INVALID_ARG;
   return factor_core(cfg, n, a, lda, omega_dev, draw, draw_ctx, workspace, workspace_bytes, perm, Lout, d_diag, d_off,
-                     pattern, trace_kind, trace_r, stats, 1, 0, nullptr, 0, cuda_stream, L_host);
+                     pattern, trace_kind, trace_r, stats, 1, 0, nullptr, 0, cuda_stream, L_host, nullptr);
+}
+
+// Exact symmetry of a row-major host matrix (core.py:48-53: A == A.T elementwise, so a NaN
+// anywhere fails), checked on host threads while the device works; 64 x 64 tile pairs.
+struct HostSymCheck {
+  std::vector<std::thread> th;
+  std::atomic<int> asym{0};
+  void start(const double* a, int64_t n, int64_t lda) {
+    const int64_t T = 64, nti = (n + T - 1) / T;
+    unsigned hw = std::thread::hardware_concurrency();
+    const int nt = (int)std::max<int64_t>(1, std::min<int64_t>({(int64_t)(hw ? hw : 1) / 2, 8, nti}));
+    for (int tt = 0; tt < nt; ++tt)
+      th.emplace_back([this, a, n, lda, nti, nt, tt]() {
+        for (int64_t I = tt; I < nti; I += nt) {  // tile row I: pairs (I, J <= I)
+          if (asym.load(std::memory_order_relaxed)) return;
+          const int64_t i0 = I * T, i1 = std::min(n, i0 + T);
+          int bad = 0;
+          for (int64_t J = 0; J <= I; ++J) {
+            const int64_t j0 = J * T, j1 = std::min(n, j0 + T);
+            for (int64_t i = i0; i < i1; ++i) {
+              const double* ri = a + i * lda;
+              const int64_t je = (I == J) ? i + 1 : j1;
+              for (int64_t j = j0; j < je; ++j) bad |= !(ri[j] == a[j * lda + i]);
+            }
+          }
+          if (bad) {
+            asym.store(1);
+            return;
+          }
+        }
+      });
+  }
+  bool join() {
+    for (auto& x : th) x.join();
+    th.clear();
+    return asym.load() != 0;
+  }
+  ~HostSymCheck() { join(); }
+};
+
+int rcp_factor_host(const rcp_config* cfg, int64_t n, const double* a_host, int64_t lda, const double* omega_dev,
+                    rcp_draw_fn draw, void* draw_ctx, void* workspace, size_t workspace_bytes, int64_t* perm,
+                    double* Lout, double* d_diag, double* d_off, int8_t* pattern, int8_t* trace_kind,
+                    int32_t* trace_r, rcp_stats* stats, double* L_host, void* cuda_stream) {
+  if (!a_host || n < 1 || lda < n) return RCP_ERR_INVALID_ARG;
+  HostSymCheck chk;
+  chk.start(a_host, n, lda);
+  const int rc = factor_core(cfg, n, nullptr, lda, omega_dev, draw, draw_ctx, workspace, workspace_bytes, perm, Lout,
+                             d_diag, d_off, pattern, trace_kind, trace_r, stats, 1, 0, nullptr, 0, cuda_stream,
+                             L_host, a_host);
+  if (rc != RCP_ERR_INVALID_ARG && rc != RCP_ERR_WORKSPACE && chk.join()) {
+    if (stats) snprintf(stats->message, sizeof(stats->message), "A must be symmetric");
+    return RCP_ERR_NOT_SYMMETRIC;  // the reference checks symmetry first (core.py:48-53)
+  }
+  return rc;
 }
 
 static int factor_core(const rcp_config* cfg, int64_t n, const double* a, int64_t lda, const double* omega_dev,
                        rcp_draw_fn draw, void* draw_ctx, void* workspace, size_t workspace_bytes, int64_t* perm,
                        double* Lout, double* d_diag, double* d_off, int8_t* pattern, int8_t* trace_kind,
                        int32_t* trace_r, rcp_stats* stats, int world, int emulate, void* worker_ws,
-                       size_t worker_ws_bytes, void* cuda_stream, double* L_host) {
+                       size_t worker_ws_bytes, void* cuda_stream, double* L_host, const double* a_host) {
   if (stats) {
     memset(stats, 0, sizeof(*stats));
     stats->deficient_from = -1;
@@ -260,7 +316,8 @@ static int factor_core(const rcp_config* cfg, int64_t n, const double* a, int64_
   int vc = validate_cfg(cfg, n);
   if (vc != RCP_OK) return vc;
   const bool rcp_strat = cfg->strategy == RCP_STRATEGY_RCP;  // bkpp / bbk: no sketch (factor.py:306)
-  if (lda < n || !a || (rcp_strat && !omega_dev) || !perm || !Lout || !d_diag || !d_off || !pattern)
+  if (lda < n || (!a && !a_host) || (rcp_strat && !omega_dev && !(a_host && draw)) || !perm || !Lout || !d_diag ||
+      !d_off || !pattern)
     return RCP_ERR_INVALID_ARG;
   const rcp_config c = *cfg;
   const Layout Lay = make_layout(n, c);
@@ -364,7 +421,27 @@ static int factor_core(const rcp_config* cfg, int64_t n, const double* a, int64_
   if (trace_r) RCP_CHECK(cudaMemsetAsync(trace_r, 0xff, sizeof(int32_t) * n, st));
 
   // ---- input validation + copy (factor.py:277-286)
-  RCP_LAUNCH(launch_validate_copy(a, lda, n, A[0], dscal->vflags, &dscal->amax, st));
+  const double* a_in = a;
+  int64_t lda_in = lda;
+  std::vector<double> omega_buf;
+  if (a_host) {  // host input: only its lower trapezoid crosses PCIe (256-row block rows), staged
+    double* stage = A[1];  // in A1 (free until the first trailing update), mirrored by the kernel
+    for (int64_t i0 = 0; i0 < n; i0 += 256) {
+      const int64_t i1 = std::min<int64_t>(n, i0 + 256);
+      RCP_CHECK(cudaMemcpy2DAsync(stage + i0 * n, (size_t)n * sizeof(double), a_host + i0 * lda,
+                                  (size_t)lda * sizeof(double), (size_t)i1 * sizeof(double), (size_t)(i1 - i0),
+                                  cudaMemcpyHostToDevice, st));
+    }
+    a_in = stage;
+    lda_in = n;
+  }
+  RCP_LAUNCH(launch_validate_copy(a_in, lda_in, n, A[0], dscal->vflags, &dscal->amax, st, a_host ? 1 : 0));
+  if (a_host && rcp_strat && !omega_dev) {  // Omega = the stream's first draw, drawn while the copies run
+    omega_buf.resize((size_t)P * n);
+    if (draw(draw_ctx, P, n, omega_buf.data()) != 0) return RCP_ERR_NEED_NORMALS;
+    RCP_CHECK(cudaMemcpyAsync(omg, omega_buf.data(), sizeof(double) * (size_t)P * n, cudaMemcpyHostToDevice, st));
+    omega_dev = omg;
+  }
   RCP_CHECK(cudaMemcpyAsync(hscal, dscal, sizeof(Scal), cudaMemcpyDeviceToHost, st));
   RCP_CHECK(cudaStreamSynchronize(st));
   if (hscal->vflags[0]) return RCP_ERR_NOT_SYMMETRIC;

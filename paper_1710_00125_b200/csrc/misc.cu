@@ -33,8 +33,11 @@ __device__ double block_max(double v) {
 // One 32x32 tile pair per block: tile (I, J) with I >= J and its mirror (J, I), each read once
 // from the input and written once to the workspace; the exact-symmetry check compares the two in
 // shared memory (core.py:48-53), finiteness and max|A| on the way (factor.py:280-286).
+// half != 0: only the upper triangle of a (column-major view: a(r, c) for r <= c, i.e. the
+// lower triangle of a row-major host matrix) was transferred and its exact symmetry is
+// checked on the host (rcp_factor_host); the kernel mirrors it and checks finiteness / max|A|.
 __global__ void validate_copy_kernel(const double* __restrict__ a, int64_t lda, int64_t n,
-                                     double* __restrict__ out, int* flags, double* amax) {
+                                     double* __restrict__ out, int* flags, double* amax, int half) {
   __shared__ double tl[32][33];  // tile (I, J): tl[x][y] = a(bi + y, bj + x)  (x = column offset)
   __shared__ double tu[32][33];  // tile (J, I): tu[x][y] = a(bj + y, bi + x)
   const long long pid = blockIdx.x;
@@ -49,7 +52,7 @@ __global__ void validate_copy_kernel(const double* __restrict__ a, int64_t lda, 
   for (int r = ty; r < 32; r += 8) {  // coalesced along rows (tx) of column bj + r / bi + r
     const int64_t il = bi + tx, jl = bj + r;
     double v = 0.0;
-    if (il < n && jl < n) {
+    if (il < n && jl < n && !(half && I != J)) {
       v = a[il + jl * lda];
       out[il + jl * n] = v;
       nonfin |= !isfinite(v);
@@ -69,6 +72,13 @@ __global__ void validate_copy_kernel(const double* __restrict__ a, int64_t lda, 
     }
   }
   __syncthreads();
+  if (half) {  // tile (I, J) = transpose of the transferred tile (J, I)
+    if (I != J)
+      for (int r = ty; r < 32; r += 8) {
+        const int64_t il = bi + tx, jl = bj + r;
+        if (il < n && jl < n) out[il + jl * n] = tu[tx][r];
+      }
+  } else
   for (int r = ty; r < 32; r += 8) {  // a(bi + tx, bj + r) vs a(bj + r, bi + tx)
     const int64_t il = bi + tx, jl = bj + r;
     if (il < n && jl < n) {
@@ -343,10 +353,10 @@ __global__ void iota_kernel(int64_t n, int* p) {
 
 // ------------------------------------------------------------------ launchers
 cudaError_t launch_validate_copy(const double* a, int64_t lda, int64_t n, double* out, int* flags, double* amax,
-                                 cudaStream_t st) {
+                                 cudaStream_t st, int half) {
   const long long nb = (n + 31) / 32;
   dim3 block(32, 8);
-  validate_copy_kernel<<<(unsigned)(nb * (nb + 1) / 2), block, 0, st>>>(a, lda, n, out, flags, amax);
+  validate_copy_kernel<<<(unsigned)(nb * (nb + 1) / 2), block, 0, st>>>(a, lda, n, out, flags, amax, half);
   return cudaGetLastError();
 }
 

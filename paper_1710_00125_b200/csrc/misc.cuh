@@ -9,7 +9,7 @@ struct PanelDesc;
 struct SchurDyn;
 
 cudaError_t launch_validate_copy(const double* a, int64_t lda, int64_t n, double* out, int* flags, double* amax,
-                                 cudaStream_t st);
+                                 cudaStream_t st, int half = 0);
 cudaError_t launch_tstamp_init(unsigned long long* ts, int64_t count, cudaStream_t st);
 cudaError_t launch_sketch_norm_max(const double* B, int P, int64_t ncols, double* out, cudaStream_t st);
 cudaError_t launch_gather(int64_t n, int k0, int k_end, int t, int tpad, int64_t rows_pad, const int* phys_of_log,

@@ -283,6 +283,28 @@ def test_streamed_host_l_matches_device(cuda_ok, n, rank, robust, kw):
     assert float(np.abs(rec - a[np.ix_(f.perm, f.perm)]).max()) / float(np.abs(a).max()) <= 1e-11
 
 
+def test_host_input_symmetry_and_finiteness_large(cuda_ok):
+    """factor(numpy) at n >= 2048: only the lower triangle goes to the device, so exact symmetry
+    is checked on the host (core.py:48-53) and reported before anything else; NaN anywhere
+    (also on the diagonal) fails it, Inf in a symmetric matrix is "NaN or Inf"."""
+    from paper_1710_00125_b200 import api, gallery
+    n = 2100
+    a = gallery.type6(n, 11)
+    for (i, j) in [(5, 2000), (2099, 0), (1000, 1001)]:  # one upper entry off by one ulp
+        b = a.copy()
+        b[min(i, j), max(i, j)] = np.nextafter(b[min(i, j), max(i, j)], np.inf)
+        with pytest.raises(ValueError, match="symmetric"):
+            api.factor(b, strategy="rcp", b=64, q=64, p=80)
+    b = a.copy()
+    b[17, 17] = np.nan
+    with pytest.raises(ValueError, match="symmetric"):
+        api.factor(b, strategy="rcp", b=64, q=64, p=80)
+    b = a.copy()
+    b[3, 1500] = b[1500, 3] = np.inf
+    with pytest.raises(ValueError, match="NaN or Inf"):
+        api.factor(b, strategy="rcp", b=64, q=64, p=80)
+
+
 def test_supplied_omega_with_guard_recompute(cuda_ok):
     """Omega passed in (its draw is skipped lazily): a guard recompute must still continue the
     same normal stream (g_c5_scaled recomputes once)."""
