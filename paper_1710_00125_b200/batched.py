@@ -30,7 +30,7 @@ from .api import (BlockDiag, DeviceFactorization, Factorization, FactorConfig, G
                   OpCounters, _blocks_from_arrays, _check_supported, _config, _device, _raise_status, _stream,
                   factor_device)
 
-__all__ = ["BatchedDeviceFactorization", "factor_batched_device", "factor_batched", "solve_batched_device",
+__all__ = ["BatchedDeviceFactorization", "factor_batched_device", "factor_batched_host", "factor_batched", "solve_batched_device",
            "solve_batched", "batched_workspace_bytes", "normal_stream"]
 
 MAX_N = 256
@@ -191,15 +191,110 @@ def _copy_single(out: BatchedDeviceFactorization, i: int, f: DeviceFactorization
     rec["mults"], rec["adds"], rec["divs"], rec["comps"] = s["counters"]
 
 
+def factor_batched_host(a: torch.Tensor, cfg: FactorConfig | None = None, *, chunk: int = 296,
+                        normals: torch.Tensor | None = None, extra_draws: int = 4,
+                        workspace: torch.Tensor | None = None, out: BatchedDeviceFactorization | None = None,
+                        check: bool = True, **overrides) -> BatchedDeviceFactorization:
+    """Factor a host-resident stack ``a`` (CPU float64 ``[count, n, n]``, ideally pinned) into host memory.
+
+    Same results as :func:`factor_batched_device` on ``a.cuda()``, with the PCIe traffic hidden
+    behind the kernel: the batch runs in chunks of ``chunk`` matrices over two device slots, the
+    upload of chunk i+1 (copy stream), the factorization of chunk i (compute stream) and the
+    download of chunk i-1's perm/L/D/pattern (second copy stream) overlap.  The returned
+    :class:`BatchedDeviceFactorization` holds pinned host tensors (``to_host`` works on it).
+    """
+    cfg = _config(cfg, overrides)
+    _check_supported(cfg, batched=True)
+    if a.dim() != 3 or a.shape[1] != a.shape[2]:
+        raise ValueError(f"expected a [count, n, n] stack, got shape {tuple(a.shape)}")
+    if a.dtype != torch.float64 or a.is_cuda:
+        raise ValueError("factor_batched_host expects a host (CPU) float64 tensor")
+    count, n = int(a.shape[0]), int(a.shape[1])
+    if n == 0:
+        raise ValueError("A must have at least one row")
+    a = a.contiguous()
+    dev = _device()
+    if not _supported(cfg, n):
+        return factor_batched_device(a.to(dev), cfg, check=check)
+    lib = _native.load()
+    pin = torch.cuda.is_available()
+    if out is None:
+        out = BatchedDeviceFactorization(
+            perm=torch.empty(count, n, dtype=torch.int64, pin_memory=pin),
+            L=torch.empty(count, n, n, dtype=torch.float64, pin_memory=pin),
+            d_diag=torch.empty(count, n, dtype=torch.float64, pin_memory=pin),
+            d_off=torch.empty(count, n, dtype=torch.float64, pin_memory=pin),
+            pattern=torch.empty(count, n, dtype=torch.int8, pin_memory=pin),
+            stats=np.zeros(count, dtype=_native.BATCH_STATS_DTYPE))
+    if normals is None:
+        normals = torch.from_numpy(normal_stream(cfg, n, extra_draws)).to(dev)
+    if workspace is None:
+        workspace = torch.empty(batched_workspace_bytes(n, cfg), dtype=torch.uint8, device=dev)
+    chunk = max(1, min(chunk, count))
+    ssz = ctypes.sizeof(_native.RcpBatchStats)
+    mstats = torch.empty(count * ssz, dtype=torch.uint8, device=dev)
+    slots = [dict(a=torch.empty(chunk, n, n, dtype=torch.float64, device=dev),
+                  L=torch.empty(chunk, n, n, dtype=torch.float64, device=dev),
+                  perm=torch.empty(chunk, n, dtype=torch.int64, device=dev),
+                  dd=torch.empty(chunk, n, dtype=torch.float64, device=dev),
+                  doff=torch.empty(chunk, n, dtype=torch.float64, device=dev),
+                  pat=torch.empty(chunk, n, dtype=torch.int8, device=dev)) for _ in range(2)]
+    main = torch.cuda.current_stream(dev)
+    up, comp, down = torch.cuda.Stream(dev), torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    for s in (up, comp, down):
+        s.wait_stream(main)  # normals / workspace / slots were made on the caller's stream
+    ev_up = [torch.cuda.Event() for _ in range(2)]
+    ev_comp = [torch.cuda.Event() for _ in range(2)]
+    ev_down = [torch.cuda.Event() for _ in range(2)]
+    c = _cfg_struct(cfg)
+    for i, c0 in enumerate(range(0, count, chunk)):
+        c1 = min(count, c0 + chunk)
+        m, k, sl = c1 - c0, i % 2, slots[i % 2]
+        if i >= 2:
+            up.wait_event(ev_comp[k])     # slot k's A was consumed by chunk i-2
+        with torch.cuda.stream(up):
+            sl["a"][:m].copy_(a[c0:c1], non_blocking=True)
+        ev_up[k].record(up)
+        comp.wait_event(ev_up[k])
+        if i >= 2:
+            comp.wait_event(ev_down[k])   # slot k's outputs were downloaded
+        status = lib.rcp_factor_batched(ctypes.byref(c), m, n, sl["a"].data_ptr(), n, n * n, normals.data_ptr(),
+                                        normals.numel(), workspace.data_ptr(), workspace.numel(),
+                                        sl["perm"].data_ptr(), sl["L"].data_ptr(), sl["dd"].data_ptr(),
+                                        sl["doff"].data_ptr(), sl["pat"].data_ptr(),
+                                        mstats.data_ptr() + c0 * ssz, comp.cuda_stream)
+        _raise_status(status, None)
+        ev_comp[k].record(comp)
+        down.wait_event(ev_comp[k])
+        with torch.cuda.stream(down):
+            out.L[c0:c1].copy_(sl["L"][:m], non_blocking=True)
+            out.perm[c0:c1].copy_(sl["perm"][:m], non_blocking=True)
+            out.d_diag[c0:c1].copy_(sl["dd"][:m], non_blocking=True)
+            out.d_off[c0:c1].copy_(sl["doff"][:m], non_blocking=True)
+            out.pattern[c0:c1].copy_(sl["pat"][:m], non_blocking=True)
+        ev_down[k].record(down)
+    down.synchronize()
+    comp.synchronize()
+    out.stats = mstats.cpu().numpy().view(_native.BATCH_STATS_DTYPE).copy()
+    redo = np.nonzero(out.stats["status"] == _native.RCP_ERR_NEED_NORMALS)[0]
+    for i in redo:
+        f = factor_device(a[int(i)].to(dev), cfg)
+        _copy_single(out, int(i), f)
+    if check:
+        bad = np.nonzero(out.stats["status"] != _native.RCP_OK)[0]
+        if bad.size:
+            i = int(bad[0])
+            _raise_matrix(i, out.stats[i])
+    return out
+
+
 def factor_batched(a: np.ndarray, cfg: FactorConfig | None = None, **overrides) -> list:
     """``[randldl.factor(a[i], cfg) for i in range(len(a))]`` in one device call."""
     cfg = _config(cfg, overrides)
     a = np.asarray(a, dtype=np.float64)
     if a.ndim != 3 or a.shape[1] != a.shape[2]:
         raise ValueError(f"expected a [count, n, n] stack, got shape {a.shape}")
-    dev = _device()
-    ad = torch.from_numpy(np.ascontiguousarray(a)).to(dev)
-    return factor_batched_device(ad, cfg).to_host()
+    return factor_batched_host(torch.from_numpy(np.ascontiguousarray(a)), cfg).to_host()
 
 
 def solve_batched_device(f: BatchedDeviceFactorization, b: torch.Tensor,

@@ -114,3 +114,31 @@ def test_batched_host_api_roundtrip(cuda_ok):
     x = solve_batched(fs, rhs)
     for i, a in enumerate(mats):
         assert np.abs(a @ x[i] - rhs[i]).max() <= 1e-10 * np.abs(rhs[i]).max() * np.abs(a).max() * 128
+
+
+def test_batched_host_pipeline_equals_device(cuda_ok):
+    """factor_batched_host (chunked upload / factor / download on three streams) returns the same
+    bits as factor_batched_device on the resident stack: ragged last chunk, both slots reused,
+    scaled members (guard recompute) and a failing matrix keep their per-matrix status."""
+    import torch
+    from paper_1710_00125_b200 import FactorConfig, _native, batched, gallery
+    cfg = FactorConfig(**C5)
+    a = gallery.c5_batch_device(301, 256, seed=7)
+    a[150, 3, 5] += 1.0  # asymmetric member
+    dev = batched.factor_batched_device(a, cfg, check=False)
+    host = batched.factor_batched_host(a.cpu().pin_memory(), cfg, chunk=64, check=False)
+    assert not host.L.is_cuda and host.L.is_pinned()
+    assert np.array_equal(host.stats["status"], dev.stats["status"])
+    ok = dev.stats["status"] == _native.RCP_OK
+    assert ok.sum() == 300  # outputs of the failed member are unspecified
+    okt = torch.from_numpy(ok)
+    for name in ("perm", "L", "d_diag", "d_off", "pattern"):
+        h, d = getattr(host, name)[okt], getattr(dev, name).cpu()[okt]
+        bad = (h != d).reshape(len(h), -1).any(dim=1).nonzero().flatten().tolist()
+        assert not bad, f"{name} differs in {len(bad)} matrices, first {bad[:5]}"
+    for name in ("recompute_count", "n_2x2", "n_steps", "rho_cheap", "max_multiplier", "mults", "comps"):
+        assert np.array_equal(host.stats[name][ok], dev.stats[name][ok]), name
+    assert host.stats["status"][150] == _native.RCP_ERR_NOT_SYMMETRIC
+    assert (host.stats["recompute_count"] > 0).sum() >= 25
+    with pytest.raises(ValueError, match="matrix 150"):
+        batched.factor_batched_host(a.cpu(), cfg, chunk=100)
