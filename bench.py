@@ -83,6 +83,15 @@ def ncu_traffic(kernel: str, detail: bool = False):
         "dram_bytes": total, "source": "profiles/r01_ncu_traffic.json (ncu --set full, one launch)"}
 
 
+def c5_traffic(count: int):
+    """DRAM bytes of one batched_factor_kernel launch over `count` matrices: the committed ncu
+    capture (16384 matrices, one launch) scaled per matrix (the kernel does the same work per matrix)."""
+    rec = ncu_traffic("batched_factor_kernel", detail=True)
+    if rec is None:
+        return None
+    return rec["dram_bytes"] * count / rec["matrices"]
+
+
 def cfg_dict(a, world: int = 1):
     return {"workload": workload_name(a), "n": a.n, "b": a.b, "q": a.b, "p_sketch": a.p,
             "oversampling": a.p - a.b,
@@ -540,7 +549,9 @@ def run_b200_c5(args, rank: int, world: int, local_rank: int):
         "pct_fp64_peak": 100.0 * value / (world * FP64_PEAK_GFLOPS),
         "roofline": {"bound": "tensor", "kernel": "batched_factor_kernel (whole factorization, one CTA per matrix)",
                      "achieved": value / 1e3, "peak": FP64_PEAK_GFLOPS / 1e3, "unit": "TFLOP/s",
-                     "frac": value / (world * FP64_PEAK_GFLOPS), "traffic": None,
+                     "frac": value / (world * FP64_PEAK_GFLOPS),
+                     "traffic": c5_traffic(args.count // world),
+                     "traffic_launch": ncu_traffic("batched_factor_kernel", detail=True),
                      "hbm_achieved_gbs": hbm_bytes / (ms_max / 1e3) / 1e9 / world,
                      "hbm_peak_gbs": 6546.6,
                      "algorithmic": "n^3/3 flop and 2 n^2 * 8 B (A in, L out) per matrix"},
