@@ -725,7 +725,7 @@ __global__ void __launch_bounds__(BT, MINB) batched_factor_kernel(BatchParams p)
       if (act0) {
         double* dst = Lst + (size_t)S.permv[i] * n + k0;
         for (int s = 0; s < t; ++s)
-          if (i > k0 + s) dst[s] = S.Lp[(size_t)s * BT + i];
+          if (i > k0 + s) __stcs(dst + s, S.Lp[(size_t)s * BT + i]);  // read once at the end: evict-first
       }
 
       if (mp > 0 && t > 0) {
@@ -857,12 +857,12 @@ __global__ void __launch_bounds__(BT, MINB) batched_factor_kernel(BatchParams p)
       for (int c = lane; c < n; c += 32) {
         double v;
         if (c < row) {
-          v = c < kdone ? src[c] : 0.0;
+          v = c < kdone ? __ldcs(src + c) : 0.0;
           mm = fmax(mm, fabs(v));
         } else {
           v = c == row ? 1.0 : 0.0;
         }
-        dst[c] = v;
+        __stcs(dst + c, v);  // output: streaming store, keeps the other CTAs' trailing blocks in L2
       }
     }
     mm = bmax(mm, S, par);
