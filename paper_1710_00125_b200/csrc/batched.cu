@@ -11,7 +11,8 @@
 //   * the trailing matrix lives in per-CTA global scratch (L2-resident) in the panel's
 //     start order; inside a panel symmetric swaps (factor.py:333-348) are bookkeeping
 //     (pol[]), and the trailing update (factor.py:369-379) gathers through it while
-//     writing the next panel's compact trailing block (lower computed, mirrored);
+//     writing the next panel's compact trailing block (lower triangle only; reads of the
+//     upper part go through the transposed index);
 //   * L columns are stored keyed by the ORIGINAL row index, so later row swaps never move
 //     them; the final L (final pivot order) is one coalesced row gather.
 // The decision logic (first-index argmax, thresholds, alpha, defer rule, 2x2 formulas with
@@ -343,7 +344,8 @@ __global__ void __launch_bounds__(BT, MINB) batched_factor_kernel(BatchParams p)
             for (int r = 0; r < PM; ++r) y[r] = 0.0;
             const int ci = i - k0;
             for (int j = 0; j < m; ++j) {
-              const double a = Acur[(size_t)j * ldA + ci];  // T(ci, j) = T(j, ci)
+              // T(ci, j) = T(j, ci); trailing blocks hold only their lower triangle
+              const double a = ci >= j ? Acur[(size_t)j * ldA + ci] : Acur[(size_t)ci * ldA + j];
               const double* zz = p.z + zoff + j;
 #pragma unroll
               for (int r = 0; r < PM; ++r)
@@ -489,7 +491,11 @@ __global__ void __launch_bounds__(BT, MINB) batched_factor_kernel(BatchParams p)
       }
       PF(0);
       // ---- SBKP steps (factor.py:602-634)
-      auto T = [&](int a, int c) -> double { return Acur[(size_t)c * ldA + a]; };
+      // element (a, c) of the symmetric active block, read from its lower triangle (the only part
+      // the trailing update stores; the input A is full, so the same rule holds for panel 0)
+      auto T = [&](int a, int c) -> double {
+        return a >= c ? Acur[(size_t)c * ldA + a] : Acur[(size_t)a * ldA + c];
+      };
       double tk = act0 ? T(S.pol[i], S.pol[k0]) : 0.0;
       int t = 0;
       bool deferred = false;
@@ -729,11 +735,12 @@ __global__ void __launch_bounds__(BT, MINB) batched_factor_kernel(BatchParams p)
       }
 
       if (mp > 0 && t > 0) {
-        // ---- trailing update A22 -= L21 W21^T, lower computed + mirrored (factor.py:369-379)
+        // ---- trailing update A22 -= L21 W21^T (factor.py:369-379). The reference mirrors the
+        // lower result into the upper part (mirror_lower); here only the lower triangle is
+        // stored and every reader takes (a, c) with a < c from (c, a) -- the same values.
         // Warp work unit: a 32-row strip I x an 8-column group g of the lower triangle; lane =
-        // row.  Lower stores are coalesced across lanes, the mirror is 64 contiguous bytes
-        // per lane; the C-in gather (through pol) of the next unit is issued before this
-        // unit's FMAs.
+        // row.  Stores are coalesced across lanes; the C-in gather (through pol) of the next
+        // unit is issued before this unit's FMAs.
         double* An = Abuf[nb];
         const int ng = (mp + 7) >> 3;
         int uI = 0, ug = warp;
@@ -748,7 +755,8 @@ __global__ void __launch_bounds__(BT, MINB) batched_factor_kernel(BatchParams p)
     const int pi_ = ii_ < n ? S.pol[ii_] : 0;                                        \
     _Pragma("unroll") for (int c2 = 0; c2 < 8; ++c2) {                               \
       const int j_ = j0_ + c2;                                                       \
-      cin_[c2] = (ii_ < n && j_ < n && ii_ >= j_) ? Acur[(size_t)S.pol[j_] * ldA + pi_] : 0.0; \
+      const int pj_ = (ii_ < n && j_ < n && ii_ >= j_) ? S.pol[j_] : -1;                      \
+      cin_[c2] = pj_ < 0 ? 0.0 : (pi_ >= pj_ ? Acur[(size_t)pj_ * ldA + pi_] : Acur[(size_t)pi_ * ldA + pj_]); \
     }                                                                                \
   }
         double cin[8];
@@ -775,14 +783,12 @@ __global__ void __launch_bounds__(BT, MINB) batched_factor_kernel(BatchParams p)
             for (int c2 = 0; c2 < 8; ++c2) acc[c2] = __fma_rn(lv, Wc[j0 + c2], acc[c2]);  // j0 + c2 <= n + 7 stays inside smem
           }
           if (ii < n) {
-            double* mir = An + (size_t)(ii - k_end) * mp + (j0 - k_end);
 #pragma unroll
             for (int c2 = 0; c2 < 8; ++c2) {
               const int j = j0 + c2;
               if (j < n && ii >= j) {
                 const double v = __dsub_rn(cin[c2], acc[c2]);
-                An[(size_t)(j - k_end) * mp + (ii - k_end)] = v;
-                mir[c2] = v;
+                An[(size_t)(j - k_end) * mp + (ii - k_end)] = v;  // lower triangle only
               }
             }
           }
