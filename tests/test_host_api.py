@@ -86,3 +86,16 @@ def test_type6_chunked_equals_one_shot():
 def test_scaled_member_is_exactly_symmetric():
     a = gallery.scaled_member(64, 10, True)
     assert np.array_equal(a, a.T)
+
+
+def test_batched_host_validates_before_device():
+    """factor_batched_host rejects bad stacks with the reference's ValueError before any device work."""
+    import torch
+    from paper_1710_00125_b200 import batched
+    cfg = api.FactorConfig(strategy="rcp", b=16, q=16, p=24, seed=0)
+    with pytest.raises(ValueError, match="stack"):
+        batched.factor_batched_host(torch.zeros(4, 8, 9, dtype=torch.float64), cfg)
+    with pytest.raises(ValueError, match="float64"):
+        batched.factor_batched_host(torch.zeros(4, 8, 8, dtype=torch.float32), cfg)
+    with pytest.raises(ValueError, match="at least one row"):
+        batched.factor_batched_host(torch.zeros(4, 0, 0, dtype=torch.float64), cfg)

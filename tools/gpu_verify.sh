@@ -7,3 +7,5 @@ timeout 900 python bench.py > gpurun_out/${tag}_bench_c3.json 2> gpurun_out/${ta
 cut -c1-400 gpurun_out/${tag}_bench_c3.json
 timeout 600 python bench.py --workload c5 > gpurun_out/${tag}_bench_c5.json 2> gpurun_out/${tag}_bench_c5.err; echo "bench c5 exit $?"
 cut -c1-300 gpurun_out/${tag}_bench_c5.json
+timeout 900 python bench.py --impl reference --steps 2 --warmup 3 > gpurun_out/${tag}_bench_ref.json 2> gpurun_out/${tag}_bench_ref.err; echo "bench ref exit $?"
+cut -c1-300 gpurun_out/${tag}_bench_ref.json
