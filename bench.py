@@ -14,10 +14,15 @@ Multi-GPU (torchrun, one process per GPU): one factorization per step whose trai
 updates are shared by all N GPUs over NVLink peer memory (paper_1710_00125_b200.dist; rank 0
 runs the panels); "scaling": "strong", value = n^3/3 / max-over-ranks step time.
 
-``--impl reference`` times the reference algorithm's CPU implementation (the
-oracle port in oracle/rcp_oracle.py — the reference is pure Python and cannot be
-shipped to the GPU box) on the host cores, on the same workload, one panel per
-step (a bounded sample), rank 0 only.
+``--impl reference`` times the reference's own CPU implementation on the host cores: the
+unmodified ``randldl`` package (pure Python + NumPy/OpenBLAS), shipped to the GPU box as
+``oracle/_ref/randldl`` by ``oracle/Makefile`` (copied from /root/reference in the build
+container), stepped one panel per step through its own engine (``_Engine._run_panel``,
+factor.py:540-568) on the same workload -- a bounded sample, rank 0 only.  Without
+``oracle/_ref`` the oracle port (oracle/rcp_oracle.py) stands in and the line says so.
+
+``python bench.py --gpus N`` without a torchrun environment re-launches itself under
+``torch.distributed.run`` with N processes (one per GPU).
 """
 
 from __future__ import annotations
@@ -43,6 +48,37 @@ FP64_PEAK_GFLOPS = 37170.0   # measured DMMA peak, profiles/r01_fp64_peaks.txt (
 FP64_PEAK_SRC = "measured DMMA m8n8k4 microbenchmark on this pool's B200 (profiles/r01_fp64_peaks.txt)"
 
 
+def hbm_peak_gbs():
+    """Measured HBM copy bandwidth from the driver-written MEASURED_PEAKS.json (fallback: the
+    profiling guide's B200 figure)."""
+    try:
+        v = float(json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["hbm_gbs"])
+        return v, "MEASURED_PEAKS.json hbm_gbs"
+    except (OSError, KeyError, ValueError):
+        return 6546.6, "fallback (B200_PROFILING.md)"
+
+
+def cpu_model() -> str:
+    try:
+        for ln in Path("/proc/cpuinfo").read_text().splitlines():
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def load_reference():
+    """The unmodified reference package from oracle/_ref (None when it was not shipped)."""
+    ref = ROOT / "oracle" / "_ref"
+    if not (ref / "randldl" / "factor.py").exists():
+        return None
+    if str(ref) not in sys.path:
+        sys.path.insert(0, str(ref))
+    import randldl
+    return randldl
+
+
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -60,6 +96,7 @@ def parse():
                     help="c3: n=32768 single matrix (headline); c5: 65536 x n=256 batched (b=16, p=8)")
     ap.add_argument("--count", type=int, default=65536, help="c5: matrices in the whole job")
     ap.add_argument("--e2e-chunk", type=int, default=296, help="c5: matrices per pipelined e2e chunk")
+    ap.add_argument("--solve-reps", type=int, default=10, help="c3: timed device solves")
     return ap.parse_args()
 
 
@@ -200,24 +237,55 @@ def cores_used() -> int:
 
 
 # ----------------------------------------------------------------------------- reference arm
+def ref_sample(a_host, args, max_panels: int, skip_panels: int):
+    """Time the REFERENCE itself (oracle/_ref/randldl) panel by panel through its own engine:
+    _Engine(a, cfg) (validation, copy, Omega, B = Omega A: setup, untimed), then _run_panel()
+    exactly as _Engine.run() loops (factor.py:508-513)."""
+    randldl = load_reference()
+    fmod = sys.modules["randldl.factor"]
+    cfg = randldl.FactorConfig(strategy="rcp", b=args.b, q=args.b, p=args.p, seed=args.seed)
+    t0 = time.perf_counter()
+    eng = fmod._Engine(a_host, cfg)
+    t_setup = time.perf_counter() - t0
+    times, works = [], []
+    npan = 0
+    while eng.k < eng.n and not eng.terminated and npan < max_panels + skip_panels:
+        k0 = eng.k
+        t1 = time.perf_counter()
+        eng._run_panel()
+        dt = time.perf_counter() - t1
+        npan += 1
+        if npan > skip_panels:
+            times.append(dt)
+            works.append(work_flops(eng.n, k0, eng.k))
+    return {"t_setup": t_setup, "times": times, "works": works, "k_done": eng.k, "panels": npan}
+
+
 def run_reference(args, rank: int):
     if rank != 0:
         return
     from paper_1710_00125_b200 import gallery
     a_host = gallery.type6(args.n, args.seed)
-    res = cpu_sample(a_host, args, budget_s=1e9, max_panels=args.steps, skip_panels=args.warmup)
+    if load_reference() is not None:
+        res = ref_sample(a_host, args, max_panels=args.steps, skip_panels=args.warmup)
+        kind = "reference"
+        what = f"the unmodified reference randldl (oracle/_ref, numpy {np.__version__} + OpenBLAS), _Engine._run_panel"
+    else:
+        res = cpu_sample(a_host, args, budget_s=1e9, max_panels=args.steps, skip_panels=args.warmup)
+        kind = "port"
+        what = f"oracle port (numpy {np.__version__} + OpenBLAS; oracle/_ref absent)"
     tsum = sum(res["times"])
     value = sum(res["works"]) / tsum / 1e9
-    sample = (f"oracle port (numpy {np.__version__} + OpenBLAS) factor() on the config-3 matrix: panels "
-              f"{args.warmup + 1}..{args.warmup + args.steps} timed one per step (panels 1..{args.warmup} warm-up), "
-              f"columns 0..{res['k_done']} eliminated; value = sum (n-j)^2 over the timed panels' columns / time; "
-              f"setup (validation, copy, Omega*A) {res['t_setup']:.1f} s excluded")
+    sample = (f"{what} on the config-3 matrix: panels {args.warmup + 1}..{args.warmup + args.steps} timed one per "
+              f"step (panels 1..{args.warmup} warm-up), columns 0..{res['k_done']} eliminated; value = sum (n-j)^2 "
+              f"over the timed panels' columns / time; setup (validation, copy, Omega*A) {res['t_setup']:.1f} s "
+              f"excluded; CPU {cpu_model()}")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tsum / max(1, len(res["times"])),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded numpy Philox type6)", "config": cfg_dict(args, args.gpus),
-        "cpu_baseline": {"value": value, "unit": "GFLOP/s", "cores": cores_used(), "kind": "port",
+        "cpu_baseline": {"value": value, "unit": "GFLOP/s", "cores": cores_used(), "kind": kind,
                          "sample": sample},
         "e2e": {"value": value, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -287,12 +355,27 @@ def run_b200(args, rank: int, world: int, local_rank: int):
     value = flops / (ms_max / 1e3) / 1e9  # one factorization per step on all N GPUs together
     stats = dict(out.stats) if out is not None else {}
 
-    bwd = None
-    if rank == 0:  # quick accuracy check of the last factorization on the device (solve + residual)
+    bwd = solve = None
+    if rank == 0:  # device solve of the last factorization: timed, and its backward error
         rhs = torch.from_numpy(gallery.rhs(n, 1)).to(dev)
-        x, _ = api.solve_device(out, rhs)
+        sws = torch.empty(int(api._native.load().rcp_solve_workspace_bytes(n, 1)), dtype=torch.uint8, device=dev)
+        x, _ = api.solve_device(out, rhs, workspace=sws)
+        torch.cuda.synchronize()
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s0.record(stream)
+        for _ in range(args.solve_reps):
+            x, _ = api.solve_device(out, rhs, workspace=sws)
+        s1.record(stream)
+        torch.cuda.synchronize()
+        solve_ms = s0.elapsed_time(s1) / args.solve_reps
         resid = float((a_dev @ x - rhs).abs().max())
         bwd = resid / (float(a_dev.abs().sum(dim=1).max()) * float(x.abs().max()))
+        hbm, hbm_src = hbm_peak_gbs()
+        sbytes = n * (n - 1) * 8  # L's strict lower triangle, read by both sweeps
+        solve = {"ms": solve_ms, "nrhs": 1, "algorithmic_bytes": sbytes,
+                 "hbm_achieved_gbs": sbytes / (solve_ms / 1e3) / 1e9, "hbm_peak_gbs": hbm, "peak_source": hbm_src,
+                 "hbm_frac": sbytes / (solve_ms / 1e3) / 1e9 / hbm, "backward_error": bwd,
+                 "kernels": "diag_inverse_kernel + fwd_sweep_kernel + block_diag_kernel + bwd_sweep_kernel"}
 
     # end to end through the public API: numpy in (pinned) -> Factorization out
     # A (single GPU: the 256-row block rows of its lower trapezoid, rcp_factor_host) + Omega;
@@ -327,13 +410,18 @@ def run_b200(args, rank: int, world: int, local_rank: int):
         try:
             del out, ws
             torch.cuda.empty_cache()
-            res = cpu_sample(a_host, args, budget_s=args.cpu_seconds)
+            if load_reference() is not None:
+                res = ref_sample(a_host, args, max_panels=1, skip_panels=0)
+                kind, what = "reference", "the unmodified reference randldl (oracle/_ref)"
+            else:
+                res = cpu_sample(a_host, args, budget_s=args.cpu_seconds)
+                kind, what = "port", "oracle port of the reference algorithm"
             cv = sum(res["works"]) / sum(res["times"]) / 1e9
-            cpu = {"value": cv, "unit": "GFLOP/s", "cores": cores_used(), "kind": "port",
-                   "sample": (f"oracle port of the reference algorithm (numpy {np.__version__}/OpenBLAS), first "
+            cpu = {"value": cv, "unit": "GFLOP/s", "cores": cores_used(), "kind": kind,
+                   "sample": (f"{what} (numpy {np.__version__}/OpenBLAS), first "
                               f"{res['panels']} panel(s) of the same n={n} matrix (columns 0..{res['k_done']}), "
                               f"{sum(res['times']):.1f} s; value = sum (n-j)^2 over eliminated columns / panel time; "
-                              f"setup {res['t_setup']:.1f} s excluded")}
+                              f"setup {res['t_setup']:.1f} s excluded; CPU {cpu_model()}")}
         except MemoryError:
             cpu = {"value": None, "unit": "GFLOP/s", "cores": cores_used(), "kind": "port",
                    "sample": "host out of memory for the n=32768 oracle sample"}
@@ -366,6 +454,7 @@ def run_b200(args, rank: int, world: int, local_rank: int):
         "factor_stats": {k: stats.get(k) for k in ("n_panels", "n_steps", "n_2x2", "recompute_count", "rho_cheap",
                                                    "max_multiplier", "t_panel_ms", "t_schur_ms")},
         "solve_backward_error": bwd,
+        "solve": solve,
     }
     print(json.dumps(line), flush=True)
 
@@ -553,7 +642,7 @@ def run_b200_c5(args, rank: int, world: int, local_rank: int):
                      "traffic": c5_traffic(args.count // world),
                      "traffic_launch": ncu_traffic("batched_factor_kernel", detail=True),
                      "hbm_achieved_gbs": hbm_bytes / (ms_max / 1e3) / 1e9 / world,
-                     "hbm_peak_gbs": 6546.6,
+                     "hbm_peak_gbs": hbm_peak_gbs()[0],
                      "algorithmic": "n^3/3 flop and 2 n^2 * 8 B (A in, L out) per matrix"},
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_val, "unit": "GFLOP/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
@@ -568,8 +657,20 @@ def run_b200_c5(args, rank: int, world: int, local_rank: int):
     print(json.dumps(line), flush=True)
 
 
+def relaunch_under_torchrun(n: int) -> int:
+    """`bench.py --gpus N` outside torchrun: run this script under torch.distributed.run with N
+    processes on this node (rendezvous on 127.0.0.1) and return its exit code."""
+    import random
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(random.randint(20000, 40000)),
+           str(Path(__file__).resolve()), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch_under_torchrun(args.gpus))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))

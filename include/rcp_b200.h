@@ -160,6 +160,29 @@ int rcp_factor_host(const rcp_config* cfg, int64_t n, const double* a_host, int6
                     int8_t* trace_kind, int32_t* trace_r,
                     rcp_stats* stats, double* L_host, void* cuda_stream);
 
+/* Experiment diagnostics of the reference engine (FactorConfig.track_growth="full" and
+ * audit_sketch, factor.py:294-296, 493-504, 566-567, 605-606).  The reference forces width-1
+ * panels for them; pass cfg->b = cfg->q = 1.  All buffers are device memory. */
+typedef struct rcp_diag {
+  int32_t track_full;     /* 1: one snapshot per step: (max|S|, largest column norm of S) of the
+                             active Schur complement S = A[k:, k:] at the step start            */
+  int32_t audit;          /* 1: sketch drift ||B[:, k:] - Omega[:, k:] S||_{1,2} after each panel
+                             with k < n (unnormalised; the caller divides by ||A||_{1,2})       */
+  double* snapshots;      /* [cap][2], zeroed by the call                                       */
+  double* drift;          /* [cap], zeroed by the call                                          */
+  double* omega_orig;     /* audit scratch, p x n                                               */
+  int64_t cap;            /* >= n + 1                                                            */
+  int64_t n_snapshots;    /* out */
+  int64_t n_drift;        /* out */
+} rcp_diag;
+/* rcp_factor plus the diagnostics above (replaces randldl.factor with track_growth="full" or
+ * audit_sketch=True, factor.py:637-647). */
+int rcp_factor_diag(const rcp_config* cfg, int64_t n, const double* a, int64_t lda,
+                    const double* omega, rcp_draw_fn draw, void* draw_ctx,
+                    void* workspace, size_t workspace_bytes,
+                    int64_t* perm, double* L, double* d_diag, double* d_off, int8_t* pattern,
+                    int8_t* trace_kind, int32_t* trace_r, rcp_stats* stats, rcp_diag* diag,
+                    void* cuda_stream);
 /* x = P^T L^-T D^-1 L^-1 P b for nrhs right-hand sides (solve.py:69-92).
  * b and x are device, column-major n x nrhs (ld = n); may alias.  *singular is
  * set to 1 if an exact-zero block was met (solve.py:47-58). */

@@ -37,6 +37,7 @@ EXPORTED_SYMBOLS = (
     "rcp_factor",
     "rcp_factor_host_l",
     "rcp_factor_host",
+    "rcp_factor_diag",
     "rcp_solve",
     "rcp_solve_workspace_bytes",
     "rcp_reconstruct",
@@ -90,6 +91,19 @@ class RcpStats(ctypes.Structure):
         ("comps", ctypes.c_int64),
         ("panel_prof_ms", ctypes.c_double * 16),
         ("message", ctypes.c_char * 160),
+    ]
+
+
+class RcpDiag(ctypes.Structure):
+    _fields_ = [
+        ("track_full", ctypes.c_int32),
+        ("audit", ctypes.c_int32),
+        ("snapshots", ctypes.c_void_p),
+        ("drift", ctypes.c_void_p),
+        ("omega_orig", ctypes.c_void_p),
+        ("cap", ctypes.c_int64),
+        ("n_snapshots", ctypes.c_int64),
+        ("n_drift", ctypes.c_int64),
     ]
 
 
@@ -157,6 +171,9 @@ def load(path: str | os.PathLike | None = None):
     lib.rcp_factor_host.argtypes = [ctypes.POINTER(RcpConfig), i64, vp, i64, vp, DRAW_FN, vp, vp, sz,
                                     vp, vp, vp, vp, vp, vp, vp, ctypes.POINTER(RcpStats), vp, vp]
     lib.rcp_factor_host.restype = ctypes.c_int
+    lib.rcp_factor_diag.argtypes = [ctypes.POINTER(RcpConfig), i64, vp, i64, vp, DRAW_FN, vp, vp, sz,
+                                    vp, vp, vp, vp, vp, vp, vp, ctypes.POINTER(RcpStats), ctypes.POINTER(RcpDiag), vp]
+    lib.rcp_factor_diag.restype = ctypes.c_int
     lib.rcp_solve.argtypes = [i64, vp, vp, vp, vp, vp, i64, vp, vp, vp, sz, ctypes.POINTER(ctypes.c_int32), vp]
     lib.rcp_solve.restype = ctypes.c_int
     lib.rcp_solve_workspace_bytes.argtypes = [i64, i64]

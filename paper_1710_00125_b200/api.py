@@ -149,6 +149,11 @@ class Factorization:
     D: BlockDiag
     pattern: np.ndarray
     stats: GrowthStats
+    # The device-resident factorization this result was copied from (factor() keeps it, so
+    # solve() / solve_many() do not re-upload the dense L).  Its host arrays are made
+    # read-only; solve() uses the device copy only while perm / L / D / pattern are still
+    # the very objects factor() returned.
+    _device: object = field(default=None, repr=False, compare=False)
 
     @property
     def n(self) -> int:
@@ -182,15 +187,21 @@ def _require_square(a: np.ndarray, name: str = "A") -> np.ndarray:
 _STRATEGY_CODE = {Strategy.RCP: 0, Strategy.BKPP: 1, Strategy.BBK: 2}  # rcp_b200.h RCP_STRATEGY_*
 
 
+def _eager(cfg: FactorConfig) -> bool:
+    """track_growth="full" and audit_sketch force width-1 panels (factor.py:294-296)."""
+    return cfg.track_growth is GrowthTracking.FULL or cfg.audit_sketch
+
+
 def _native_config(cfg: FactorConfig) -> _native.RcpConfig:
-    return _native.RcpConfig(cfg.p, cfg.b, cfg.q, cfg.robust_r, _STRATEGY_CODE[cfg.strategy])
+    b, q = (1, 1) if _eager(cfg) else (cfg.b, cfg.q)
+    return _native.RcpConfig(cfg.p, b, q, cfg.robust_r, _STRATEGY_CODE[cfg.strategy])
 
 
 def _check_supported(cfg: FactorConfig, batched: bool = False) -> None:
     if batched and cfg.strategy is not Strategy.RCP:
         raise ValueError(f"the batched kernel runs strategy 'rcp' only, got {cfg.strategy.value!r}")
-    if cfg.track_growth is GrowthTracking.FULL or cfg.audit_sketch:
-        raise ValueError("track_growth='full' / audit_sketch diagnostics are not part of the B200 build")
+    if batched and _eager(cfg):
+        raise ValueError("track_growth='full' / audit_sketch run through factor(), not the batched kernel")
 
 
 def _raise_status(status: int, st: _native.RcpStats | None) -> None:
@@ -263,7 +274,10 @@ class DeviceFactorization:
         blocks = _blocks_from_arrays(self.d_diag.cpu().numpy(), self.d_off.cpu().numpy(), pattern)
         s = self.stats
         stats = GrowthStats(rho_cheap=s["rho_cheap"], max_multiplier=s["max_multiplier"],
-                            counters=OpCounters(*s["counters"]), recompute_count=s["recompute_count"])
+                            counters=OpCounters(*s["counters"]), recompute_count=s["recompute_count"],
+                            rho_elem=s.get("rho_elem"), rho_col=s.get("rho_col"), L_norm1=s.get("L_norm1"),
+                            Linv_norm1=s.get("Linv_norm1"), snapshots=s.get("snapshots"),
+                            sketch_drift=s.get("sketch_drift"))
         perm = self.perm.cpu().numpy().astype(np.int64)
         if lh is not None:
             L = lh.numpy()
@@ -383,8 +397,10 @@ def factor_device(a: torch.Tensor, cfg: FactorConfig | None = None, *, omega: to
     elif omega is None:
         omega = torch.from_numpy(normals.first(cfg.p, n)).to(dev)
     else:
+        if tuple(omega.shape) != (cfg.p, n):
+            raise ValueError(f"omega must have shape ({cfg.p}, {n}), got {tuple(omega.shape)}")
         normals.skip_first(cfg.p, n)  # advance past the supplied first draw when needed
-        omega = omega.contiguous()
+        omega = omega.to(device=dev, dtype=torch.float64).contiguous()
     c = _native_config(cfg)
     need = int(lib.rcp_workspace_bytes(n, ctypes.byref(c)))
     if isinstance(workspace, tuple):
@@ -412,30 +428,88 @@ def factor_device(a: torch.Tensor, cfg: FactorConfig | None = None, *, omega: to
         out.trace_kind = torch.empty(n, dtype=torch.int8, device=dev)
         out.trace_r = torch.empty(n, dtype=torch.int32, device=dev)
     st = _native.RcpStats()
-    if l_host is not None:
-        if world != 1 or l_host.dtype != torch.float64 or tuple(l_host.shape) != (n, n) \
-                or not l_host.is_pinned() or not l_host.is_contiguous():
-            raise ValueError("l_host must be a contiguous pinned float64 (n, n) tensor (single GPU)")
-        status = lib.rcp_factor_host_l(
-            ctypes.byref(c), n, a.data_ptr(), lda, 0 if omega is None else omega.data_ptr(), normals.cfunc, None,
-            ws_ptr, ws_bytes, out.perm.data_ptr(), out.L.data_ptr(),
-            out.d_diag.data_ptr(), out.d_off.data_ptr(), out.pattern.data_ptr(),
-            _ptr(out.trace_kind if trace else None), _ptr(out.trace_r if trace else None),
-            ctypes.byref(st), l_host.data_ptr(), _stream())
-        _raise_status(status, st)
-        out.host_L = l_host
-    else:
-        out.host_L = None
-        status = lib.rcp_factor_dist(
-            ctypes.byref(c), n, a.data_ptr(), lda, 0 if omega is None else omega.data_ptr(), normals.cfunc, None,
-            ws_ptr, ws_bytes, out.perm.data_ptr(), out.L.data_ptr(),
-            out.d_diag.data_ptr(), out.d_off.data_ptr(), out.pattern.data_ptr(),
-            _ptr(out.trace_kind if trace else None), _ptr(out.trace_r if trace else None),
-            ctypes.byref(st), int(world), 1 if emulate else 0, _ptr(wws), 0 if wws is None else wws.numel(),
-            _stream())
-        _raise_status(status, st)
+    diag = None
+    if _eager(cfg):
+        if world != 1 or l_host is not None:
+            raise ValueError("track_growth='full' / audit_sketch run on a single GPU without l_host")
+        cap = n + 1
+        snaps = torch.zeros(cap, 2, dtype=torch.float64, device=dev)
+        drift = torch.zeros(cap, dtype=torch.float64, device=dev)
+        omega_orig = (torch.empty(cfg.p, n, dtype=torch.float64, device=dev)
+                      if cfg.audit_sketch and cfg.strategy is Strategy.RCP else None)
+        diag = _native.RcpDiag(int(cfg.track_growth is GrowthTracking.FULL), int(cfg.audit_sketch),
+                               snaps.data_ptr(), drift.data_ptr(), _ptr(omega_orig), cap, 0, 0)
+    with torch.cuda.device(dev):
+        if diag is not None:
+            out.host_L = None
+            status = lib.rcp_factor_diag(
+                ctypes.byref(c), n, a.data_ptr(), lda, 0 if omega is None else omega.data_ptr(), normals.cfunc, None,
+                ws_ptr, ws_bytes, out.perm.data_ptr(), out.L.data_ptr(),
+                out.d_diag.data_ptr(), out.d_off.data_ptr(), out.pattern.data_ptr(),
+                _ptr(out.trace_kind if trace else None), _ptr(out.trace_r if trace else None),
+                ctypes.byref(st), ctypes.byref(diag), _stream())
+            _raise_status(status, st)
+        elif l_host is not None:
+            if world != 1 or l_host.dtype != torch.float64 or tuple(l_host.shape) != (n, n) \
+                    or not l_host.is_pinned() or not l_host.is_contiguous():
+                raise ValueError("l_host must be a contiguous pinned float64 (n, n) tensor (single GPU)")
+            status = lib.rcp_factor_host_l(
+                ctypes.byref(c), n, a.data_ptr(), lda, 0 if omega is None else omega.data_ptr(), normals.cfunc, None,
+                ws_ptr, ws_bytes, out.perm.data_ptr(), out.L.data_ptr(),
+                out.d_diag.data_ptr(), out.d_off.data_ptr(), out.pattern.data_ptr(),
+                _ptr(out.trace_kind if trace else None), _ptr(out.trace_r if trace else None),
+                ctypes.byref(st), l_host.data_ptr(), _stream())
+            _raise_status(status, st)
+            out.host_L = l_host
+        else:
+            out.host_L = None
+            status = lib.rcp_factor_dist(
+                ctypes.byref(c), n, a.data_ptr(), lda, 0 if omega is None else omega.data_ptr(), normals.cfunc, None,
+                ws_ptr, ws_bytes, out.perm.data_ptr(), out.L.data_ptr(),
+                out.d_diag.data_ptr(), out.d_off.data_ptr(), out.pattern.data_ptr(),
+                _ptr(out.trace_kind if trace else None), _ptr(out.trace_r if trace else None),
+                ctypes.byref(st), int(world), 1 if emulate else 0, _ptr(wws), 0 if wws is None else wws.numel(),
+                _stream())
+            _raise_status(status, st)
     out.stats = _stats_dict(st)
+    if diag is not None:
+        out.stats.update(_diag_stats(cfg, a, out, diag, snaps, drift))
     return out
+
+
+def _max_col_norm(m: torch.Tensor) -> float:
+    """norm_1_2 (metrics.py:83-90): the largest scaled Euclidean column norm (core.py:122-142)."""
+    if m.numel() == 0:
+        return 0.0
+    scale = m.abs().amax(dim=0)
+    safe = torch.where(scale > 0, scale, torch.ones_like(scale))
+    return float((scale * torch.sqrt(((m / safe) ** 2).sum(dim=0))).max())
+
+
+def _diag_stats(cfg, a, out, diag, snaps, drift) -> dict:
+    """GrowthStats' diagnostic fields (factor.py:514-531; metrics.py:93-127) from the device
+    snapshots / drift; rho_elem / rho_col, ||L||_1 and ||L^-1||_1 only with snapshots."""
+    res = {"snapshots": None, "sketch_drift": None}
+    if cfg.track_growth is GrowthTracking.FULL:
+        k = int(diag.n_snapshots)
+        res["snapshots"] = [tuple(map(float, r)) for r in snaps[:k].cpu().numpy()]
+    if cfg.audit_sketch:
+        k = int(diag.n_drift)
+        norm12 = _max_col_norm(a) if cfg.strategy is Strategy.RCP else 0.0
+        vals = drift[:k].cpu().numpy() if cfg.strategy is Strategy.RCP else np.zeros(0)
+        res["sketch_drift"] = [float(v / norm12) if norm12 else float(v) for v in vals]
+    if res["snapshots"]:
+        sn = np.array(res["snapshots"])
+        if sn[0, 0] == 0.0 or sn[0, 1] == 0.0:
+            raise ValueError("snapshot of the input matrix is zero; growth undefined")
+        res["rho_elem"] = float(sn[:, 0].max() / sn[0, 0])
+        res["rho_col"] = float(sn[:, 1].max() / sn[0, 1])
+        L = out.L
+        res["L_norm1"] = float(L.abs().sum(dim=0).max())
+        eye = torch.eye(L.shape[0], dtype=L.dtype, device=L.device)
+        linv = torch.linalg.solve_triangular(L, eye, upper=False, unitriangular=True)
+        res["Linv_norm1"] = float(linv.abs().sum(dim=0).max())
+    return res
 
 
 def _stats_dict(st) -> dict:
@@ -459,20 +533,25 @@ def solve_device(f: DeviceFactorization, b: torch.Tensor, x: torch.Tensor | None
     """x = A^-1 b on the device; b is (n,) or (n, k) CUDA float64."""
     lib = _native.load()
     n = f.n
-    vec = b.dim() == 1
-    if b.shape[0] != n or b.dim() not in (1, 2):
+    if b.dim() not in (1, 2) or b.shape[0] != n:
         raise ValueError(f"right-hand side shape {tuple(b.shape)} does not match n={n}")
+    vec = b.dim() == 1
+    dev = f.L.device
+    b = b.to(device=dev, dtype=torch.float64)  # the kernels read float64 on the factor's device
     nrhs = 1 if vec else int(b.shape[1])
+    if nrhs == 0:
+        return (torch.empty_like(b) if x is None else x), False
     bc = b.reshape(n, 1) if vec else b
     bcol = bc.t().contiguous()  # (k, n): column-major n x k
     xcol = torch.empty_like(bcol)
     need = int(lib.rcp_solve_workspace_bytes(n, nrhs))
-    if workspace is None or workspace.numel() < need:
-        workspace = torch.empty(need, dtype=torch.uint8, device=b.device)
+    if workspace is None or workspace.numel() < need or workspace.device != dev:
+        workspace = torch.empty(need, dtype=torch.uint8, device=dev)
     sing = ctypes.c_int32(0)
-    status = lib.rcp_solve(n, f.perm.data_ptr(), f.L.data_ptr(), f.d_diag.data_ptr(), f.d_off.data_ptr(),
-                           f.pattern.data_ptr(), nrhs, bcol.data_ptr(), xcol.data_ptr(), workspace.data_ptr(),
-                           workspace.numel(), ctypes.byref(sing), _stream())
+    with torch.cuda.device(dev):
+        status = lib.rcp_solve(n, f.perm.data_ptr(), f.L.data_ptr(), f.d_diag.data_ptr(), f.d_off.data_ptr(),
+                               f.pattern.data_ptr(), nrhs, bcol.data_ptr(), xcol.data_ptr(), workspace.data_ptr(),
+                               workspace.numel(), ctypes.byref(sing), _stream())
     _raise_status(status, None)
     res = xcol.t()
     res = res.reshape(n) if vec else res.contiguous()
@@ -486,8 +565,9 @@ def reconstruct_device(f: DeviceFactorization) -> torch.Tensor:
     lib = _native.load()
     n = f.n
     out = torch.empty((n, n), dtype=torch.float64, device=f.L.device)
-    status = lib.rcp_reconstruct(n, f.L.data_ptr(), f.d_diag.data_ptr(), f.d_off.data_ptr(),
-                                 f.pattern.data_ptr(), out.data_ptr(), _stream())
+    with torch.cuda.device(f.L.device):
+        status = lib.rcp_reconstruct(n, f.L.data_ptr(), f.d_diag.data_ptr(), f.d_off.data_ptr(),
+                                     f.pattern.data_ptr(), out.data_ptr(), _stream())
     _raise_status(status, None)
     return out
 
@@ -506,7 +586,29 @@ def factor(a: np.ndarray, cfg: FactorConfig | None = None, **overrides) -> Facto
     a = _require_square(a)
     _check_supported(cfg)
     _native.load()
-    return _factor_host(np.ascontiguousarray(a), cfg, _device()).to_host()
+    if _eager(cfg):  # diagnostics: exact symmetry / finiteness are checked on the device
+        dev = _device()
+        df = factor_device(torch.from_numpy(np.ascontiguousarray(a)).to(dev), cfg)
+    else:
+        df = _factor_host(np.ascontiguousarray(a), cfg, _device())
+    return _attach(df.to_host(), df)
+
+
+def _attach(f: Factorization, df: DeviceFactorization) -> Factorization:
+    for arr in (f.perm, f.L, f.pattern):
+        arr.flags.writeable = False
+    f._device = (df, f.perm, f.L, f.D, f.pattern)
+    return f
+
+
+def _attached(f: Factorization) -> DeviceFactorization | None:
+    ref = getattr(f, "_device", None)
+    if ref is None:
+        return None
+    df, perm, L, D, pattern = ref
+    if f.perm is perm and f.L is L and f.D is D and f.pattern is pattern:
+        return df
+    return None
 
 
 def _factor_host(a: np.ndarray, cfg: FactorConfig, dev: torch.device) -> DeviceFactorization:
@@ -594,7 +696,7 @@ def solve(f: Factorization, b: np.ndarray, a: np.ndarray | None = None) -> Solve
     b = np.asarray(b, dtype=np.float64)
     if b.shape != (f.n,):
         raise ValueError(f"right-hand side shape {b.shape} does not match n={f.n}")
-    df = _device_from_host(f)
+    df = _attached(f) or _device_from_host(f)
     xd, sing = solve_device(df, torch.from_numpy(b).to(df.L.device))
     x = xd.cpu().numpy()
     err = _backward_error(np.asarray(a, dtype=np.float64), x, b) if a is not None else None
@@ -606,6 +708,6 @@ def solve_many(f: Factorization, b_rhs: np.ndarray) -> np.ndarray:
     b_rhs = np.asarray(b_rhs, dtype=np.float64)
     if b_rhs.ndim != 2 or b_rhs.shape[0] != f.n:
         raise ValueError(f"right-hand sides must be ({f.n}, k), got {b_rhs.shape}")
-    df = _device_from_host(f)
+    df = _attached(f) or _device_from_host(f)
     xd, _ = solve_device(df, torch.from_numpy(b_rhs).to(df.L.device))
     return xd.cpu().numpy()

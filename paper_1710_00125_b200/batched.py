@@ -129,7 +129,7 @@ def factor_batched_device(a: torch.Tensor, cfg: FactorConfig | None = None, *, n
     count, n = int(a.shape[0]), int(a.shape[1])
     if n == 0:
         raise ValueError("A must have at least one row")
-    if a.stride(2) != 1 or a.stride(1) != n:
+    if not a.is_contiguous():  # the kernel reads matrix i at a + i * n * n
         a = a.contiguous()
     dev = a.device
     if out is None:
@@ -214,10 +214,22 @@ def factor_batched_host(a: torch.Tensor, cfg: FactorConfig | None = None, *, chu
         raise ValueError("A must have at least one row")
     a = a.contiguous()
     dev = _device()
-    if not _supported(cfg, n):
-        return factor_batched_device(a.to(dev), cfg, check=check)
-    lib = _native.load()
     pin = torch.cuda.is_available()
+    if not _supported(cfg, n):  # single-matrix GPU path per matrix, results copied into `out`
+        res = factor_batched_device(a.to(dev), cfg, check=check)
+        if out is None:
+            out = BatchedDeviceFactorization(
+                perm=torch.empty(count, n, dtype=torch.int64, pin_memory=pin),
+                L=torch.empty(count, n, n, dtype=torch.float64, pin_memory=pin),
+                d_diag=torch.empty(count, n, dtype=torch.float64, pin_memory=pin),
+                d_off=torch.empty(count, n, dtype=torch.float64, pin_memory=pin),
+                pattern=torch.empty(count, n, dtype=torch.int8, pin_memory=pin),
+                stats=np.zeros(count, dtype=_native.BATCH_STATS_DTYPE))
+        for name in ("perm", "L", "d_diag", "d_off", "pattern"):
+            getattr(out, name).copy_(getattr(res, name))
+        out.stats = res.stats
+        return out
+    lib = _native.load()
     if out is None:
         out = BatchedDeviceFactorization(
             perm=torch.empty(count, n, dtype=torch.int64, pin_memory=pin),

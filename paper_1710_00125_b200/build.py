@@ -43,12 +43,29 @@ def needs_build() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False) -> Path:
+    """Compile each .cu to an object in parallel (nvcc per file), then link the shared library."""
     if not force and not needs_build():
         return OUT
+    from concurrent.futures import ThreadPoolExecutor
     extra = ["-DRCP_PANEL_PROF=1"] if os.environ.get("RCP_PANEL_PROF") == "1" else []
     if os.environ.get("RCP_BATCH_PROF") == "1":
         extra.append("-DRCP_BATCH_PROF=1")
-    cmd = [_nvcc(), *NVCC_FLAGS, *extra, "-o", str(OUT) + ".tmp", *map(str, sources())]
+    objdir = ROOT / "build" / "obj"
+    objdir.mkdir(parents=True, exist_ok=True)
+    compile_flags = [f for f in NVCC_FLAGS if f != "-shared"]
+    nvcc = _nvcc()
+
+    def one(src: Path) -> Path:
+        obj = objdir / (src.stem + ".o")
+        cmd = [nvcc, *compile_flags, *extra, "-c", str(src), "-o", str(obj)]
+        if verbose:
+            print(" ".join(cmd), flush=True)
+        subprocess.run(cmd, check=True, cwd=str(ROOT))
+        return obj
+
+    with ThreadPoolExecutor(max_workers=max(1, min(len(sources()), os.cpu_count() or 1))) as ex:
+        objs = list(ex.map(one, sources()))
+    cmd = [nvcc, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", str(OUT) + ".tmp", *map(str, objs)]
     if verbose:
         print(" ".join(cmd), flush=True)
     subprocess.run(cmd, check=True, cwd=str(ROOT))

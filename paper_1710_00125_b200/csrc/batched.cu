@@ -1093,8 +1093,14 @@ int rcp_factor_batched(const rcp_config* cfg, int64_t count, int64_t n, const do
   prm.q = cfg->q;
   prm.armed = cfg->robust_r >= 1;
   prm.alpha = std::sqrt(2.0) / 2.0;
-  for (int j = 0; j < kMaxThr; ++j)
-    prm.thr[j] = prm.armed ? std::pow(DBL_EPSILON, (double)(j + 1) / cfg->robust_r) : 0.0;
+  {  // thresholds exactly as the reference accumulates them: delta = 1/r, then delta += 1/r per
+     // recompute, threshold = eps**delta (factor.py:316, 400-401)
+    double delta = prm.armed ? 1.0 / cfg->robust_r : 0.0;
+    for (int j = 0; j < kMaxThr; ++j) {
+      prm.thr[j] = prm.armed ? std::pow(DBL_EPSILON, delta) : 0.0;
+      if (prm.armed) delta += 1.0 / cfg->robust_r;
+    }
+  }
   prm.A = a;
   prm.lda = lda;
   prm.a_stride = a_stride;

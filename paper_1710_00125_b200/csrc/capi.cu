@@ -228,7 +228,8 @@ static int factor_core(const rcp_config* cfg, int64_t n, const double* a, int64_
                        rcp_draw_fn draw, void* draw_ctx, void* workspace, size_t workspace_bytes, int64_t* perm,
                        double* Lout, double* d_diag, double* d_off, int8_t* pattern, int8_t* trace_kind,
                        int32_t* trace_r, rcp_stats* stats, int world, int emulate, void* worker_ws,
-                       size_t worker_ws_bytes, void* cuda_stream, double* L_host, const double* a_host);
+                       size_t worker_ws_bytes, void* cuda_stream, double* L_host, const double* a_host,
+                       rcp_diag* diag = nullptr);
 
 int rcp_factor_dist(const rcp_config* cfg, int64_t n, const double* a, int64_t lda, const double* omega_dev,
                     rcp_draw_fn draw, void* draw_ctx, void* workspace, size_t workspace_bytes, int64_t* perm,
@@ -247,6 +248,17 @@ int rcp_factor_host_l(const rcp_config* cfg, int64_t n, const double* a, int64_t
   if (!L_host) return RCP_ERR_INVALID_ARG;
   return factor_core(cfg, n, a, lda, omega_dev, draw, draw_ctx, workspace, workspace_bytes, perm, Lout, d_diag, d_off,
                      pattern, trace_kind, trace_r, stats, 1, 0, nullptr, 0, cuda_stream, L_host, nullptr);
+}
+
+int rcp_factor_diag(const rcp_config* cfg, int64_t n, const double* a, int64_t lda, const double* omega_dev,
+                    rcp_draw_fn draw, void* draw_ctx, void* workspace, size_t workspace_bytes, int64_t* perm,
+                    double* Lout, double* d_diag, double* d_off, int8_t* pattern, int8_t* trace_kind,
+                    int32_t* trace_r, rcp_stats* stats, rcp_diag* diag, void* cuda_stream) {
+  if (!diag || diag->cap < n + 1 || (diag->track_full && !diag->snapshots) ||
+      (diag->audit && (!diag->drift || !diag->omega_orig)))
+    return RCP_ERR_INVALID_ARG;
+  return factor_core(cfg, n, a, lda, omega_dev, draw, draw_ctx, workspace, workspace_bytes, perm, Lout, d_diag, d_off,
+                     pattern, trace_kind, trace_r, stats, 1, 0, nullptr, 0, cuda_stream, nullptr, nullptr, diag);
 }
 
 // Exact symmetry of a row-major host matrix (core.py:48-53: A == A.T elementwise, so a NaN
@@ -308,7 +320,8 @@ static int factor_core(const rcp_config* cfg, int64_t n, const double* a, int64_
                        rcp_draw_fn draw, void* draw_ctx, void* workspace, size_t workspace_bytes, int64_t* perm,
                        double* Lout, double* d_diag, double* d_off, int8_t* pattern, int8_t* trace_kind,
                        int32_t* trace_r, rcp_stats* stats, int world, int emulate, void* worker_ws,
-                       size_t worker_ws_bytes, void* cuda_stream, double* L_host, const double* a_host) {
+                       size_t worker_ws_bytes, void* cuda_stream, double* L_host, const double* a_host,
+                       rcp_diag* diag) {
   if (stats) {
     memset(stats, 0, sizeof(*stats));
     stats->deficient_from = -1;
@@ -448,6 +461,14 @@ static int factor_core(const rcp_config* cfg, int64_t n, const double* a, int64_
   if (hscal->vflags[1]) return RCP_ERR_NONFINITE_INPUT;
   const double amax = hscal->amax;
 
+  const bool dsnap = diag && diag->track_full, daudit = diag && diag->audit && rcp_strat;
+  if (diag) {
+    diag->n_snapshots = diag->n_drift = 0;
+    if (dsnap) RCP_CHECK(cudaMemsetAsync(diag->snapshots, 0, sizeof(double) * 2 * (size_t)diag->cap, st));
+    if (diag->audit && diag->drift) RCP_CHECK(cudaMemsetAsync(diag->drift, 0, sizeof(double) * (size_t)diag->cap, st));
+    if (daudit)  // Omega in original column order (the permutation is the identity here)
+      RCP_CHECK(cudaMemcpyAsync(diag->omega_orig, omega_dev, sizeof(double) * (size_t)P * n, cudaMemcpyDeviceToDevice, st));
+  }
   // ---- sketch B = Omega A (factor.py:307-309) and guard setup (factor.py:314-317)
   if (rcp_strat) RCP_LAUNCH(launch_sketch_gemm(P, n, omega_dev, n, A[0], n, B[0], 0, st));
   const bool armed = rcp_strat && c.robust_r >= 1;  // factor.py:314
@@ -563,6 +584,7 @@ static int factor_core(const rcp_config* cfg, int64_t n, const double* a, int64_
       prm.B = B[curB];
       prm.Bout = B[curB ^ 1];
       prm.perm_cur = permb[pcur];
+      if (dsnap) RCP_LAUNCH(launch_snapshot(n, A[curA], din, diag->snapshots + 2 * (size_t)pidx, st));
       RCP_LAUNCH(launch_panel(prm, gmax, (size_t)smem_budget, st));
       RCP_LAUNCH(launch_panel_commit(din, dout, dplog, dstate, n, c.b, q_eff, P, (long long)Lay.snap_cap, st));
       RCP_LAUNCH(launch_gather(n, 0, 0, 0, tpad, 0, pol, Lbuf, W, permb[pcur], permb[pcur ^ 1], snap, phys, Lneg, Wg,
@@ -588,6 +610,9 @@ static int factor_core(const rcp_config* cfg, int64_t n, const double* a, int64_
         RCP_LAUNCH(launch_sketch_correction(P, n, 0, Y, tpad, c.b, Lneg, B[curB], phys, B[curB ^ 1], st, din, n));
       }
       // q = 1: the panel kernel itself wrote the per-step-updated sketch into B[curB ^ 1]
+      if (daudit)
+        RCP_LAUNCH(launch_drift(n, P, A[curA ^ 1], B[curB ^ 1], diag->omega_orig, permb[pcur ^ 1], din,
+                                diag->drift + pidx, st));
       curA ^= 1;
       curB ^= 1;
       pcur ^= 1;
@@ -680,6 +705,7 @@ static int factor_core(const rcp_config* cfg, int64_t n, const double* a, int64_
     draw_buf.resize((size_t)P * m0);
     if (draw(draw_ctx, P, m0, draw_buf.data()) != 0) return RCP_ERR_NEED_NORMALS;
     RCP_CHECK(cudaMemcpyAsync(omg, draw_buf.data(), sizeof(double) * (size_t)P * m0, cudaMemcpyHostToDevice, st));
+    if (daudit) RCP_LAUNCH(launch_omega_scatter(n, P, k0, omg, m0, permb[pcur], diag->omega_orig, st));
 #if !RCP_FULL_STORAGE
     RCP_LAUNCH(launch_mirror_lower(n, k0, A[curA], st));  // the projection reads full columns
 #endif
@@ -720,6 +746,12 @@ static int factor_core(const rcp_config* cfg, int64_t n, const double* a, int64_
     if (np > 0) {
       RCP_CHECK(cudaMemcpyAsync(logs.data(), dplog, sizeof(PanelLog) * (size_t)np, cudaMemcpyDeviceToHost, st));
       RCP_CHECK(cudaStreamSynchronize(st));
+    }
+    if (diag) {  // snapshots: one per step run (the stopping one included); drift: panels with k < n
+      diag->n_snapshots = dsnap ? (int64_t)np + (stop_k0 >= 0 ? 1 : 0) : 0;
+      int64_t nd = 0;
+      for (const PanelLog& lg : logs) nd += (lg.k_end < n) ? 1 : 0;
+      diag->n_drift = daudit ? nd : 0;
     }
     for (const PanelLog& lg : logs) {
       panels.push_back(PanelRecord{lg.k0, lg.k_end, (int64_t)lg.snap_off});

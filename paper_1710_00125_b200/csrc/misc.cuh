@@ -31,6 +31,13 @@ cudaError_t launch_deficient_fill(int64_t n, int64_t k0, const int* perm_cur, in
 cudaError_t launch_mirror_lower(int64_t n, int64_t k, double* A, cudaStream_t st);
 cudaError_t launch_iota(int64_t n, int* p, cudaStream_t st);
 
+// ---- experiment diagnostics (diag.cu): track_growth="full" snapshots and the audit_sketch drift
+cudaError_t launch_snapshot(int64_t n, const double* A, const PanelDesc* d, double* out, cudaStream_t st);
+cudaError_t launch_drift(int64_t n, int P, const double* A, const double* B, const double* omega_orig,
+                         const int* perm, const PanelDesc* d, double* out, cudaStream_t st);
+cudaError_t launch_omega_scatter(int64_t n, int P, int64_t k0, const double* om, int64_t m, const int* perm,
+                                 double* omega_orig, cudaStream_t st);
+
 // ---- FP64 tensor-core GEMMs (schur.cu)
 // A_out[k+i, k+j] = A_in(phys[i], phys[j]) - sum_s L[i,s] W[j,s]   for i >= j (lower tiles)
 cudaError_t launch_schur_update(int64_t n, int64_t k, int64_t mp, const double* Lneg, const double* Wg, int tpad,

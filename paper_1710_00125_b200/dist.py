@@ -138,16 +138,20 @@ def factor_distributed_device(a: torch.Tensor | None, cfg: FactorConfig | None =
     ops = ops if ops is not None else default_ops()
     if world == 1:
         return ops.factor(a, cfg, None, 1)
+    src = 0 if group is None else dist.get_global_rank(group, 0)  # group rank 0 as a global rank
     if rank == 0:
         if a is None:
             raise ValueError("rank 0 must pass the matrix")
         n = int(a.shape[0])
-        ws = ops.alloc_workspace(n, cfg)
         try:
+            ws = ops.alloc_workspace(n, cfg)
             ops.prepare(n, cfg, ws)  # zero the signal block before any worker can look at it
             plan = _Plan(ops.export(ws), n, cfg.p, cfg.b, cfg.q, cfg.robust_r, world)
-            obj = [plan]
-            dist.broadcast_object_list(obj, src=0, group=group)
+        except Exception as exc:  # release the workers (they wait in the broadcast) before raising
+            dist.broadcast_object_list([("setup-failed", repr(exc))], src=src, group=group)
+            raise
+        try:
+            dist.broadcast_object_list([plan], src=src, group=group)
             try:
                 f = ops.factor(a, cfg, ws, world)
             finally:
@@ -156,7 +160,9 @@ def factor_distributed_device(a: torch.Tensor | None, cfg: FactorConfig | None =
         finally:
             ops.free_workspace(ws)
     obj = [None]
-    dist.broadcast_object_list(obj, src=0, group=group)
+    dist.broadcast_object_list(obj, src=src, group=group)
+    if isinstance(obj[0], tuple) and obj[0] and obj[0][0] == "setup-failed":
+        raise RuntimeError(f"rank 0 failed to set up the distributed factorization: {obj[0][1]}")
     plan: _Plan = obj[0]
     ptr = ops.import_(plan.handle)
     try:

@@ -59,6 +59,28 @@ def kkt(n1: int, n2: int, seed: int = 0) -> np.ndarray:
     return mirror_lower_inplace(a)
 
 
+def kkt_c4(n1: int = 16000, n2: int = 4000, seed: int = 0) -> np.ndarray:
+    """Config 4 with an order-independent H: as :func:`kkt`, but G's N(0,1) draws are rounded
+    to multiples of 2^-8.  Every product g_i g_j then has <= 22 significant bits and every
+    partial sum of n1 <= 2^16 of them stays below 2^36 units of 2^-16, so G^T G is EXACT in
+    fp64 under any summation order (OpenBLAS here, a device GEMM on the GPU box): both sides
+    factor bit-identical matrices without shipping the 3.2 GB input."""
+    assert n1 <= 1 << 16
+    g = _gen(seed)
+    G = np.round(g.standard_normal((n1, n1)) * 256.0) / 256.0
+    Bm = g.standard_normal((n2, n1))
+    H = G.T @ G
+    del G
+    H /= n1
+    H += np.eye(n1)
+    n = n1 + n2
+    a = np.zeros((n, n))
+    a[:n1, :n1] = H
+    del H
+    a[n1:, :n1] = Bm
+    return mirror_lower_inplace(a)
+
+
 def scaled_member(n: int, seed: int, scaled: bool) -> np.ndarray:
     """One matrix of the batched configuration (config 5)."""
     g = _gen(seed)

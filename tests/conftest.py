@@ -25,7 +25,9 @@ def pytest_configure(config):
 
 
 def golden_names():
-    return sorted(p.stem for p in GOLDEN.glob("g_*.npz"))
+    """Small reference fixtures (inputs stored or cheap to regenerate); the full-size
+    BASELINE fixtures g_full_* are read by tests/test_full_size.py only."""
+    return sorted(p.stem for p in GOLDEN.glob("g_*.npz") if not p.stem.startswith("g_full_"))
 
 
 def load_golden(name):

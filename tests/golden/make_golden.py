@@ -114,8 +114,56 @@ def main_bk():
     save("g_bbk_exchange4", np.eye(4)[::-1].copy(), dict(strategy="bbk", b=2, q=1, p=5, seed=0))
 
 
+def save_diag(name, a, cfg, robust=False):
+    """Diagnostics fixtures: track_growth="full" snapshots and the
+    audit_sketch drift as the reference records them (factor.py:493-504, 514-531)."""
+    fn = randldl.factor_robust if robust else randldl.factor
+    f = fn(a, randldl.FactorConfig(**cfg))
+    dd, off = d_arrays(f)
+    s = f.stats
+    c = s.counters
+    out = dict(
+        a=a, perm=f.perm, pattern=f.pattern, d_diag=dd, d_off=off, L=f.L,
+        counters=np.array([c.mults, c.adds, c.divs, c.comps], dtype=np.int64),
+        rho_cheap=np.array(s.rho_cheap), max_multiplier=np.array(s.max_multiplier),
+        recompute_count=np.array(s.recompute_count),
+        snapshots=np.array(s.snapshots if s.snapshots is not None else [], dtype=np.float64).reshape(-1, 2),
+        has_snapshots=np.array(s.snapshots is not None),
+        drift=np.array(s.sketch_drift if s.sketch_drift is not None else [], dtype=np.float64),
+        has_drift=np.array(s.sketch_drift is not None),
+        rho_elem=np.array(np.nan if s.rho_elem is None else s.rho_elem),
+        rho_col=np.array(np.nan if s.rho_col is None else s.rho_col),
+        L_norm1=np.array(np.nan if s.L_norm1 is None else s.L_norm1),
+        Linv_norm1=np.array(np.nan if s.Linv_norm1 is None else s.Linv_norm1),
+        cfg=np.array(json.dumps(cfg)), robust=np.array(robust),
+    )
+    np.savez_compressed(HERE / "diag" / f"{name}.npz", **out)
+    print(name, "snapshots", len(s.snapshots or []), "drift", len(s.sketch_drift or []),
+          "recompute", s.recompute_count)
+
+
+def main_diag():
+    (HERE / "diag").mkdir(exist_ok=True)
+    sym = gallery.type6
+    save_diag("d_full_n100", sym(100, 1), dict(strategy="rcp", b=8, q=8, p=8, seed=7, track_growth="full"))
+    save_diag("d_audit_n100", sym(100, 1), dict(strategy="rcp", b=8, q=8, p=8, seed=7, audit_sketch=True))
+    save_diag("d_both_n61", sym(61, 2), dict(strategy="rcp", b=16, q=1, p=10, seed=3, track_growth="full",
+                                            audit_sketch=True))
+    save_diag("d_both_c5_scaled", gallery.scaled_member(256, 10, True),
+              dict(strategy="rcp", b=16, q=16, p=24, seed=0, track_growth="full", audit_sketch=True))
+    tail = np.zeros((65, 65))
+    tail[:40, :40] = sym(40, 5)
+    save_diag("d_full_zero_tail", tail, dict(strategy="rcp", b=16, q=16, p=16, seed=2, track_growth="full",
+                                             audit_sketch=True), robust=True)
+    save_diag("d_full_bkpp", sym(80, 4), dict(strategy="bkpp", b=8, q=1, p=5, seed=0, track_growth="full"))
+    save_diag("d_full_kkt", gallery.kkt(160, 40, 4), dict(strategy="rcp", b=16, q=16, p=26, seed=0,
+                                                           track_growth="full"))
+
+
 if __name__ == "__main__":
     if "--bk" in sys.argv:
         main_bk()
+    elif "--diag" in sys.argv:
+        main_diag()
     else:
         main()
