@@ -97,6 +97,8 @@ def parse():
     ap.add_argument("--count", type=int, default=65536, help="c5: matrices in the whole job")
     ap.add_argument("--e2e-chunk", type=int, default=296, help="c5: matrices per pipelined e2e chunk")
     ap.add_argument("--solve-reps", type=int, default=10, help="c3: timed device solves")
+    ap.add_argument("--ref-seconds", type=float, default=150.0,
+                    help="--impl reference: budget of timed reference panels (each ~70 s at C3 on 16 cores)")
     return ap.parse_args()
 
 
@@ -237,10 +239,11 @@ def cores_used() -> int:
 
 
 # ----------------------------------------------------------------------------- reference arm
-def ref_sample(a_host, args, max_panels: int, skip_panels: int):
+def ref_sample(a_host, args, max_panels: int, skip_panels: int, budget_s: float = 1e30):
     """Time the REFERENCE itself (oracle/_ref/randldl) panel by panel through its own engine:
     _Engine(a, cfg) (validation, copy, Omega, B = Omega A: setup, untimed), then _run_panel()
-    exactly as _Engine.run() loops (factor.py:508-513)."""
+    exactly as _Engine.run() loops (factor.py:508-513).  Stops after max_panels timed panels or
+    once the timed panels exceed budget_s (at least one is always timed)."""
     randldl = load_reference()
     fmod = sys.modules["randldl.factor"]
     cfg = randldl.FactorConfig(strategy="rcp", b=args.b, q=args.b, p=args.p, seed=args.seed)
@@ -258,6 +261,8 @@ def ref_sample(a_host, args, max_panels: int, skip_panels: int):
         if npan > skip_panels:
             times.append(dt)
             works.append(work_flops(eng.n, k0, eng.k))
+            if sum(times) >= budget_s:
+                break
     return {"t_setup": t_setup, "times": times, "works": works, "k_done": eng.k, "panels": npan}
 
 
@@ -266,8 +271,13 @@ def run_reference(args, rank: int):
         return
     from paper_1710_00125_b200 import gallery
     a_host = gallery.type6(args.n, args.seed)
+    warm = args.warmup
     if load_reference() is not None:
-        res = ref_sample(a_host, args, max_panels=args.steps, skip_panels=args.warmup)
+        # One C3 panel of the reference takes ~70 s on a 16-core host (mirror_lower's tril_indices
+        # scatter, core.py:115-119, dominates), so the sample is bounded: at most one untimed warm-up
+        # panel and --ref-seconds of timed panels (at least one).
+        warm = min(args.warmup, 1)
+        res = ref_sample(a_host, args, max_panels=args.steps, skip_panels=warm, budget_s=args.ref_seconds)
         kind = "reference"
         what = f"the unmodified reference randldl (oracle/_ref, numpy {np.__version__} + OpenBLAS), _Engine._run_panel"
     else:
@@ -276,13 +286,14 @@ def run_reference(args, rank: int):
         what = f"oracle port (numpy {np.__version__} + OpenBLAS; oracle/_ref absent)"
     tsum = sum(res["times"])
     value = sum(res["works"]) / tsum / 1e9
-    sample = (f"{what} on the config-3 matrix: panels {args.warmup + 1}..{args.warmup + args.steps} timed one per "
-              f"step (panels 1..{args.warmup} warm-up), columns 0..{res['k_done']} eliminated; value = sum (n-j)^2 "
-              f"over the timed panels' columns / time; setup (validation, copy, Omega*A) {res['t_setup']:.1f} s "
-              f"excluded; CPU {cpu_model()}")
+    nt = len(res["times"])
+    sample = (f"{what} on the config-3 matrix: panels {warm + 1}..{warm + nt} timed one per step "
+              f"({nt} of the {args.steps} requested; panels 1..{warm} warm-up), columns 0..{res['k_done']} "
+              f"eliminated; value = sum (n-j)^2 over the timed panels' columns / time; setup (validation, copy, "
+              f"Omega*A) {res['t_setup']:.1f} s excluded; CPU {cpu_model()}")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tsum / max(1, len(res["times"])),
+        "steps": nt, "steps_requested": args.steps, "warmup": warm, "ms_per_step": 1e3 * tsum / max(1, nt),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded numpy Philox type6)", "config": cfg_dict(args, args.gpus),
         "cpu_baseline": {"value": value, "unit": "GFLOP/s", "cores": cores_used(), "kind": kind,

@@ -37,8 +37,12 @@ from .batched import (  # noqa: F401
     BatchedDeviceFactorization,
     factor_batched,
     factor_batched_device,
+    factor_batched_sharded,
+    shard_range,
     solve_batched,
     solve_batched_device,
 )
 
-__version__ = "0.1.0"
+from . import grid  # noqa: F401,E402
+
+__version__ = "0.2.0"

@@ -353,6 +353,11 @@ def _config(cfg: FactorConfig | None, overrides: dict) -> FactorConfig:
         raise ValueError("pass either cfg or keyword overrides, not both")
     if cfg is None:
         cfg = FactorConfig(**overrides)
+    elif not isinstance(cfg, FactorConfig):  # e.g. the reference's own randldl.FactorConfig
+        cfg = FactorConfig(strategy=getattr(cfg.strategy, "value", cfg.strategy), p=cfg.p, b=cfg.b, q=cfg.q,
+                           seed=cfg.seed, robust_r=cfg.robust_r,
+                           track_growth=getattr(cfg.track_growth, "value", cfg.track_growth),
+                           audit_sketch=bool(cfg.audit_sketch))
     return cfg
 
 

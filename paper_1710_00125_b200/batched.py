@@ -31,7 +31,7 @@ from .api import (BlockDiag, DeviceFactorization, Factorization, FactorConfig, G
                   factor_device)
 
 __all__ = ["BatchedDeviceFactorization", "factor_batched_device", "factor_batched_host", "factor_batched", "solve_batched_device",
-           "solve_batched", "batched_workspace_bytes", "normal_stream"]
+           "solve_batched", "batched_workspace_bytes", "normal_stream", "shard_range", "factor_batched_sharded"]
 
 MAX_N = 256
 
@@ -297,6 +297,78 @@ def factor_batched_host(a: torch.Tensor, cfg: FactorConfig | None = None, *, chu
         if bad.size:
             i = int(bad[0])
             _raise_matrix(i, out.stats[i])
+    return out
+
+
+def shard_range(count: int, rank: int, world: int) -> tuple:
+    """Contiguous, balanced shard [start, stop) of ``count`` independent matrices for ``rank`` of
+    ``world`` (config C5: sharded by matrix, no communication; the first count % world shards
+    get one extra matrix)."""
+    if world < 1 or not (0 <= rank < world):
+        raise ValueError(f"rank {rank} outside world {world}")
+    base, extra = divmod(count, world)
+    start = rank * base + min(rank, extra)
+    return start, start + base + (1 if rank < extra else 0)
+
+
+def factor_batched_sharded(a: torch.Tensor, cfg: FactorConfig | None = None, *, devices=None,
+                           chunk: int = 296, check: bool = True, **overrides) -> BatchedDeviceFactorization:
+    """Factor a host stack (CPU float64 ``[count, n, n]``, ideally pinned) on several GPUs of this
+    process: matrix shard ``shard_range(count, r, len(devices))`` goes to ``devices[r]`` (default:
+    every visible GPU), each through :func:`factor_batched_host` in its own host thread (the
+    native calls release the GIL), results land in one pinned host
+    :class:`BatchedDeviceFactorization`.  Same results as :func:`factor_batched_host` on one GPU
+    (every matrix restarts the same normal stream).  Under torchrun, give each rank its own
+    ``shard_range`` slice instead."""
+    import threading
+
+    cfg = _config(cfg, overrides)
+    _check_supported(cfg, batched=True)
+    if a.dim() != 3 or a.shape[1] != a.shape[2] or a.is_cuda or a.dtype != torch.float64:
+        raise ValueError("factor_batched_sharded expects a host (CPU) float64 [count, n, n] stack")
+    if devices is None:
+        devices = list(range(torch.cuda.device_count()))
+    devices = [torch.device("cuda", d) if isinstance(d, int) else torch.device(d) for d in devices]
+    if not devices:
+        raise _native.NativeUnavailable("no CUDA device: the B200 build has no CPU fallback")
+    count, n = int(a.shape[0]), int(a.shape[1])
+    a = a.contiguous()
+    pin = True
+    out = BatchedDeviceFactorization(
+        perm=torch.empty(count, n, dtype=torch.int64, pin_memory=pin),
+        L=torch.empty(count, n, n, dtype=torch.float64, pin_memory=pin),
+        d_diag=torch.empty(count, n, dtype=torch.float64, pin_memory=pin),
+        d_off=torch.empty(count, n, dtype=torch.float64, pin_memory=pin),
+        pattern=torch.empty(count, n, dtype=torch.int8, pin_memory=pin),
+        stats=np.zeros(count, dtype=_native.BATCH_STATS_DTYPE))
+    errors = [None] * len(devices)
+
+    def work(r, dev):
+        s0, s1 = shard_range(count, r, len(devices))
+        if s1 <= s0:
+            return
+        try:
+            with torch.cuda.device(dev):
+                part = BatchedDeviceFactorization(out.perm[s0:s1], out.L[s0:s1], out.d_diag[s0:s1],
+                                                  out.d_off[s0:s1], out.pattern[s0:s1], None)
+                res = factor_batched_host(a[s0:s1], cfg, chunk=chunk, out=part, check=False)
+                torch.cuda.synchronize(dev)
+            out.stats[s0:s1] = res.stats
+        except BaseException as exc:  # re-raised on the caller's thread
+            errors[r] = exc
+
+    threads = [threading.Thread(target=work, args=(r, d)) for r, d in enumerate(devices)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    for exc in errors:
+        if exc is not None:
+            raise exc
+    if check:
+        bad = np.nonzero(out.stats["status"] != _native.RCP_OK)[0]
+        if bad.size:
+            _raise_matrix(int(bad[0]), out.stats[int(bad[0])])
     return out
 
 

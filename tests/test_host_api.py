@@ -99,3 +99,46 @@ def test_batched_host_validates_before_device():
         batched.factor_batched_host(torch.zeros(4, 8, 8, dtype=torch.float32), cfg)
     with pytest.raises(ValueError, match="at least one row"):
         batched.factor_batched_host(torch.zeros(4, 0, 0, dtype=torch.float64), cfg)
+
+
+def test_shard_range_partitions_the_batch():
+    from paper_1710_00125_b200 import shard_range
+    for count in (0, 1, 7, 65536, 65537):
+        for world in (1, 2, 3, 8):
+            spans = [shard_range(count, r, world) for r in range(world)]
+            assert spans[0][0] == 0 and spans[-1][1] == count
+            assert all(spans[i][1] == spans[i + 1][0] for i in range(world - 1))
+            sizes = [e - s for s, e in spans]
+            assert max(sizes) - min(sizes) <= 1
+    with pytest.raises(ValueError):
+        shard_range(10, 3, 3)
+
+
+def test_foreign_factor_config_is_accepted():
+    """The reference's own FactorConfig objects (str-Enum fields) convert to this package's."""
+    import enum
+    from dataclasses import dataclass
+
+    from paper_1710_00125_b200 import api
+
+    class S(str, enum.Enum):
+        RCP = "rcp"
+
+    class G(str, enum.Enum):
+        FULL = "full"
+
+    @dataclass
+    class Foreign:
+        strategy: S = S.RCP
+        p: int = 7
+        b: int = 4
+        q: int = 4
+        seed: int = 3
+        robust_r: int = 2
+        track_growth: G = G.FULL
+        audit_sketch: bool = True
+
+    c = api._config(Foreign(), {})
+    assert isinstance(c, api.FactorConfig)
+    assert (c.strategy, c.p, c.b, c.q, c.seed, c.robust_r) == (api.Strategy.RCP, 7, 4, 4, 3, 2)
+    assert c.track_growth is api.GrowthTracking.FULL and c.audit_sketch
