@@ -42,15 +42,19 @@ def needs_build() -> bool:
     return any(p.stat().st_mtime > t for p in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    """Compile each .cu to an object in parallel (nvcc per file), then link the shared library."""
-    if not force and not needs_build():
+def build(force: bool = False, verbose: bool = False, out: Path | None = None, defines: list | None = None) -> Path:
+    """Compile each .cu to an object in parallel (nvcc per file), then link the shared library.
+    ``out`` / ``defines`` build an experiment variant (e.g. ``librcp_lower.so`` with
+    ``-DRCP_FULL_STORAGE=0``), selected at run time with ``RCP_B200_LIB``."""
+    target = Path(out) if out else OUT
+    if out is None and not force and not needs_build():
         return OUT
     from concurrent.futures import ThreadPoolExecutor
     extra = ["-DRCP_PANEL_PROF=1"] if os.environ.get("RCP_PANEL_PROF") == "1" else []
     if os.environ.get("RCP_BATCH_PROF") == "1":
         extra.append("-DRCP_BATCH_PROF=1")
-    objdir = ROOT / "build" / "obj"
+    extra += list(defines or [])
+    objdir = ROOT / "build" / ("obj" if out is None else "obj_" + target.stem)
     objdir.mkdir(parents=True, exist_ok=True)
     compile_flags = [f for f in NVCC_FLAGS if f != "-shared"]
     nvcc = _nvcc()
@@ -65,14 +69,21 @@ def build(force: bool = False, verbose: bool = False) -> Path:
 
     with ThreadPoolExecutor(max_workers=max(1, min(len(sources()), os.cpu_count() or 1))) as ex:
         objs = list(ex.map(one, sources()))
-    cmd = [nvcc, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", str(OUT) + ".tmp", *map(str, objs)]
+    cmd = [nvcc, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", str(target) + ".tmp", *map(str, objs)]
     if verbose:
         print(" ".join(cmd), flush=True)
     subprocess.run(cmd, check=True, cwd=str(ROOT))
-    os.replace(str(OUT) + ".tmp", OUT)
-    return OUT
+    os.replace(str(target) + ".tmp", target)
+    return target
 
 
 if __name__ == "__main__":
-    p = build(force="--force" in sys.argv, verbose=True)
+    # python -m paper_1710_00125_b200.build [--force] [--variant NAME -DFOO=1 ...]
+    argv = sys.argv[1:]
+    if "--variant" in argv:
+        name = argv[argv.index("--variant") + 1]
+        defs = [a for a in argv if a.startswith("-D")]
+        p = build(verbose=True, out=PKG / f"librcp_{name}.so", defines=defs)
+    else:
+        p = build(force="--force" in argv, verbose=True)
     print(p)

@@ -127,8 +127,8 @@ cudaError_t launch_schur_update_dyn(int64_t n, const double* Lneg, const double*
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  schur_ws_kernel<true><<<(unsigned)sms, ws::kThreads, schur_ws_smem_bytes(), st>>>(Lneg, Wg, tpad, 0, nullptr, nullptr, phys,
-                                                                             n, 0, 0, 0, nullptr, part, nparts, dyn);
+  schur_ws_kernel<true><<<(unsigned)sms, ws::kThreads, schur_ws_smem_bytes(), st>>>(
+        Lneg, Wg, tpad, 0, nullptr, nullptr, phys, n, 0, 0, 0, nullptr, part, nparts, dyn);
   return cudaGetLastError();
 }
 

@@ -346,4 +346,6 @@ schur_ws_kernel(const double* __restrict__ Lneg, const double* __restrict__ Wg, 
 
 inline size_t schur_ws_smem_bytes() { return sizeof(ws::Smem); }
 
+
+
 }  // namespace rcp
