@@ -217,6 +217,15 @@ size_t rcp_worker_workspace_bytes(int64_t n, const rcp_config* cfg);
 int rcp_dist_prepare(int64_t n, const rcp_config* cfg, void* workspace, void* cuda_stream);
 int rcp_schur_worker(const rcp_config* cfg, int64_t n, int rank, int world, void* rank0_workspace,
                      void* worker_ws, size_t worker_ws_bytes, void* cuda_stream);
+/* Host-side plan of one panel's trailing update: the tiles (m0 = first trailing row, n0 = first
+ * column or, for a sketch tile, first sketch row; sketch = 1 for the fused sketch-correction tiles,
+ * which exist only when P > 0 on a single device) that device `part` of `nparts` processes, in the
+ * order its `grid` CTAs take them (CTA 0's tiles, then CTA 1's, ...).  Computed with the same
+ * functions the kernel uses (schur_ws.cuh tile_sequence / tile_at); lets the distributed host
+ * logic and its tests check the dealing without a GPU.  Returns the tile count (entries beyond
+ * cap are not written), -1 on bad arguments. */
+int64_t rcp_schur_tile_plan(int64_t mp, int32_t P, int32_t part, int32_t nparts, int32_t grid,
+                            int64_t* m0, int64_t* n0, int8_t* sketch, int64_t cap);
 /* Dense host copy of a device unit-lower L (row-major n x n): the lower trapezoid is copied,
  * the strictly upper part is written as zeros on the host; synchronises cuda_stream.
  * Replaces the dense L transfer of the reference's result (factor.py:637-647 returns L dense). */

@@ -55,6 +55,7 @@ EXPORTED_SYMBOLS = (
     "rcp_ipc_export",
     "rcp_ipc_import",
     "rcp_ipc_close",
+    "rcp_schur_tile_plan",
 )
 
 
@@ -209,6 +210,9 @@ def load(path: str | os.PathLike | None = None):
     lib.rcp_ipc_import.restype = ctypes.c_int
     lib.rcp_ipc_close.argtypes = [vp]
     lib.rcp_ipc_close.restype = ctypes.c_int
+    lib.rcp_schur_tile_plan.argtypes = [i64, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, vp, vp,
+                                        vp, i64]
+    lib.rcp_schur_tile_plan.restype = i64
     lib.rcp_version.argtypes = []
     lib.rcp_version.restype = ctypes.c_char_p
     _lib = lib

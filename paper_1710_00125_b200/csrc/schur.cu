@@ -199,3 +199,29 @@ cudaError_t launch_sketch_correction(int P, int64_t mp, int64_t k, const double*
 }
 
 }  // namespace rcp
+
+extern "C" int64_t rcp_schur_tile_plan(int64_t mp, int32_t P, int32_t part, int32_t nparts, int32_t grid,
+                                       int64_t* m0, int64_t* n0, int8_t* sketch, int64_t cap) {
+  using namespace rcp;
+  if (mp < 1 || P < 0 || nparts < 1 || part < 0 || part >= nparts || grid < 1) return -1;
+  const long long nbi = (mp + ws::BM - 1) / ws::BM;
+  const long long tiles_tri = nbi * (nbi + 1);
+  const int nbp = P > 0 ? (P + ws::BN - 1) / ws::BN : 0;
+  const long long tiles = tiles_tri + nbi * nbp;
+  int64_t cnt = 0;
+  for (int cta = 0; cta < grid; ++cta) {
+    long long x0, xs;
+    ws::tile_sequence(nparts > 1, part, nparts, cta, grid, x0, xs);
+    for (long long x = x0; x < tiles; x += xs, ++cnt) {
+      if (cnt < cap) {
+        int64_t a, b;
+        const bool sk = ws::tile_at(x, tiles_tri, nbp, a, b);
+        if (m0) m0[cnt] = a;
+        if (n0) n0[cnt] = b;
+        if (sketch) sketch[cnt] = sk ? 1 : 0;
+      }
+    }
+  }
+  return cnt;
+}
+

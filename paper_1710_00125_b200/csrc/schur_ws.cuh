@@ -87,12 +87,31 @@ RCP_D void mbar_wait(unsigned long long* b, unsigned parity) {
 RCP_D void st_c(double* p, double v) { *p = v; }  // (streaming stores measured: no difference)
 RCP_D void named_sync(int id, int nthreads) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory"); }
 
-RCP_D void tile_of(long long x, int64_t& m0, int64_t& n0) {
+// Lower-triangle tile x -> (m0, n0): row block I holds 2I + 2 column blocks of BN = BM / 2.
+RCP_HD void tile_of(long long x, int64_t& m0, int64_t& n0) {
   long long I = static_cast<long long>((sqrt(4.0 * (double)x + 1.0) - 1.0) * 0.5);
   while (I * (I + 1) > x) --I;
   while ((I + 1) * (I + 2) <= x) ++I;
   m0 = I * BM;
   n0 = (x - I * (I + 1)) * BN;
+}
+// Tile list of one panel's update: nbi (nbi + 1) lower-triangle tiles, then nbi * nbp sketch tiles
+// (sketch rows n0..n0+BN of the 128-row block m0).  Returns true for a sketch tile.
+RCP_HD bool tile_at(long long x, long long tiles_tri, int nbp, int64_t& m0, int64_t& n0) {
+  if (x < tiles_tri) {
+    tile_of(x, m0, n0);
+    return false;
+  }
+  const long long sx = x - tiles_tri;
+  m0 = (sx / nbp) * BM;
+  n0 = (sx % nbp) * BN;
+  return true;
+}
+// The tiles CTA `cta` of a `grid`-CTA launch takes on device `part` of `nparts` sharing the update:
+// x = first, first + step, ... (tiles dealt round robin to the devices, then to their CTAs).
+RCP_HD void tile_sequence(bool multi, int part, int nparts, int cta, int grid, long long& first, long long& step) {
+  first = multi ? part + (long long)nparts * cta : (long long)cta;
+  step = multi ? (long long)nparts * grid : (long long)grid;
 }
 
 }  // namespace ws
@@ -129,16 +148,7 @@ schur_ws_kernel(const double* __restrict__ Lneg, const double* __restrict__ Wg, 
   }
   // tile x: lower-triangle tile (returns false) or sketch tile (true): rows m0 of -L21, sketch
   // rows n0 (of Y and B)
-  auto tile_at = [&](long long x, int64_t& m0, int64_t& n0) -> bool {
-    if (x < tiles_tri) {
-      tile_of(x, m0, n0);
-      return false;
-    }
-    const long long sx = x - tiles_tri;
-    m0 = (sx / nbp) * BM;
-    n0 = (sx % nbp) * BN;
-    return true;
-  };
+  auto tile_at = [&](long long x, int64_t& m0, int64_t& n0) -> bool { return ws::tile_at(x, tiles_tri, nbp, m0, n0); };
   unsigned long long* const ts_schur = (tstamp && d) ? tstamp + 4 * (size_t)d->pidx + 2 : nullptr;
   stamp_start(ts_schur);
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -147,8 +157,8 @@ schur_ws_kernel(const double* __restrict__ Lneg, const double* __restrict__ Wg, 
   const int KT = Kl / kBK;
   // tile sequence of this CTA: x0, x0 + xs, ...  (multi-GPU: tiles are dealt round robin to the
   // nparts devices sharing the update, then to their CTAs)
-  const long long x0 = kMulti ? part + (long long)nparts * blockIdx.x : (long long)blockIdx.x;
-  const long long xs = kMulti ? (long long)nparts * gridDim.x : (long long)gridDim.x;
+  long long x0, xs;
+  tile_sequence(kMulti, part, nparts, (int)blockIdx.x, (int)gridDim.x, x0, xs);
   if (tid == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&sm.full[s], kProdThreads);

@@ -25,7 +25,24 @@ import torch.distributed as dist
 from . import _native
 from .api import FactorConfig, _check_supported, _config, _stream, factor_device
 
-__all__ = ["factor_distributed_device", "factor_distributed", "DeviceOps"]
+__all__ = ["factor_distributed_device", "factor_distributed", "DeviceOps", "tile_plan"]
+
+
+def tile_plan(mp: int, P: int, part: int, nparts: int, grid: int):
+    """The trailing-update tiles device ``part`` of ``nparts`` processes for one panel (``mp``
+    trailing rows, ``P`` fused sketch rows -- 0 when the update is shared), in its CTAs' order,
+    as numpy arrays (m0, n0, is_sketch).  Computed by the C ABI (``rcp_schur_tile_plan``) with
+    the same dealing functions the CUDA kernel runs; needs no GPU."""
+    import numpy as np
+    lib = _native.load()
+    cnt = int(lib.rcp_schur_tile_plan(mp, P, part, nparts, grid, None, None, None, 0))
+    if cnt < 0:
+        raise ValueError("bad tile plan arguments")
+    m0 = np.empty(cnt, dtype=np.int64)
+    n0 = np.empty(cnt, dtype=np.int64)
+    sk = np.empty(cnt, dtype=np.int8)
+    lib.rcp_schur_tile_plan(mp, P, part, nparts, grid, m0.ctypes.data, n0.ctypes.data, sk.ctypes.data, cnt)
+    return m0, n0, sk.astype(bool)
 
 
 @dataclass

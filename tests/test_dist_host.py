@@ -89,3 +89,61 @@ def test_protocol_over_gloo(world):
         assert log[0] == ("import", b"H" * 64)
         assert log[1] == ("worker", 40, 16, 16, 24, world, r, 0xDEF000)
         assert log[2] == ("close", 0xDEF000)
+
+
+def _plan_body(rank, world, port, q):
+    """Each rank asks the C ABI (no GPU) for its share of several panels' updates; the shares are
+    exchanged over gloo and rank 0 checks they cover every tile exactly once."""
+    import torch.distributed as dist
+
+    from paper_1710_00125_b200 import dist as rdist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        mine = {}
+        for mp in (1, 100, 128, 129, 1000, 4097, 30100):
+            m0, n0, sk = rdist.tile_plan(mp, 0, rank, world, 148)
+            mine[mp] = (m0.tolist(), n0.tolist(), sk.tolist())
+        allp = [None] * world
+        dist.all_gather_object(allp, mine)
+        q.put((rank, allp if rank == 0 else None))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_tile_dealing_over_gloo(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 29711 + world
+    procs = [ctx.Process(target=_plan_body, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = {}
+    for _ in range(world):
+        rank, payload = q.get(timeout=120)
+        res[rank] = payload
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    shares = res[0]
+    for mpv in (1, 100, 128, 129, 1000, 4097, 30100):
+        nbi = (mpv + 127) // 128
+        expect = {(I * 128, J * 64) for I in range(nbi) for J in range(2 * I + 2)}
+        seen = []
+        for r in range(world):
+            m0, n0, sk = shares[r][mpv]
+            assert not any(sk)  # no fused sketch tiles when the update is shared
+            seen += list(zip(m0, n0))
+        assert len(seen) == len(expect) and set(seen) == expect, mpv
+        sizes = [len(shares[r][mpv][0]) for r in range(world)]
+        assert max(sizes) - min(sizes) <= 148, sizes  # round robin: balanced to within one tile per CTA
+
+
+def test_single_device_plan_includes_sketch_tiles():
+    from paper_1710_00125_b200 import dist as rdist
+    m0, n0, sk = rdist.tile_plan(1000, 144, 0, 1, 148)
+    nbi = (1000 + 127) // 128
+    assert int(sk.sum()) == nbi * 3 and len(m0) == nbi * (nbi + 1) + nbi * 3
+    assert set(zip(m0[sk].tolist(), n0[sk].tolist())) == {(I * 128, j * 64) for I in range(nbi) for j in range(3)}
