@@ -85,41 +85,77 @@ def parse():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--n", type=int, default=32768)
-    ap.add_argument("--b", type=int, default=128)
-    ap.add_argument("--p", type=int, default=144, help="sketch rows P (reference FactorConfig.p = b + oversampling)")
+    ap.add_argument("--n", type=int, default=None, help="default: the workload's (C2 8192, C3 32768, C4 20000)")
+    ap.add_argument("--b", type=int, default=None)
+    ap.add_argument("--p", type=int, default=None, help="sketch rows P (reference FactorConfig.p = b + oversampling)")
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--cpu-seconds", type=float, default=20.0, help="budget of the cpu_baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--workload", default="c3", choices=["c3", "c5"],
-                    help="c3: n=32768 single matrix (headline); c5: 65536 x n=256 batched (b=16, p=8)")
+    ap.add_argument("--workload", default="c3", choices=["c2", "c3", "c4", "c5"],
+                    help="c3: n=32768 single matrix (headline); c2: n=8192 b=64; c4: KKT n=20000 b=64; "
+                         "c5: 65536 x n=256 batched (b=16, p=8)")
     ap.add_argument("--count", type=int, default=65536, help="c5: matrices in the whole job")
     ap.add_argument("--e2e-chunk", type=int, default=296, help="c5: matrices per pipelined e2e chunk")
     ap.add_argument("--solve-reps", type=int, default=10, help="c3: timed device solves")
     ap.add_argument("--ref-seconds", type=float, default=150.0,
                     help="--impl reference: budget of timed reference panels (each ~70 s at C3 on 16 cores)")
-    return ap.parse_args()
+    args = ap.parse_args()
+    dn, db, dp = WORKLOADS.get(args.workload, WORKLOADS["c3"])[:3]
+    args.n = dn if args.n is None else args.n
+    args.b = db if args.b is None else args.b
+    args.p = dp if args.p is None else args.p
+    return args
+
+
+# single-matrix workloads: (n, b, P, generator); BASELINE.json configs 2-4 (SURVEY section 8 mapping)
+WORKLOADS = {
+    "c2": (8192, 64, 74, "type6"),
+    "c3": (32768, 128, 144, "type6"),
+    "c4": (20000, 64, 74, "kkt_c4"),
+}
+
+
+def make_matrix(args):
+    from paper_1710_00125_b200 import gallery
+    if WORKLOADS.get(args.workload, WORKLOADS["c3"])[3] == "kkt_c4":
+        n1 = args.n * 4 // 5
+        return gallery.kkt_c4(n1, args.n - n1, args.seed)
+    return gallery.type6(args.n, args.seed)
+
+
+def metric_name(args):
+    return METRIC if args.workload == "c3" else (
+        f"RCP LDL^T fp64 GFLOP/s (n³/3) at n={args.n} ({args.workload.upper()}), % of FP64 peak")
 
 
 def workload_name(a):
-    return (f"C3 type6 (seeded iid N(0,1) lower triangle mirrored) n={a.n}, b={a.b}, q=b, "
+    if a.workload == "c4":
+        return (f"C4 KKT [[H, B^T], [B, 0]] n={a.n} (H = G^T G / n1 + I, G on a 2^-8 grid so G^T G is exact; "
+                f"B iid N(0,1)), b={a.b}, q=b, P=b+{a.p - a.b}={a.p} sketch rows, seed={a.seed}")
+    return (f"{a.workload.upper()} type6 (seeded iid N(0,1) lower triangle mirrored) n={a.n}, b={a.b}, q=b, "
             f"P=b+{a.p - a.b}={a.p} sketch rows, seed={a.seed}")
 
 
 def ncu_traffic(kernel: str, detail: bool = False):
-    """DRAM bytes (read + write) of one profiled launch of `kernel` from the committed ncu summary
-    (profiles/r01_ncu_traffic.json); with detail, the launch it refers to and its algorithmic bytes."""
-    path = Path(__file__).resolve().parent / "profiles" / "r01_ncu_traffic.json"
-    try:
-        rec = json.loads(path.read_text())[kernel]
-    except (OSError, KeyError, ValueError):
+    """DRAM bytes (read + write) of one profiled launch of `kernel` from the committed ncu summaries
+    (profiles/r02_ncu_traffic.json, then r01); with detail, the launch it refers to and its
+    algorithmic bytes.  Keys: kernel name (C3 / C5 captures) or "<kernel>@c2" etc."""
+    rec, path = None, None
+    for name in ("r02_ncu_traffic.json", "r01_ncu_traffic.json"):
+        path = Path(__file__).resolve().parent / "profiles" / name
+        try:
+            rec = json.loads(path.read_text())[kernel]
+            break
+        except (OSError, KeyError, ValueError):
+            rec = None
+    if rec is None:
         return None
     total = rec["dram_read_bytes"] + rec["dram_write_bytes"]
     if not detail:
         return total
     return {k: rec[k] for k in rec if k not in ("dram_read_bytes", "dram_write_bytes")} | {
-        "dram_bytes": total, "source": "profiles/r01_ncu_traffic.json (ncu --set full, one launch)"}
+        "dram_bytes": total, "source": f"profiles/{path.name} (ncu --set full, one launch)"}
 
 
 def c5_traffic(count: int):
@@ -136,7 +172,7 @@ def cfg_dict(a, world: int = 1):
             "oversampling": a.p - a.b,
             "parallelism": "single GPU" if world == 1 else
                            f"{world} GPUs: panels on rank 0, trailing-update tiles dealt round robin over NVLink",
-            "l2": "input 8.6 GB >> 126 MB L2 (no flush needed)"}
+            "l2": f"input {a.n * a.n * 8 / 1e9:.2f} GB >> 126 MB L2 (no flush needed)"}
 
 
 def work_flops(n: int, k0: int, k1: int) -> float:
@@ -269,8 +305,7 @@ def ref_sample(a_host, args, max_panels: int, skip_panels: int, budget_s: float 
 def run_reference(args, rank: int):
     if rank != 0:
         return
-    from paper_1710_00125_b200 import gallery
-    a_host = gallery.type6(args.n, args.seed)
+    a_host = make_matrix(args)
     warm = args.warmup
     if load_reference() is not None:
         # One C3 panel of the reference takes ~70 s on a 16-core host (mirror_lower's tril_indices
@@ -292,7 +327,7 @@ def run_reference(args, rank: int):
               f"eliminated; value = sum (n-j)^2 over the timed panels' columns / time; setup (validation, copy, "
               f"Omega*A) {res['t_setup']:.1f} s excluded; CPU {cpu_model()}")
     line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": args.gpus,
+        "impl": "reference", "metric": metric_name(args), "value": value, "unit": "GFLOP/s", "n_gpus": args.gpus,
         "steps": nt, "steps_requested": args.steps, "warmup": warm, "ms_per_step": 1e3 * tsum / max(1, nt),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded numpy Philox type6)", "config": cfg_dict(args, args.gpus),
@@ -320,7 +355,7 @@ def run_b200(args, rank: int, world: int, local_rank: int):
 
     a_host = a_pin = a_dev = omega = ws = None
     if rank == 0:
-        a_host = gallery.type6(n, args.seed)
+        a_host = make_matrix(args)
         a_pin = torch.from_numpy(a_host).pin_memory()
         a_dev = a_pin.to(dev, non_blocking=True)
         omega = torch.from_numpy(np.random.Generator(np.random.Philox(cfg.seed)).standard_normal((P, n))).to(dev)
@@ -437,8 +472,9 @@ def run_b200(args, rank: int, world: int, local_rank: int):
             cpu = {"value": None, "unit": "GFLOP/s", "cores": cores_used(), "kind": "port",
                    "sample": "host out of memory for the n=32768 oracle sample"}
     achieved = schur_flops / (schur_ms / 1e3) / 1e12 if schur_ms > 0 else None
+    schur_key = "schur_ws_kernel" if args.workload == "c3" else f"schur_ws_kernel@{args.workload}"
     line = {
-        "metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
+        "metric": metric_name(args), "value": value, "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
         "warmup": max(3, args.warmup), "ms_per_step": ms_max, "higher_is_better": True,
         "scaling": "strong" if world > 1 else "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded numpy Philox type6; Omega from Philox(seed))",
@@ -448,8 +484,8 @@ def run_b200(args, rank: int, world: int, local_rank: int):
         "roofline": {"bound": "tensor", "kernel": "schur_ws_kernel (trailing Schur update, DMMA.8x8x4)",
                      "achieved": achieved, "peak": FP64_PEAK_GFLOPS / 1e3, "unit": "TFLOP/s",
                      "frac": (achieved / (FP64_PEAK_GFLOPS / 1e3)) if achieved else None,
-                     "traffic": ncu_traffic("schur_ws_kernel"),
-                     "traffic_launch": ncu_traffic("schur_ws_kernel", detail=True),
+                     "traffic": ncu_traffic(schur_key),
+                     "traffic_launch": ncu_traffic(schur_key, detail=True),
                      "algorithmic": "sum over panels of t*m*(m+1) flops (lower-triangle rank-t update) + 2*P*t*m "
                                     "for the sketch-correction tiles the same kernel runs (single GPU)"
                                     + (" (rank 0's share of the tiles; achieved over its Schur time)" if world > 1
