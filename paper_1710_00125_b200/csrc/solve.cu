@@ -19,6 +19,7 @@
 // Summation orders are fixed (per-lane partials over the strip, then a fixed shuffle
 // tree), so the result is deterministic.
 #include <algorithm>
+#include <atomic>
 #include "gemm_dmma.cuh"
 #include "rcp_common.cuh"
 #include "solve.cuh"
@@ -28,7 +29,14 @@ namespace rcp {
 namespace {
 
 constexpr int NB = 64;
-constexpr int kSweepThreads = 256;  // 8 warps x 8 rows (forward) or 8 rows per strip block (backward)
+// 8 warps x 8 rows of a 64-row block (measured: 128-thread CTAs, 4 per SM so that every C3 block row
+// is resident from the start, were slower: 5.60 vs 4.56 ms -- the chain, not the tail, dominates)
+constexpr int kSweepThreads = 256;
+constexpr int kWarps = kSweepThreads / 32, kRPW = NB / kWarps;   // rows per warp
+constexpr int kMvLanes = kSweepThreads / NB, kMvCols = NB / kMvLanes;  // matrix-vector split
+// published strip blocks streamed per iteration (memory-level parallelism); measured at C3:
+// R = 1: kU 4 -> 4.36 ms, kU 2 -> 4.82 ms; R = 3: kU 2 -> 8.37 ms, kU 4 -> 9.13 ms (registers)
+// (strip_unroll: kU = 4 for one right-hand side, 2 for more)
 
 RCP_D int ld_acquire_i(const int* p) {
   int v;
@@ -37,25 +45,66 @@ RCP_D int ld_acquire_i(const int* p) {
 }
 RCP_D void st_release_i(int* p, int v) { asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory"); }
 
-// Inverse of every 64x64 unit-lower diagonal block of L (rows beyond n: identity), stored
-// row-major per block: Linv[blk][a][c], zero above the diagonal.  Thread c computes column c
-// by forward substitution against e_c.
-__global__ void __launch_bounds__(NB) diag_inverse_kernel(int64_t n, const double* __restrict__ L,
-                                                            double* __restrict__ Linv) {
-  __shared__ double X[NB][NB];  // column c belongs to thread c (conflict-free)
-  const int64_t i0 = (int64_t)blockIdx.x * NB;
+// Per 64-row block i of L (rows beyond n: identity / zero), all blocks in parallel:
+//   Linv_i = inverse of the unit-lower diagonal block L_ii           (row-major [a][c])
+//   M_i    = Linv_i L_{i,i-1}   (coupling of block i to the block before it, forward sweep)
+//   N_i    = Linv_i^T L_{i+1,i}^T   (coupling to the block after it, backward sweep)
+// With them the forward step is z_i = Linv_i (y_i - sum_{j<i-1} L_ij z_j) - M_i z_{i-1}: only the
+// last product waits for the previous block, so the serial chain per block is one flag hop and a
+// 64 x 64 matrix-vector product (same for the backward sweep with N_i).
+constexpr int kPrepThreads = 256;
+__global__ void __launch_bounds__(kPrepThreads) block_prep_kernel(int64_t n, int nblk, const double* __restrict__ L,
+                                                                   double* __restrict__ Linv, double* __restrict__ M,
+                                                                   double* __restrict__ N) {
+  extern __shared__ double sp[];
+  double(*X)[NB] = reinterpret_cast<double(*)[NB]>(sp);                // Linv_i, column c by thread c
+  double(*B)[NB + 1] = reinterpret_cast<double(*)[NB + 1]>(sp + NB * NB);  // an off-diagonal L block
+  const int i = blockIdx.x, tid = threadIdx.x;
+  const int64_t i0 = (int64_t)i * NB;
   const int nb = (int)(n - i0 < NB ? n - i0 : NB);
-  const int c = threadIdx.x;
-  for (int a = 0; a < NB; ++a) X[a][c] = 0.0;
-  X[c][c] = 1.0;
-  for (int a = c + 1; a < nb; ++a) {  // L_ii rows are read by all threads at once (broadcast)
-    const double* la = L + (i0 + a) * n + i0;
-    double s = 0.0;
-    for (int j = c; j < a; ++j) s = __fma_rn(__ldg(la + j), X[j][c], s);
-    X[a][c] = -s;
+  if (tid < NB) {
+    const int c = tid;
+    for (int a = 0; a < NB; ++a) X[a][c] = 0.0;
+    X[c][c] = 1.0;
+    for (int a = c + 1; a < nb; ++a) {  // L_ii rows are read by all threads at once (broadcast)
+      const double* la = L + (i0 + a) * n + i0;
+      double s = 0.0;
+      for (int j = c; j < a; ++j) s = __fma_rn(__ldg(la + j), X[j][c], s);
+      X[a][c] = -s;
+    }
   }
-  double* out = Linv + (int64_t)blockIdx.x * NB * NB;
-  for (int a = 0; a < NB; ++a) out[a * NB + c] = X[a][c];
+  __syncthreads();
+  for (int e = tid; e < NB * NB; e += kPrepThreads) Linv[(int64_t)i * NB * NB + e] = X[e >> 6][e & 63];
+  // M_i = Linv_i L_{i,i-1}: B[e][c] = L[i0 + e][i0 - 64 + c]
+  if (i > 0) {
+    for (int e = tid; e < NB * NB; e += kPrepThreads) {
+      const int r = e >> 6, c = e & 63;
+      B[r][c] = (r < nb) ? L[(i0 + r) * n + i0 - NB + c] : 0.0;
+    }
+    __syncthreads();
+    for (int e = tid; e < NB * NB; e += kPrepThreads) {
+      const int a = e >> 6, c = e & 63;
+      double s = 0.0;
+      for (int k = 0; k < NB; ++k) s = __fma_rn(X[a][k], B[k][c], s);
+      M[(int64_t)i * NB * NB + e] = s;
+    }
+    __syncthreads();
+  }
+  // N_i = Linv_i^T L_{i+1,i}^T: B[e'][a] = L[i0 + 64 + e'][i0 + a];  N[c][e'] = sum_a X[a][c] B[e'][a]
+  if (i + 1 < nblk) {
+    const int nb1 = (int)(n - i0 - NB < NB ? n - i0 - NB : NB);
+    for (int e = tid; e < NB * NB; e += kPrepThreads) {
+      const int r = e >> 6, a = e & 63;
+      B[r][a] = (r < nb1) ? L[(i0 + NB + r) * n + i0 + a] : 0.0;
+    }
+    __syncthreads();
+    for (int e = tid; e < NB * NB; e += kPrepThreads) {
+      const int c = e >> 6, r = e & 63;
+      double s = 0.0;
+      for (int a = 0; a < NB; ++a) s = __fma_rn(X[a][c], B[r][a], s);
+      N[(int64_t)i * NB * NB + e] = s;
+    }
+  }
 }
 
 RCP_D double2 ld_pair(const double* p, bool aligned) {
@@ -69,52 +118,104 @@ RCP_D double warp_sum(double v) {
   return v;
 }
 
+// The block on the serial chain is also published as "LL" words (32 data bits + a 32-bit tag per
+// 64-bit store, single-copy atomic): the next block polls the data itself, one L2 round trip instead
+// of flag-then-data, and the producer needs no release fence for it.  tag = a per-call epoch.
+typedef unsigned long long u64;
+RCP_D void ll_put2(u64* p, unsigned tag, double x) {
+  const u64 b = static_cast<u64>(__double_as_longlong(x));
+  const u64 w0 = (static_cast<u64>(tag) << 32) | (b & 0xffffffffull), w1 = (static_cast<u64>(tag) << 32) | (b >> 32);
+  asm volatile("st.relaxed.gpu.global.v2.b64 [%0], {%1, %2};" ::"l"(p), "l"(w0), "l"(w1) : "memory");
+}
+// Read N consecutive LL doubles (2 words each) once every word carries `tag`.
+template <int N>
+RCP_D void ll_get_n(const u64* p, unsigned tag, double (&out)[N]) {
+  for (;;) {
+    bool ok = true;
+#pragma unroll
+    for (int e = 0; e < N; ++e) {
+      u64 w0, w1;
+      asm volatile("ld.relaxed.gpu.global.v2.b64 {%0, %1}, [%2];" : "=l"(w0), "=l"(w1) : "l"(p + 2 * e) : "memory");
+      ok &= (static_cast<unsigned>(w0 >> 32) == tag) & (static_cast<unsigned>(w1 >> 32) == tag);
+      out[e] = __longlong_as_double(static_cast<long long>((w1 << 32) | (w0 & 0xffffffffull)));
+    }
+    if (ok) return;
+  }
+}
+
 // Forward sweep L z = P b (R right-hand sides; z column-major with ld ldz).  Block i:
-// acc = y_i - sum_{j<i} L_ij z_j, z_i = Linv_ii acc.  The gather y = b[perm] is fused.
-// Per warp: 8 rows of the block, lanes over 2 columns of each 64-wide strip block.  The L
-// strip of block j is loaded BEFORE waiting for z_j's flag (L is read-only), so the wait for
-// the last, just-published block overlaps its HBM latency; Linv_ii is staged in shared memory
-// while the strip streams.
+//   pre = Linv_i (y_i - sum_{j<i-1} L_ij z_j)   (streamed as earlier blocks are published)
+//   z_i = pre - M_i z_{i-1}                     (the one product on the serial chain)
+// Warps take 8 rows of the block each, lanes 2 columns of each 64-wide strip block; the L strip of
+// block j is loaded before waiting for z_j.  The gather y = b[perm] is fused.
 template <int R>
 __global__ void __launch_bounds__(kSweepThreads) fwd_sweep_kernel(int64_t n, int64_t ldz, int nblk,
                                                                   const int64_t* __restrict__ perm,
                                                                   const double* __restrict__ L,
                                                                   const double* __restrict__ Linv,
+                                                                  const double* __restrict__ M,
                                                                   const double* __restrict__ b, double* __restrict__ z,
-                                                                  int* flags, int* ticket) {
+                                                                  u64* __restrict__ zll, unsigned tag, int* flags,
+                                                                  int* ticket) {
+  constexpr int kU = (R == 1) ? 4 : 2;  // see strip_unroll
   __shared__ int s_blk;
   __shared__ double s_acc[R][NB];
-  __shared__ double s_inv[NB][NB + 1];
+  __shared__ double s_cpl[NB][NB + 1];  // M_i, staged while the strip streams
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const bool al = (n & 1) == 0;  // rows of L are 16-byte aligned
+  const int a = threadIdx.x / kMvLanes, qtr = threadIdx.x % kMvLanes;  // matrix-vector: row a, kMvCols columns
+  const bool al = (n & 1) == 0;
   for (;;) {
     if (threadIdx.x == 0) s_blk = atomicAdd(ticket, 1);
     __syncthreads();
     const int i = s_blk;
     if (i >= nblk) return;
     const int64_t r0 = (int64_t)i * NB;
-    for (int e = threadIdx.x; e < NB * NB; e += kSweepThreads) s_inv[e >> 6][e & 63] = Linv[(int64_t)i * NB * NB + e];
-    double part[8][R];
+    if (i > 0)  // M_i, needed after the wait (staged now, off the chain)
+      for (int e = threadIdx.x; e < NB * NB; e += kSweepThreads) s_cpl[e >> 6][e & 63] = __ldg(M + (int64_t)i * NB * NB + e);
+    double part[kRPW][R];
 #pragma unroll
-    for (int q = 0; q < 8; ++q)
+    for (int q = 0; q < kRPW; ++q)
 #pragma unroll
       for (int c = 0; c < R; ++c) part[q][c] = 0.0;
-    int ready = 0;  // blocks j < ready are known to be published (lane 0 polls, the warp shares it)
-    for (int j = 0; j < i; ++j) {
-      const int64_t c0 = (int64_t)j * NB + 2 * lane;  // j < i: a full block
-      double2 lv[8];
+    int ready = 0;  // blocks j < ready are known to be published
+    for (int j = 0; j + 1 < i;) {
+      if (j + kU <= i - 1 && j + kU <= ready) {  // kU published blocks: all their loads in flight at once
+        double2 lv[kU][kRPW], zv[kU][R];
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const int64_t r = r0 + warp * 8 + q;
+        for (int u = 0; u < kU; ++u) {
+          const int64_t c0 = (int64_t)(j + u) * NB + 2 * lane;
+#pragma unroll
+          for (int q = 0; q < kRPW; ++q) {
+            const int64_t r = r0 + warp * kRPW + q;
+            lv[u][q] = (r < n) ? ld_pair(L + r * n + c0, al) : make_double2(0.0, 0.0);
+          }
+#pragma unroll
+          for (int c = 0; c < R; ++c) zv[u][c] = __ldcg(reinterpret_cast<const double2*>(z + c * ldz + c0));
+        }
+#pragma unroll
+        for (int u = 0; u < kU; ++u)
+#pragma unroll
+          for (int q = 0; q < kRPW; ++q)
+#pragma unroll
+            for (int c = 0; c < R; ++c)
+              part[q][c] = __fma_rn(lv[u][q].y, zv[u][c].y, __fma_rn(lv[u][q].x, zv[u][c].x, part[q][c]));
+        j += kU;
+        continue;
+      }
+      const int64_t c0 = (int64_t)j * NB + 2 * lane;
+      double2 lv[kRPW];
+#pragma unroll
+      for (int q = 0; q < kRPW; ++q) {
+        const int64_t r = r0 + warp * kRPW + q;
         lv[q] = (r < n) ? ld_pair(L + r * n + c0, al) : make_double2(0.0, 0.0);
       }
       if (j >= ready) {
         if (lane == 0) {
           while (ld_acquire_i(flags + j) == 0) {
           }
-          int r = j + 1;
-          while (r < i && ld_acquire_i(flags + r) != 0) ++r;
-          ready = r;
+          int rr = j + 1;
+          while (rr + 1 < i && ld_acquire_i(flags + rr) != 0) ++rr;
+          ready = rr;
         }
         ready = __shfl_sync(0xffffffffu, ready, 0);
         __syncwarp();
@@ -123,38 +224,52 @@ __global__ void __launch_bounds__(kSweepThreads) fwd_sweep_kernel(int64_t n, int
 #pragma unroll
       for (int c = 0; c < R; ++c) zv[c] = __ldcg(reinterpret_cast<const double2*>(z + c * ldz + c0));
 #pragma unroll
-      for (int q = 0; q < 8; ++q)
+      for (int q = 0; q < kRPW; ++q)
 #pragma unroll
         for (int c = 0; c < R; ++c) part[q][c] = __fma_rn(lv[q].y, zv[c].y, __fma_rn(lv[q].x, zv[c].x, part[q][c]));
+      ++j;
     }
-    // acc = y - sum (fixed shuffle tree), then z_i = Linv_ii acc
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const int a = warp * 8 + q;
-      const int64_t r = r0 + a;
+    for (int q = 0; q < kRPW; ++q) {
+      const int ar = warp * kRPW + q;
+      const int64_t r = r0 + ar;
 #pragma unroll
       for (int c = 0; c < R; ++c) {
-        const double s = warp_sum(part[q][c]);
-        if (lane == 0) s_acc[c][a] = (r < n) ? __dsub_rn(b[c * n + perm[r]], s) : 0.0;
+        const double sm = warp_sum(part[q][c]);
+        if (lane == 0) s_acc[c][ar] = (r < n) ? __dsub_rn(b[c * n + perm[r]], sm) : 0.0;
       }
     }
     __syncthreads();
+    double d[R];
     {
-      const int a = threadIdx.x >> 2, qtr = threadIdx.x & 3;  // 4 lanes per output row
-      double d[R];
+      const double* li = Linv + (int64_t)i * NB * NB + a * NB + qtr * kMvCols;
 #pragma unroll
       for (int c = 0; c < R; ++c) d[c] = 0.0;
 #pragma unroll
-      for (int e = 0; e < 16; ++e) {
-        const double lv = s_inv[a][qtr * 16 + e];
+      for (int e = 0; e < kMvCols; ++e) {
+        const double lv = __ldg(li + e);
 #pragma unroll
-        for (int c = 0; c < R; ++c) d[c] = __fma_rn(lv, s_acc[c][qtr * 16 + e], d[c]);
+        for (int c = 0; c < R; ++c) d[c] = __fma_rn(lv, s_acc[c][qtr * kMvCols + e], d[c]);
       }
+    }
+    if (i > 0) {  // the serial step: z_{i-1} straight from its LL words, subtract M_i z_{i-1}
 #pragma unroll
       for (int c = 0; c < R; ++c) {
-        d[c] = __dadd_rn(d[c], __shfl_xor_sync(0xffffffffu, d[c], 1));
-        d[c] = __dadd_rn(d[c], __shfl_xor_sync(0xffffffffu, d[c], 2));
-        if (qtr == 0 && r0 + a < n) z[c * ldz + r0 + a] = d[c];
+        double zz[kMvCols];
+        ll_get_n<kMvCols>(zll + (((int64_t)(i - 1) * R + c) * NB + qtr * kMvCols) * 2, tag, zz);
+        double m = 0.0;
+#pragma unroll
+        for (int e = 0; e < kMvCols; ++e) m = __fma_rn(s_cpl[a][qtr * kMvCols + e], zz[e], m);
+        d[c] = __dsub_rn(d[c], m);
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < R; ++c) {
+#pragma unroll
+      for (int off = 1; off < kMvLanes; off <<= 1) d[c] = __dadd_rn(d[c], __shfl_xor_sync(0xffffffffu, d[c], off));
+      if (qtr == 0) {
+        ll_put2(zll + (((int64_t)i * R + c) * NB + a) * 2, tag, d[c]);
+        if (r0 + a < n) z[c * ldz + r0 + a] = d[c];
       }
     }
     __syncthreads();  // every z_i store precedes the release (cumulativity through the barrier)
@@ -162,20 +277,24 @@ __global__ void __launch_bounds__(kSweepThreads) fwd_sweep_kernel(int64_t n, int
   }
 }
 
-// Backward sweep L^T v = w (w = D^-1 z; v is a separate buffer).  Column block i:
-// acc = w_i - sum_{j>i} L_ji^T v_j, v_i = Linv_ii^T acc; the scatter x[perm] = v is fused.
+// Backward sweep L^T v = w (w = D^-1 z; v a separate buffer).  Column block i (descending):
+//   pre = Linv_i^T (w_i - sum_{j>i+1} L_ji^T v_j),  v_i = pre - N_i v_{i+1};  x[perm] = v fused.
 template <int R>
 __global__ void __launch_bounds__(kSweepThreads) bwd_sweep_kernel(int64_t n, int64_t ldz, int nblk,
                                                                   const int64_t* __restrict__ perm,
                                                                   const double* __restrict__ L,
                                                                   const double* __restrict__ Linv,
+                                                                  const double* __restrict__ Nc,
                                                                   const double* __restrict__ w, double* __restrict__ v,
-                                                                  double* __restrict__ x, int* flags, int* ticket) {
+                                                                  double* __restrict__ x, u64* __restrict__ vll, unsigned tag,
+                                                                  int* flags, int* ticket) {
+  constexpr int kU = (R == 1) ? 4 : 2;  // see strip_unroll
   __shared__ int s_blk;
-  __shared__ double s_part[8][R][NB];
+  __shared__ double s_part[kWarps][R][NB];
   __shared__ double s_acc[R][NB];
-  __shared__ double s_inv[NB][NB + 1];
+  __shared__ double s_cpl[NB][NB + 1];  // N_i, staged while the strip streams
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int col = threadIdx.x / kMvLanes, qtr = threadIdx.x % kMvLanes;  // output column col, kMvCols rows
   const bool al = (n & 1) == 0;
   for (;;) {
     if (threadIdx.x == 0) s_blk = nblk - 1 - atomicAdd(ticket, 1);
@@ -184,18 +303,53 @@ __global__ void __launch_bounds__(kSweepThreads) bwd_sweep_kernel(int64_t n, int
     if (i < 0) return;
     const int64_t c0 = (int64_t)i * NB;
     const int ncol = (int)(n - c0 < NB ? n - c0 : NB);
-    for (int e = threadIdx.x; e < NB * NB; e += kSweepThreads) s_inv[e >> 6][e & 63] = Linv[(int64_t)i * NB * NB + e];
+    if (i + 1 < nblk)
+      for (int e = threadIdx.x; e < NB * NB; e += kSweepThreads) s_cpl[e >> 6][e & 63] = __ldg(Nc + (int64_t)i * NB * NB + e);
     double part[2][R];
 #pragma unroll
     for (int e = 0; e < 2; ++e)
 #pragma unroll
       for (int c = 0; c < R; ++c) part[e][c] = 0.0;
     int ready = nblk;  // blocks j >= ready are known to be published
-    for (int j = nblk - 1; j > i; --j) {
-      const int64_t rb = (int64_t)j * NB + warp * 8;
-      double2 lv[8];
+    for (int j = nblk - 1; j > i + 1;) {
+      if (j - kU + 1 > i + 1 && j - kU + 1 >= ready) {  // blocks j-kU+1..j published: loads in flight together
+        double2 lv[kU][kRPW];
+        double vr[kU][kRPW][R];
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
+        for (int u = 0; u < kU; ++u) {
+          const int64_t rb = (int64_t)(j - u) * NB + warp * kRPW;
+#pragma unroll
+          for (int q = 0; q < kRPW; ++q) {
+            const int64_t r = rb + q;
+            const double* lp = L + r * n + c0 + 2 * lane;
+            lv[u][q] = make_double2(0.0, 0.0);
+            if (r < n) {
+              if (2 * lane + 1 < ncol) {
+                lv[u][q] = ld_pair(lp, al);
+              } else if (2 * lane < ncol) {
+                lv[u][q].x = __ldcs(lp);
+              }
+            }
+#pragma unroll
+            for (int c = 0; c < R; ++c) vr[u][q][c] = (r < n) ? __ldcg(v + c * ldz + r) : 0.0;
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < kU; ++u)
+#pragma unroll
+          for (int q = 0; q < kRPW; ++q)
+#pragma unroll
+            for (int c = 0; c < R; ++c) {
+              part[0][c] = __fma_rn(lv[u][q].x, vr[u][q][c], part[0][c]);
+              part[1][c] = __fma_rn(lv[u][q].y, vr[u][q][c], part[1][c]);
+            }
+        j -= kU;
+        continue;
+      }
+      const int64_t rb = (int64_t)j * NB + warp * kRPW;
+      double2 lv[kRPW];
+#pragma unroll
+      for (int q = 0; q < kRPW; ++q) {
         const int64_t r = rb + q;
         const double* lp = L + r * n + c0 + 2 * lane;
         lv[q] = make_double2(0.0, 0.0);
@@ -211,15 +365,15 @@ __global__ void __launch_bounds__(kSweepThreads) bwd_sweep_kernel(int64_t n, int
         if (lane == 0) {
           while (ld_acquire_i(flags + j) == 0) {
           }
-          int r = j;
-          while (r - 1 > i && ld_acquire_i(flags + r - 1) != 0) --r;
-          ready = r;
+          int rr = j;
+          while (rr - 1 > i + 1 && ld_acquire_i(flags + rr - 1) != 0) --rr;
+          ready = rr;
         }
         ready = __shfl_sync(0xffffffffu, ready, 0);
         __syncwarp();
       }
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
+      for (int q = 0; q < kRPW; ++q) {
         const int64_t r = rb + q;
         if (r < n) {
 #pragma unroll
@@ -230,6 +384,7 @@ __global__ void __launch_bounds__(kSweepThreads) bwd_sweep_kernel(int64_t n, int
           }
         }
       }
+      --j;
     }
 #pragma unroll
     for (int c = 0; c < R; ++c) {
@@ -237,32 +392,45 @@ __global__ void __launch_bounds__(kSweepThreads) bwd_sweep_kernel(int64_t n, int
       s_part[warp][c][2 * lane + 1] = part[1][c];
     }
     __syncthreads();
-    if (threadIdx.x < NB * R) {
-      const int col = threadIdx.x % NB, c = threadIdx.x / NB;
-      double s = 0.0;
+    for (int f = threadIdx.x; f < NB * R; f += kSweepThreads) {
+      const int cc = f % NB, c = f / NB;
+      double sm = 0.0;
 #pragma unroll
-      for (int ww = 0; ww < 8; ++ww) s = __dadd_rn(s, s_part[ww][c][col]);
-      s_acc[c][col] = (col < ncol) ? __dsub_rn(w[c * ldz + c0 + col], s) : 0.0;
+      for (int ww = 0; ww < kWarps; ++ww) sm = __dadd_rn(sm, s_part[ww][c][cc]);
+      s_acc[c][cc] = (cc < ncol) ? __dsub_rn(w[c * ldz + c0 + cc], sm) : 0.0;
     }
     __syncthreads();
+    double d[R];
     {
-      // v_i[col] = sum_a Linv[a][col] acc[a]: 4 lanes per output column, 16 rows each
-      const int col = threadIdx.x >> 2, qtr = threadIdx.x & 3;
-      double d[R];
+      const double* li = Linv + (int64_t)i * NB * NB + col;
 #pragma unroll
       for (int c = 0; c < R; ++c) d[c] = 0.0;
 #pragma unroll
-      for (int e = 0; e < 16; ++e) {
-        const int a = qtr * 16 + e;
-        const double lv = s_inv[a][col];
+      for (int e = 0; e < kMvCols; ++e) {
+        const int ar = qtr * kMvCols + e;
+        const double lv = __ldg(li + ar * NB);
 #pragma unroll
-        for (int c = 0; c < R; ++c) d[c] = __fma_rn(lv, s_acc[c][a], d[c]);
+        for (int c = 0; c < R; ++c) d[c] = __fma_rn(lv, s_acc[c][ar], d[c]);
       }
+    }
+    if (i + 1 < nblk) {  // the serial step: v_{i+1} straight from its LL words, subtract N_i v_{i+1}
 #pragma unroll
       for (int c = 0; c < R; ++c) {
-        d[c] = __dadd_rn(d[c], __shfl_xor_sync(0xffffffffu, d[c], 1));
-        d[c] = __dadd_rn(d[c], __shfl_xor_sync(0xffffffffu, d[c], 2));
-        if (qtr == 0 && col < ncol) {
+        double vv[kMvCols];
+        ll_get_n<kMvCols>(vll + (((int64_t)(i + 1) * R + c) * NB + qtr * kMvCols) * 2, tag, vv);
+        double m = 0.0;
+#pragma unroll
+        for (int e = 0; e < kMvCols; ++e) m = __fma_rn(s_cpl[col][qtr * kMvCols + e], vv[e], m);
+        d[c] = __dsub_rn(d[c], m);
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < R; ++c) {
+#pragma unroll
+      for (int off = 1; off < kMvLanes; off <<= 1) d[c] = __dadd_rn(d[c], __shfl_xor_sync(0xffffffffu, d[c], off));
+      if (qtr == 0) {
+        ll_put2(vll + (((int64_t)i * R + c) * NB + col) * 2, tag, col < ncol ? d[c] : 0.0);
+        if (col < ncol) {
           v[c * ldz + c0 + col] = d[c];
           x[c * n + perm[c0 + col]] = d[c];
         }
@@ -345,22 +513,26 @@ struct ReconEpi {
 
 }  // namespace
 
-// workspace: Linv (nblk x 64 x 64) | z (n x nrhs) | v (n x nrhs) | 2 x nblk flags + 2 tickets
+// workspace: Linv, M, N (nblk x 64 x 64 each) | z, v (ldz x nrhs) | z, v LL words (nblk x 3 x 64 x 2) |
+//            2 x nblk flags + 2 tickets
 static size_t rup(size_t x) { return (x + 255) / 256 * 256; }
 size_t solve_workspace_bytes(int64_t n, int64_t nrhs) {
   const size_t nblk = (size_t)((n + NB - 1) / NB);
-  return rup(nblk * NB * NB * 8) + 2 * rup(nblk * NB * (size_t)nrhs * 8) + rup((2 * nblk + 2) * 4);
+  return 3 * rup(nblk * NB * NB * 8) + 2 * rup(nblk * NB * (size_t)nrhs * 8) + 2 * rup(nblk * 3 * NB * 16) +
+         rup((2 * nblk + 2) * 4);
 }
 
 template <int R>
 static void launch_sweeps(int64_t n, int nblk, const int64_t* perm, const double* L, const double* Linv,
-                          const double* dd, const double* doff, const int8_t* pattern, const double* b, double* x,
-                          double* z, double* v, int* flags, int* singular, int grid_f, int grid_b, cudaStream_t st) {
+                          const double* M, const double* N, const double* dd, const double* doff,
+                          const int8_t* pattern, const double* b, double* x, double* z, double* v, u64* zll,
+                          u64* vll, unsigned tag, int* flags, int* singular, int grid, cudaStream_t st) {
   const int64_t ldz = (int64_t)nblk * NB;
-  fwd_sweep_kernel<R><<<grid_f, kSweepThreads, 0, st>>>(n, ldz, nblk, perm, L, Linv, b, z, flags, flags + 2 * nblk);
+  fwd_sweep_kernel<R><<<grid, kSweepThreads, 0, st>>>(n, ldz, nblk, perm, L, Linv, M, b, z, zll, tag, flags,
+                                                      flags + 2 * nblk);
   block_diag_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(n, ldz, R, dd, doff, pattern, z, singular);
-  bwd_sweep_kernel<R><<<grid_b, kSweepThreads, 0, st>>>(n, ldz, nblk, perm, L, Linv, z, v, x, flags + nblk,
-                                                         flags + 2 * nblk + 1);
+  bwd_sweep_kernel<R><<<grid, kSweepThreads, 0, st>>>(n, ldz, nblk, perm, L, Linv, N, z, v, x, vll, tag,
+                                                      flags + nblk, flags + 2 * nblk + 1);
 }
 
 cudaError_t solve_device(int64_t n, const int64_t* perm, const double* L, const double* dd, const double* doff,
@@ -368,18 +540,34 @@ cudaError_t solve_device(int64_t n, const int64_t* perm, const double* L, const 
                          cudaStream_t st, int num_sms) {
   const int nblk = (int)((n + NB - 1) / NB);
   unsigned char* p = reinterpret_cast<unsigned char*>(ws);
+  const size_t blk_bytes = rup((size_t)nblk * NB * NB * 8);
   double* Linv = reinterpret_cast<double*>(p);
-  p += rup((size_t)nblk * NB * NB * 8);
+  double* M = reinterpret_cast<double*>(p + blk_bytes);
+  double* N = reinterpret_cast<double*>(p + 2 * blk_bytes);
+  p += 3 * blk_bytes;
   double* z = reinterpret_cast<double*>(p);
   const int64_t ldz = (int64_t)nblk * NB;
   p += rup((size_t)ldz * (size_t)nrhs * 8);
   double* v = reinterpret_cast<double*>(p);
   p += rup((size_t)ldz * (size_t)nrhs * 8);
+  u64* zll = reinterpret_cast<u64*>(p);
+  p += rup((size_t)nblk * 3 * NB * 16);
+  u64* vll = reinterpret_cast<u64*>(p);
+  p += rup((size_t)nblk * 3 * NB * 16);
   int* flags = reinterpret_cast<int*>(p);
-  diag_inverse_kernel<<<nblk, NB, 0, st>>>(n, L, Linv);
+  const size_t prep_smem = sizeof(double) * (NB * NB + NB * (NB + 1));
+  static thread_local int prep_dev = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev != prep_dev) {
+    cudaError_t e = cudaFuncSetAttribute(block_prep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)prep_smem);
+    if (e != cudaSuccess) return e;
+    prep_dev = dev;
+  }
+  block_prep_kernel<<<nblk, kPrepThreads, prep_smem, st>>>(n, nblk, L, Linv, M, N);
   // x may alias b: the forward sweep reads b (gather) before the backward sweep writes x
   const int grid = std::max(1, std::min(nblk, 2 * num_sms));
-  for (int64_t c0 = 0; c0 < nrhs; c0 += 3) {  // up to 3 right-hand sides per pair of sweeps (smem)
+  for (int64_t c0 = 0; c0 < nrhs; c0 += 3) {  // up to 3 right-hand sides per pair of sweeps
     const int64_t r = std::min<int64_t>(3, nrhs - c0);
     cudaError_t e = cudaMemsetAsync(flags, 0, (size_t)(2 * nblk + 2) * 4, st);
     if (e != cudaSuccess) return e;
@@ -387,12 +575,19 @@ cudaError_t solve_device(int64_t n, const int64_t* perm, const double* L, const 
     double* xc = x + c0 * n;
     double* zc = z + c0 * ldz;
     double* vc = v + c0 * ldz;
+    // LL tag: a fresh epoch per pair of sweeps (the LL buffers are never cleared; a stale word from
+    // an earlier call carries an older tag)
+    static std::atomic<unsigned> epoch{0};
+    const unsigned tag = epoch.fetch_add(1) + 1;
     if (r == 3)
-      launch_sweeps<3>(n, nblk, perm, L, Linv, dd, doff, pattern, bc, xc, zc, vc, flags, singular, grid, grid, st);
+      launch_sweeps<3>(n, nblk, perm, L, Linv, M, N, dd, doff, pattern, bc, xc, zc, vc, zll, vll, tag, flags, singular,
+                       grid, st);
     else if (r == 2)
-      launch_sweeps<2>(n, nblk, perm, L, Linv, dd, doff, pattern, bc, xc, zc, vc, flags, singular, grid, grid, st);
+      launch_sweeps<2>(n, nblk, perm, L, Linv, M, N, dd, doff, pattern, bc, xc, zc, vc, zll, vll, tag, flags, singular,
+                       grid, st);
     else
-      launch_sweeps<1>(n, nblk, perm, L, Linv, dd, doff, pattern, bc, xc, zc, vc, flags, singular, grid, grid, st);
+      launch_sweeps<1>(n, nblk, perm, L, Linv, M, N, dd, doff, pattern, bc, xc, zc, vc, zll, vll, tag, flags, singular,
+                       grid, st);
   }
   return cudaGetLastError();
 }
