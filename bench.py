@@ -125,6 +125,8 @@ def make_matrix(args):
 
 
 def metric_name(args):
+    if args.workload == "c5":
+        return "RCP LDL^T fp64 GFLOP/s (n³/3 per matrix) over 65536 batched n=256 matrices (C5), % of FP64 peak"
     return METRIC if args.workload == "c3" else (
         f"RCP LDL^T fp64 GFLOP/s (n³/3) at n={args.n} ({args.workload.upper()}), % of FP64 peak")
 
@@ -524,28 +526,37 @@ def c5_host_member(i: int, seed: int) -> np.ndarray:
     return gallery.scaled_member(C5_N, seed + i, scaled=(i % 10 == 0))
 
 
-def c5_cpu_sample(args, budget_s: float, max_count: int | None = None):
+def c5_factor_fn(seed: int):
+    """CPU factor() of one C5 member: the unmodified reference (oracle/_ref/randldl) when shipped,
+    else the oracle port.  Returns (callable, kind)."""
+    randldl = load_reference()
+    if randldl is not None:
+        cfg = randldl.FactorConfig(strategy="rcp", b=C5_B, q=C5_B, p=C5_P, seed=seed)
+        return (lambda a: randldl.factor(a, cfg)), "reference"
     from oracle.rcp_oracle import OracleConfig, oracle_factor
-    cfg = OracleConfig(p=C5_P, b=C5_B, q=C5_B, seed=args.seed)
-    mats = []
+    ocfg = OracleConfig(p=C5_P, b=C5_B, q=C5_B, seed=seed)
+    return (lambda a: oracle_factor(a, ocfg)), "port"
+
+
+def c5_cpu_sample(args, budget_s: float, max_count: int | None = None):
+    fn, kind = c5_factor_fn(args.seed)
     t_total, done = 0.0, 0
     while True:
         a = c5_host_member(done, args.seed)
         t0 = time.perf_counter()
-        oracle_factor(a, cfg)
+        fn(a)
         t_total += time.perf_counter() - t0
         done += 1
         if (max_count is not None and done >= max_count) or (max_count is None and t_total >= budget_s):
             break
-    return done, t_total
+    return done, t_total, kind
 
 
 def _c5_worker(job):
     seed, idx = job
-    from oracle.rcp_oracle import OracleConfig, oracle_factor
-    cfg = OracleConfig(p=C5_P, b=C5_B, q=C5_B, seed=seed)
+    fn, _ = c5_factor_fn(seed)
     for i in idx:
-        oracle_factor(c5_host_member(i, seed), cfg)
+        fn(c5_host_member(i, seed))
     return len(idx)
 
 
@@ -571,14 +582,16 @@ def run_reference_c5(args, rank: int):
     cnt = sum(c for c, _ in steps)
     tsum = sum(t for _, t in steps)
     value = cnt * C5_N ** 3 / 3.0 / tsum / 1e9
+    kind = c5_factor_fn(args.seed)[1]
     line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": args.gpus,
+        "impl": "reference", "metric": metric_name(args), "value": value, "unit": "GFLOP/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tsum / len(steps),
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded numpy Philox C5 members)", "config": c5_cfg(args, args.gpus),
-        "cpu_baseline": {"value": value, "unit": "GFLOP/s", "cores": cores, "kind": "port",
-                         "sample": f"oracle port factor() on {cores * per_core} C5 members per step, {cores} "
-                                   f"processes x 1 BLAS thread"},
+        "cpu_baseline": {"value": value, "unit": "GFLOP/s", "cores": cores, "kind": kind,
+                         "sample": f"{'reference randldl (oracle/_ref)' if kind == 'reference' else 'oracle port'} "
+                                   f"factor() on {cores * per_core} C5 members per step, {cores} processes x 1 BLAS "
+                                   f"thread; CPU {cpu_model()}"},
         "e2e": {"value": value, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -672,13 +685,14 @@ def run_b200_c5(args, rank: int, world: int, local_rank: int):
         return
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
-        cnt, tc = c5_cpu_sample(args, budget_s=args.cpu_seconds)
+        cnt, tc, kind = c5_cpu_sample(args, budget_s=args.cpu_seconds)
         cv = cnt * C5_N ** 3 / 3.0 / tc / 1e9
-        cpu = {"value": cv, "unit": "GFLOP/s", "cores": 1, "kind": "port",
-               "sample": f"oracle port factor() on {cnt} C5 members (numpy/OpenBLAS, one process), {tc:.1f} s"}
+        cpu = {"value": cv, "unit": "GFLOP/s", "cores": 1, "kind": kind,
+               "sample": f"{'reference randldl (oracle/_ref)' if kind == 'reference' else 'oracle port'} factor() on "
+                         f"{cnt} C5 members (numpy/OpenBLAS, one process), {tc:.1f} s; CPU {cpu_model()}"}
     hbm_bytes = args.count * C5_N * C5_N * 8 * 2  # read A, write L (algorithmic)
     line = {
-        "metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
+        "metric": metric_name(args), "value": value, "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
         "warmup": max(3, args.warmup), "ms_per_step": ms_max, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded torch generator on the device)",
         "config": c5_cfg(args, world),
