@@ -423,7 +423,7 @@ def run_b200(args, rank: int, world: int, local_rank: int):
         solve = {"ms": solve_ms, "nrhs": 1, "algorithmic_bytes": sbytes,
                  "hbm_achieved_gbs": sbytes / (solve_ms / 1e3) / 1e9, "hbm_peak_gbs": hbm, "peak_source": hbm_src,
                  "hbm_frac": sbytes / (solve_ms / 1e3) / 1e9 / hbm, "backward_error": bwd,
-                 "kernels": "diag_inverse_kernel + fwd_sweep_kernel + block_diag_kernel + bwd_sweep_kernel"}
+                 "kernels": "block_prep_kernel + fwd_sweep_kernel + block_diag_kernel + bwd_sweep_kernel"}
 
     # end to end through the public API: numpy in (pinned) -> Factorization out
     # A (single GPU: the 256-row block rows of its lower trapezoid, rcp_factor_host) + Omega;
