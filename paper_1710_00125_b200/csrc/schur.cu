@@ -3,6 +3,8 @@
 #include "gemm_dmma.cuh"
 #include "misc.cuh"
 #include "schur_ws.cuh"
+#include "schur_ws2.cuh"
+#include <cstdlib>
 #include <algorithm>
 #include <type_traits>
 
@@ -58,6 +60,31 @@ struct SketchCorrEpi {
 
 constexpr int kRectStages = 3;
 
+// Single-GPU trailing update kernel: 2 = schur_ws2_kernel (two MMA warps per sub-partition,
+// default), 1 = schur_ws_kernel.  RCP_SCHUR_V=1 selects the first generation (A/B runs).
+int schur_version() {
+  static const int v = [] {
+    const char* e = std::getenv("RCP_SCHUR_V");
+    return (e && e[0] == '1') ? 1 : 2;
+  }();
+  return v;
+}
+
+// L2 cache-policy hints in schur_ws2_kernel: RCP_SCHUR_HINTS = 0 none, 1 (default) operand panels
+// evict_last, 2 also C-in / C-out evict_first.
+int schur_hints() {
+  static const int v = [] {
+    const char* e = std::getenv("RCP_SCHUR_HINTS");
+    return (e && e[0] >= '0' && e[0] <= '2') ? e[0] - '0' : 1;
+  }();
+  return v;
+}
+using Ws2Kernel = decltype(&schur_ws2_kernel<0>);
+Ws2Kernel ws2_kernel() {
+  const int h = schur_hints();
+  return h == 2 ? schur_ws2_kernel<2> : (h == 1 ? schur_ws2_kernel<1> : schur_ws2_kernel<0>);
+}
+
 bool aligned16(const void* p, int64_t ld) {
   return (reinterpret_cast<uintptr_t>(p) % 16 == 0) && (ld % 2 == 0);
 }
@@ -71,6 +98,15 @@ cudaError_t gemm_init_attributes() {
   if (e != cudaSuccess) return e;
   e = cudaFuncSetAttribute(schur_ws_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)schur_ws_smem_bytes());
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(schur_ws2_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)schur_ws2_smem_bytes());
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(schur_ws2_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)schur_ws2_smem_bytes());
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(schur_ws2_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)schur_ws2_smem_bytes());
   if (e != cudaSuccess) return e;
   e = cudaFuncSetAttribute(dmma_gemm_kernel<64, 128, kRectStages, 2, RectMap, SketchEpi>,
                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gemm_smem_bytes<64, 128, kRectStages>());
@@ -104,12 +140,28 @@ cudaError_t launch_schur_update(int64_t n, int64_t k, int64_t mp, const double* 
       schur_ws_kernel<true><<<(unsigned)sms, ws::kThreads, schur_ws_smem_bytes(), st>>>(
           Lneg, Wg, tpad, 0, A_in, A_out, phys, n, 0, 0, 0, d, part, nparts, nullptr, nullptr, nullptr, nullptr, 0,
           tstamp);
+    else if (schur_version() == 2)
+      ws2_kernel()
+          <<<(unsigned)sms, ws2::kThreads, schur_ws2_smem_bytes(), st>>>(Lneg, Wg, tpad, 0, A_in, A_out, phys, n, 0, 0,
+                                                                          d, ysk, bin, bout, P, tstamp);
     else
       schur_ws_kernel<false><<<(unsigned)sms, ws::kThreads, schur_ws_smem_bytes(), st>>>(
           Lneg, Wg, tpad, 0, A_in, A_out, phys, n, 0, 0, 0, d, part, nparts, nullptr, ysk, bin, bout, P, tstamp);
     return cudaGetLastError();
   }
   if (mp <= 0 || K <= 0) return cudaSuccess;
+  if (schur_version() == 2) {
+    const int64_t nb2 = (mp + ws::BM - 1) / ws::BM;
+    const long long supers = nb2 * (nb2 + 1) / 2;
+    const int Kl2 = ((K + kBK - 1) / kBK) * kBK;
+    int dev2 = 0, sms2 = 148;
+    cudaGetDevice(&dev2);
+    cudaDeviceGetAttribute(&sms2, cudaDevAttrMultiProcessorCount, dev2);
+    ws2_kernel()
+        <<<(unsigned)std::min<long long>(supers, sms2), ws2::kThreads, schur_ws2_smem_bytes(), st>>>(
+            Lneg, Wg, tpad, Kl2, A_in, A_out, phys, n, k, mp, nullptr, nullptr, nullptr, nullptr, 0, nullptr);
+    return cudaGetLastError();
+  }
   const int64_t nbi = (mp + ws::BM - 1) / ws::BM;
   const long long tiles = nbi * (nbi + 1);  // row block I has 2I+2 column blocks of 64
   const int Kl = ((K + kBK - 1) / kBK) * kBK;  // operands are zero padded to tpad along K

@@ -1,0 +1,8 @@
+cd $GRAFT_REPO_ROOT
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests/test_gpu_parity.py -x -q -m gpu 2>&1 | tail -5
+for v in 1 2; do
+  echo "RCP_SCHUR_V=$v"
+  RCP_SCHUR_V=$v timeout 300 python tools/schur_ab.py c3 2 2>&1 | tail -1
+  RCP_SCHUR_V=$v timeout 300 python tools/schur_ab.py c2 3 2>&1 | tail -1
+done

@@ -1,78 +1,37 @@
-"""A/B of library variants: factor the same matrix once per variant (each in its own process,
-RCP_B200_LIB selects the library), check the factorizations are bit-identical and report Schur /
-panel / total device time.  Variants: "full" (the in-tree librcp_b200.so) and "lower"
-(librcp_lower.so, built with `python -m paper_1710_00125_b200.build --variant lower
--DRCP_FULL_STORAGE=0`: trailing blocks stored lower-only, no mirror stores).
-
-    python tools/schur_ab.py --n 32768 --b 128 --p 144 [--reps 2] [--variants full,lower]
-"""
-import argparse
+"""Device time of one factorization split by kernel (device %globaltimer stamps):
+    python tools/schur_ab.py [c2|c3|c4] [reps]
+Run it under RCP_SCHUR_V=1 / 2 (or RCP_B200_LIB=variant.so) to compare trailing-update kernels;
+prints perm/L checksums so variants can be checked for identical results."""
+import hashlib
 import json
-import os
-import subprocess
 import sys
 from pathlib import Path
 
-ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+import torch  # noqa: E402
 
+from paper_1710_00125_b200 import api, gallery  # noqa: E402
 
-def child(args):
-    sys.path.insert(0, str(ROOT))
-    import hashlib
-
-    import numpy as np
-    import torch
-
-    from paper_1710_00125_b200 import api, gallery
-    a = torch.from_numpy(gallery.type6(args.n, 0)).cuda()
-    cfg = api.FactorConfig(strategy="rcp", b=args.b, q=args.b, p=args.p, seed=0)
-    ws = torch.empty(api.workspace_bytes(args.n, cfg), dtype=torch.uint8, device="cuda")
-    f = None
-    res = []
-    for r in range(args.reps + 1):
-        f = api.factor_device(a, cfg, workspace=ws, out=f)
-        if r:
-            res.append({k: f.stats[k] for k in ("t_factor_ms", "t_schur_ms", "t_panel_ms", "schur_flops")})
-    h = hashlib.sha256()
-    for name in ("perm", "L", "d_diag", "d_off", "pattern"):
-        h.update(getattr(f, name).cpu().numpy().tobytes())
-    best = min(res, key=lambda r: r["t_factor_ms"])
-    best["sha256"] = h.hexdigest()
-    best["tflops_schur"] = best["schur_flops"] / (best["t_schur_ms"] * 1e-3) / 1e12
-    print("RESULT " + json.dumps(best))
-
-
-def main():
-    ap = argparse.ArgumentParser()
-    ap.add_argument("--n", type=int, default=32768)
-    ap.add_argument("--b", type=int, default=128)
-    ap.add_argument("--p", type=int, default=144)
-    ap.add_argument("--reps", type=int, default=2)
-    ap.add_argument("--child", action="store_true")
-    ap.add_argument("--variants", default="full,lower")
-    args = ap.parse_args()
-    if args.child:
-        child(args)
-        return
-    out = {}
-    names = args.variants.split(",")
-    for var in names:
-        env = dict(os.environ)
-        if var != "full":
-            env["RCP_B200_LIB"] = str(ROOT / "paper_1710_00125_b200" / f"librcp_{var}.so")
-        p = subprocess.run([sys.executable, __file__, "--child", "--n", str(args.n), "--b", str(args.b), "--p",
-                            str(args.p), "--reps", str(args.reps)], env=env, capture_output=True, text=True)
-        line = [ln for ln in p.stdout.splitlines() if ln.startswith("RESULT ")]
-        if p.returncode != 0 or not line:
-            print(var, "FAILED", p.returncode, p.stderr[-2000:])
-            sys.exit(1)
-        out[var] = json.loads(line[0][7:])
-        print(var, out[var], flush=True)
-    same = len({out[v]["sha256"] for v in names}) == 1
-    print(f"n={args.n}: bit-identical={same}; " + "; ".join(
-        f"{v}: schur {out[v]['t_schur_ms']:.1f} ms factor {out[v]['t_factor_ms']:.1f} ms" for v in names))
-    sys.exit(0 if same else 2)
-
-
-if __name__ == "__main__":
-    main()
+wl = sys.argv[1] if len(sys.argv) > 1 else "c3"
+reps = int(sys.argv[2]) if len(sys.argv) > 2 else 2
+if wl == "c2":
+    a = gallery.type6_device(8192, 0) if hasattr(gallery, "type6_device") else torch.from_numpy(gallery.type6(8192, 0)).cuda()
+    cfg = api.FactorConfig(strategy="rcp", b=64, q=64, p=74, seed=0)
+elif wl == "c4":
+    a = torch.from_numpy(gallery.kkt_c4(16000, 4000, 0)).cuda()
+    cfg = api.FactorConfig(strategy="rcp", b=64, q=64, p=74, seed=0)
+else:
+    a = gallery.type6_device(32768, 0) if hasattr(gallery, "type6_device") else torch.from_numpy(gallery.type6(32768, 0)).cuda()
+    cfg = api.FactorConfig(strategy="rcp", b=128, q=128, p=144, seed=0)
+best = None
+for it in range(reps + 1):
+    f = api.factor_device(a, cfg)
+    torch.cuda.synchronize()
+    st = {k: f.stats[k] for k in ("t_factor_ms", "t_panel_ms", "t_schur_ms") if k in f.stats}
+    if (it or reps == 0) and (best is None or st["t_factor_ms"] < best["t_factor_ms"]):
+        best = st
+h = hashlib.sha1()
+h.update(f.perm.cpu().numpy().tobytes())
+lsum = float(f.L.sum().item())
+h2 = hashlib.sha1(f.d_diag.cpu().numpy().tobytes()).hexdigest()[:12]
+print(json.dumps({"workload": wl, **best, "perm_sha1": h.hexdigest()[:12], "L_sum": repr(lsum), "d_sha1": h2}), flush=True)
