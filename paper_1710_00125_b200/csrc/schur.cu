@@ -79,10 +79,91 @@ int schur_hints() {
   }();
   return v;
 }
-using Ws2Kernel = decltype(&schur_ws2_kernel<0>);
-Ws2Kernel ws2_kernel() {
+// TMA operand staging in schur_ws2_kernel (RCP_SCHUR_TMA=0: cp.async producer warps instead).
+bool schur_tma_requested() {
+  static const bool v = [] {
+    const char* e = std::getenv("RCP_SCHUR_TMA");
+    return !(e && e[0] == '0');
+  }();
+  return v;
+}
+using Ws2Kernel = decltype(&schur_ws2_kernel<0, false>);
+Ws2Kernel ws2_kernel(bool tma) {
   const int h = schur_hints();
-  return h == 2 ? schur_ws2_kernel<2> : (h == 1 ? schur_ws2_kernel<1> : schur_ws2_kernel<0>);
+  if (tma) return h == 2 ? schur_ws2_kernel<2, true> : (h == 1 ? schur_ws2_kernel<1, true> : schur_ws2_kernel<0, true>);
+  return h == 2 ? schur_ws2_kernel<2, false> : (h == 1 ? schur_ws2_kernel<1, false> : schur_ws2_kernel<0, false>);
+}
+
+// Tensor maps of the operand panels: a K-contiguous [rows][tpad] fp64 array viewed as
+// {4, rows, tpad / 4} with box {4, 128, 4} (see tma_load_3d).  Encoded through the driver entry
+// point (no link against libcuda) and cached per thread: the panels of one factorization keep
+// their addresses.
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiledFn encode_tiled() {
+  static const EncodeTiledFn fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      p = nullptr;
+    return reinterpret_cast<EncodeTiledFn>(p);
+  }();
+  return fn;
+}
+struct OperandMap {
+  const void* ptr = nullptr;
+  int64_t rows = 0;
+  int tpad = 0;
+  bool ok = false;
+  CUtensorMap tm;
+};
+// Returns nullptr when the panel cannot be described (the caller then uses the cp.async kernel).
+const CUtensorMap* operand_map(const double* ptr, int64_t rows, int tpad) {
+  thread_local OperandMap cache[4];
+  thread_local int next = 0;
+  for (auto& c : cache)
+    if (c.ptr == ptr && c.rows == rows && c.tpad == tpad) return c.ok ? &c.tm : nullptr;
+  OperandMap& c = cache[next];
+  next = (next + 1) % 4;
+  c.ptr = ptr;
+  c.rows = rows;
+  c.tpad = tpad;
+  c.ok = false;
+  EncodeTiledFn enc = encode_tiled();
+  if (enc && ptr && rows > 0 && tpad % 4 == 0 && reinterpret_cast<uintptr_t>(ptr) % 16 == 0) {
+    const cuuint64_t dims[3] = {4, (cuuint64_t)rows, (cuuint64_t)(tpad / 4)};
+    const cuuint64_t strides[2] = {(cuuint64_t)tpad * 8, 32};
+    const cuuint32_t box[3] = {4, (cuuint32_t)ws::BM, (cuuint32_t)(kBK / 4)};
+    const cuuint32_t es[3] = {1, 1, 1};
+    c.ok = enc(&c.tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(ptr), dims, strides, box, es,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  }
+  return c.ok ? &c.tm : nullptr;
+}
+
+// One schur_ws2_kernel launch (TMA when the three operand maps exist, else cp.async).
+cudaError_t launch_ws2(unsigned grid, cudaStream_t st, const double* Lneg, const double* Wg, int tpad, int Kl,
+                       const double* A_in, double* A_out, const int* phys, int64_t n, int64_t k, int64_t mp,
+                       const PanelDesc* d, const double* ysk, const double* bin, double* bout, int P,
+                       unsigned long long* tstamp) {
+  const int64_t rows_pad = ((n + ws::BM - 1) / ws::BM) * ws::BM;  // layout.cuh: rows of Lneg / Wg
+  const CUtensorMap* ta = nullptr;
+  const CUtensorMap* tb = nullptr;
+  const CUtensorMap* ty = nullptr;
+  if (schur_tma_requested()) {
+    ta = operand_map(Lneg, rows_pad, tpad);
+    tb = operand_map(Wg, rows_pad, tpad);
+    ty = ysk ? operand_map(ysk, P, tpad) : tb;
+  }
+  const bool tma = ta && tb && ty;
+  static const CUtensorMap none{};
+  ws2_kernel(tma)<<<grid, ws2::kThreads, schur_ws2_smem_bytes(), st>>>(
+      tma ? *ta : none, tma ? *tb : none, tma ? *ty : none, Lneg, Wg, tpad, Kl, A_in, A_out, phys, n, k, mp, d, ysk, bin,
+      bout, P, tstamp);
+  return cudaGetLastError();
 }
 
 bool aligned16(const void* p, int64_t ld) {
@@ -99,15 +180,11 @@ cudaError_t gemm_init_attributes() {
   e = cudaFuncSetAttribute(schur_ws_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)schur_ws_smem_bytes());
   if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(schur_ws2_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)schur_ws2_smem_bytes());
-  if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(schur_ws2_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)schur_ws2_smem_bytes());
-  if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(schur_ws2_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)schur_ws2_smem_bytes());
-  if (e != cudaSuccess) return e;
+  for (Ws2Kernel f : {schur_ws2_kernel<0, false>, schur_ws2_kernel<1, false>, schur_ws2_kernel<2, false>,
+                      schur_ws2_kernel<0, true>, schur_ws2_kernel<1, true>, schur_ws2_kernel<2, true>}) {
+    e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)schur_ws2_smem_bytes());
+    if (e != cudaSuccess) return e;
+  }
   e = cudaFuncSetAttribute(dmma_gemm_kernel<64, 128, kRectStages, 2, RectMap, SketchEpi>,
                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gemm_smem_bytes<64, 128, kRectStages>());
   if (e != cudaSuccess) return e;
@@ -141,9 +218,7 @@ cudaError_t launch_schur_update(int64_t n, int64_t k, int64_t mp, const double* 
           Lneg, Wg, tpad, 0, A_in, A_out, phys, n, 0, 0, 0, d, part, nparts, nullptr, nullptr, nullptr, nullptr, 0,
           tstamp);
     else if (schur_version() == 2)
-      ws2_kernel()
-          <<<(unsigned)sms, ws2::kThreads, schur_ws2_smem_bytes(), st>>>(Lneg, Wg, tpad, 0, A_in, A_out, phys, n, 0, 0,
-                                                                          d, ysk, bin, bout, P, tstamp);
+      return launch_ws2((unsigned)sms, st, Lneg, Wg, tpad, 0, A_in, A_out, phys, n, 0, 0, d, ysk, bin, bout, P, tstamp);
     else
       schur_ws_kernel<false><<<(unsigned)sms, ws::kThreads, schur_ws_smem_bytes(), st>>>(
           Lneg, Wg, tpad, 0, A_in, A_out, phys, n, 0, 0, 0, d, part, nparts, nullptr, ysk, bin, bout, P, tstamp);
@@ -157,10 +232,8 @@ cudaError_t launch_schur_update(int64_t n, int64_t k, int64_t mp, const double* 
     int dev2 = 0, sms2 = 148;
     cudaGetDevice(&dev2);
     cudaDeviceGetAttribute(&sms2, cudaDevAttrMultiProcessorCount, dev2);
-    ws2_kernel()
-        <<<(unsigned)std::min<long long>(supers, sms2), ws2::kThreads, schur_ws2_smem_bytes(), st>>>(
-            Lneg, Wg, tpad, Kl2, A_in, A_out, phys, n, k, mp, nullptr, nullptr, nullptr, nullptr, 0, nullptr);
-    return cudaGetLastError();
+    return launch_ws2((unsigned)std::min<long long>(supers, sms2), st, Lneg, Wg, tpad, Kl2, A_in, A_out, phys, n, k, mp,
+                      nullptr, nullptr, nullptr, nullptr, 0, nullptr);
   }
   const int64_t nbi = (mp + ws::BM - 1) / ws::BM;
   const long long tiles = nbi * (nbi + 1);  // row block I has 2I+2 column blocks of 64

@@ -18,6 +18,8 @@
 // Arithmetic is the same as schur_ws_kernel (zero-initialised accumulators, k ascending, one
 // add into C-in): outputs are bit-identical.
 #pragma once
+#include <cuda.h>
+
 #include "schur_ws.cuh"
 
 namespace rcp {
@@ -112,6 +114,25 @@ RCP_D void stg(u64a g, double v, u64a pol) {
   if (H) asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(g), "d"(v), "l"(pol) : "memory");
   else asm volatile("st.global.f64 [%0], %1;" ::"l"(g), "d"(v) : "memory");
 }
+// TMA: 3-D tiled load of one operand stage.  The tensor map views a K-contiguous panel
+// [rows][tpad] as {4 (k inside a chunk), rows, tpad / 4 (chunks)} with box {4, 128, 4}, so the box
+// lands in shared memory chunk-major ([chunk][row][4]) -- the layout the fragment loads want.
+template <bool H>
+RCP_D void tma_load_3d(unsigned dst, const CUtensorMap* tm, int c0, int c1, int c2, unsigned bar, u64a pol) {
+  if (H)
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint "
+        "[%0], [%1, {%2, %3, %4}], [%5], %6;" ::"r"(dst), "l"(tm), "r"(c0), "r"(c1), "r"(c2), "r"(bar), "l"(pol)
+        : "memory");
+  else
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::
+            "r"(dst), "l"(tm), "r"(c0), "r"(c1), "r"(c2), "r"(bar)
+        : "memory");
+}
+RCP_D void mbar_expect_tx(unsigned long long* b, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(ws::sa(b)), "r"(bytes) : "memory");
+}
 RCP_D u64a policy_evict_last() {
   u64a p;
   asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
@@ -121,9 +142,12 @@ RCP_D u64a policy_evict_last() {
 }  // namespace ws2
 
 // kHints: 0 none, 1 operand panels evict_last, 2 also C-in / C-out evict_first
-template <int kHints>
+// kTma: operand stages filled by TMA (one elected thread, mbarrier transaction counts) instead of
+// 64 threads' cp.async.
+template <int kHints, bool kTma>
 __global__ void __launch_bounds__(ws2::kThreads, 1)
-schur_ws2_kernel(const double* __restrict__ Lneg, const double* __restrict__ Wg, int tpad, int Kl,
+schur_ws2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                 const __grid_constant__ CUtensorMap tmY, const double* __restrict__ Lneg, const double* __restrict__ Wg, int tpad, int Kl,
                  const double* __restrict__ ain, double* __restrict__ aout, const int* __restrict__ phys, int64_t n,
                  int64_t k, int64_t mp, const PanelDesc* __restrict__ d, const double* __restrict__ ysk,
                  const double* __restrict__ bin, double* __restrict__ bout, int P,
@@ -141,20 +165,21 @@ schur_ws2_kernel(const double* __restrict__ Lneg, const double* __restrict__ Wg,
   const long long s_all = s_tri + nbi * nbp2;
   unsigned long long* const ts_schur = (tstamp && d) ? tstamp + 4 * (size_t)d->pidx + 2 : nullptr;
   stamp_start(ts_schur);
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
+  extern __shared__ __align__(128) unsigned char smem_ws2[];
+  Smem& sm = *reinterpret_cast<Smem*>(smem_ws2);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int KT = Kl / kBK;
   const long long x0 = blockIdx.x, xs = gridDim.x;
   if (tid == 0) {
     for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&sm.full[s], kProdThreads);
+      mbar_init(&sm.full[s], kTma ? 1 : kProdThreads);
       mbar_init(&sm.empty[s], kMmaWarps);
     }
     for (int h = 0; h < 2; ++h) {
       mbar_init(&sm.cin[h], kEpiThreads);
       mbar_init(&sm.accd[h], kMmaWarps / 2);
     }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
 
@@ -247,6 +272,27 @@ schur_ws2_kernel(const double* __restrict__ Lneg, const double* __restrict__ Wg,
       static_assert(BM == SN, "operand stages share the row count");
       unsigned stage = 0, ephase = 1;  // fresh "empty" barriers count as released
       const u64a pol_keep = kHints >= 1 ? policy_evict_last() : 0;
+      if (kTma) {
+        if (pt == 0) {  // one elected thread feeds the ring
+          for (long long x = x0; x < s_all; x += xs) {
+            int64_t m0, n0;
+            const bool skt = super_at(x, s_tri, nbp2, m0, n0);
+            const CUtensorMap* tb = skt ? &tmY : &tmB;
+            for (int kt = 0; kt < KT; ++kt) {
+              mbar_wait(&sm.empty[stage], ephase);
+              mbar_expect_tx(&sm.full[stage], (unsigned)(sizeof(double) * (BM + SN) * kBK));
+              tma_load_3d<(kHints >= 1)>(ws::sa(sm.a[stage]), &tmA, 0, (int)m0, kt * (kBK / 4), ws::sa(&sm.full[stage]),
+                                         pol_keep);
+              tma_load_3d<(kHints >= 1)>(ws::sa(sm.b[stage]), tb, 0, (int)n0, kt * (kBK / 4), ws::sa(&sm.full[stage]),
+                                         pol_keep);
+              if (++stage == STAGES) {
+                stage = 0;
+                ephase ^= 1;
+              }
+            }
+          }
+        }
+      } else
       for (long long x = x0; x < s_all; x += xs) {
         int64_t m0, n0;
         const bool skt = super_at(x, s_tri, nbp2, m0, n0);
