@@ -186,8 +186,12 @@ schur_ws2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
   if (warp < kMmaWarps) {
     // ======================= MMA groups =======================
     setmaxnreg_inc<kMmaRegs>();
-    const int h = warp >> 2, w = warp & 3;
-    const int g = lane >> 2, q = lane & 3;
+    // Identity shuffles: ptxas otherwise re-derives lane / warp / fragment offsets from S2R SR_TID.X
+    // inside the k-loop (a ~50-cycle special-register read per stage); a SHFL result is not
+    // rematerialised, so these stay in registers.
+    const int mlane = __shfl_sync(0xffffffffu, lane, lane), mwarp = __shfl_sync(0xffffffffu, warp, lane);
+    const int h = mwarp >> 2, w = mwarp & 3;
+    const int g = mlane >> 2, q = mlane & 3;
     const int wm0 = (w >> 1) * 64, wc0 = (w & 1) * 32;  // rows of A / columns inside the half
     constexpr int MF = 8, NF = 4;
     // fragment offsets inside a stage: row (base + 8 i + g), k = 4 c + q
@@ -244,7 +248,7 @@ schur_ws2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
             for (int i = 0; i < MF; ++i) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[cb][i], bf[cb][j]);
         }
         __syncwarp();
-        if (lane == 0) mbar_arrive(&sm.empty[stage]);
+        if (mlane == 0) mbar_arrive(&sm.empty[stage]);
         stage = nstage;
         sphase = nphase;
       }
@@ -259,7 +263,7 @@ schur_ws2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
           sm.c[h][lj + 1][li] = __dadd_rn(sm.c[h][lj + 1][li], acc[i][j][1]);
         }
       __syncwarp();
-      if (lane == 0) mbar_arrive(&sm.accd[h]);
+      if (mlane == 0) mbar_arrive(&sm.accd[h]);
     }
   } else {
     setmaxnreg_dec<kAuxRegs>();
