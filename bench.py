@@ -474,7 +474,9 @@ def run_b200(args, rank: int, world: int, local_rank: int):
             cpu = {"value": None, "unit": "GFLOP/s", "cores": cores_used(), "kind": "port",
                    "sample": "host out of memory for the n=32768 oracle sample"}
     achieved = schur_flops / (schur_ms / 1e3) / 1e12 if schur_ms > 0 else None
-    schur_key = "schur_ws_kernel" if args.workload == "c3" else f"schur_ws_kernel@{args.workload}"
+    # the single-GPU trailing update is schur_ws2_kernel (N > 1: the tile-dealing schur_ws_kernel)
+    schur_name = "schur_ws2_kernel" if world == 1 else "schur_ws_kernel"
+    schur_key = schur_name if args.workload == "c3" else f"{schur_name}@{args.workload}"
     line = {
         "metric": metric_name(args), "value": value, "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
         "warmup": max(3, args.warmup), "ms_per_step": ms_max, "higher_is_better": True,
@@ -483,7 +485,7 @@ def run_b200(args, rank: int, world: int, local_rank: int):
         "config": cfg_dict(args, world),
         "pct_fp64_peak": 100.0 * value / (world * FP64_PEAK_GFLOPS),
         "fp64_peak": {"value": FP64_PEAK_GFLOPS, "unit": "GFLOP/s", "source": FP64_PEAK_SRC},
-        "roofline": {"bound": "tensor", "kernel": "schur_ws_kernel (trailing Schur update, DMMA.8x8x4)",
+        "roofline": {"bound": "tensor", "kernel": schur_name + " (trailing Schur update, DMMA.8x8x4)",
                      "achieved": achieved, "peak": FP64_PEAK_GFLOPS / 1e3, "unit": "TFLOP/s",
                      "frac": (achieved / (FP64_PEAK_GFLOPS / 1e3)) if achieved else None,
                      "traffic": ncu_traffic(schur_key),

@@ -29,7 +29,16 @@ namespace {
 
 constexpr int kPanelThreads = 256;
 constexpr int kWarps = kPanelThreads / 32;
-constexpr int kRegRows = 32;  // QRCP register mode: sketch rows [0, 32) of each column live in registers
+constexpr int kRegRows = 32;  // QRCP register mode: 32 sketch rows of each column live in registers
+#ifndef RCP_QRCP_REG_TAIL
+#define RCP_QRCP_REG_TAIL 0
+#endif
+// Which rows: head (0, default) = rows [0, 32); tail (1) = the last 32 rows, which stay live through
+// every QRCP step (rows [0, j) are finished after step j), cutting the shared-memory row passes of
+// a 128-step panel at P = 144 from 9776 to 6328.  Measured at C3: panel 407.3 ms (tail) vs 404.8 ms
+// (head), identical results -- the reflect pass is bound by its per-thread dependent chain, not by
+// shared-memory bandwidth, and the tail mode runs the 32 predicated register rows in all steps.
+constexpr bool kRegTail = RCP_QRCP_REG_TAIL != 0;
 constexpr long long kWatchdogCycles = 8000000000LL;
 
 struct BlockBest {
@@ -244,14 +253,17 @@ __global__ void __launch_bounds__(kPanelThreads, 1) panel_kernel(PanelParams pin
     const bool regmode = p.qmode == 1;
     const int PRr = regmode ? min(P, kRegRows) : 0;
     const int Ps = P - PRr;
+    const int RR0 = kRegTail ? P - PRr : 0;  // first register row (register rows [RR0, RR0 + PRr))
+    const int S0 = kRegTail ? 0 : PRr;       // first shared-memory row (rows [S0, S0 + Ps))
+    const int S1 = S0 + Ps;
     const int Rs = regmode ? R : p.Rs;  // columns whose rows >= PRr live in smem
     const int Rg = R - Rs;
     double* Bs = reinterpret_cast<double*>(region);  // [Ps][Rs] row-major
     double* qnorm = Bs + (size_t)Ps * Rs;             // generic mode only
     int* qsel = reinterpret_cast<int*>(qnorm + R);
     double* qg = p.qscr + (size_t)cta * Ps * (Rg > 0 ? Rg : 0);
-    auto bsm = [&](int r, int c) -> double& {  // row r >= PRr of column c
-      return c < Rs ? Bs[(r - PRr) * Rs + c] : qg[(size_t)(r - PRr) * Rg + (c - Rs)];
+    auto bsm = [&](int r, int c) -> double& {  // shared-memory row r in [S0, S1) of column c
+      return c < Rs ? Bs[(r - S0) * Rs + c] : qg[(size_t)(r - S0) * Rg + (c - Rs)];
     };
     double rg[kRegRows];
     const bool own = regmode && tid < rcnt;
@@ -269,7 +281,7 @@ __global__ void __launch_bounds__(kPanelThreads, 1) panel_kernel(PanelParams pin
     if (own) {
       const double* src = p.B + (size_t)(k0 + r0 + tid) * P;
 #pragma unroll
-      for (int r = 0; r < kRegRows; ++r) rg[r] = (r < PRr) ? src[r] : 0.0;
+      for (int r = 0; r < kRegRows; ++r) rg[r] = (r < PRr) ? src[RR0 + r] : 0.0;
     }
     {  // sketch rows >= PRr of the owned columns: 8 independent loads in flight per thread
       const int tot = Ps * rcnt;
@@ -279,17 +291,17 @@ __global__ void __launch_bounds__(kPanelThreads, 1) panel_kernel(PanelParams pin
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
           const int e = f + u * nthr, c = e / Ps, r = e - c * Ps;
-          v[u] = __ldcg(p.B + (size_t)(k0 + r0 + c) * P + PRr + r);
+          v[u] = __ldcg(p.B + (size_t)(k0 + r0 + c) * P + S0 + r);
         }
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
           const int e = f + u * nthr, c = e / Ps, r = e - c * Ps;
-          bsm(PRr + r, c) = v[u];
+          bsm(S0 + r, c) = v[u];
         }
       }
       for (; f < tot; f += nthr) {
         const int c = f / Ps, r = f - c * Ps;
-        bsm(PRr + r, c) = p.B[(size_t)(k0 + r0 + c) * P + PRr + r];
+        bsm(S0 + r, c) = p.B[(size_t)(k0 + r0 + c) * P + S0 + r];
       }
     }
     if (!regmode)
@@ -300,13 +312,13 @@ __global__ void __launch_bounds__(kPanelThreads, 1) panel_kernel(PanelParams pin
       double ss0 = 0.0, ss1 = 0.0, am = 0.0;
 #pragma unroll
       for (int r = 0; r < kRegRows; ++r) {
-        if (r >= lo && r < PRr) {
+        if (RR0 + r >= lo && r < PRr) {
           am = fmax(am, fabs(rg[r]));
           if (r & 1) ss1 = __fma_rn(rg[r], rg[r], ss1); else ss0 = __fma_rn(rg[r], rg[r], ss0);
         }
       }
-      for (int r = max(lo, PRr); r < P; ++r) {
-        const double x = Bs[(r - PRr) * Rs + tid];
+      for (int r = max(lo, S0); r < S1; ++r) {
+        const double x = Bs[(r - S0) * Rs + tid];
         am = fmax(am, fabs(x));
         if (r & 1) ss1 = __fma_rn(x, x, ss1); else ss0 = __fma_rn(x, x, ss0);
       }
@@ -321,12 +333,12 @@ __global__ void __launch_bounds__(kPanelThreads, 1) panel_kernel(PanelParams pin
         double s2 = 0.0;
 #pragma unroll
         for (int r = 0; r < kRegRows; ++r)
-          if (r >= lo && r < PRr) {
+          if (RR0 + r >= lo && r < PRr) {
             const double x = fabs(rg[r]) / am;
             s2 = __fma_rn(x, x, s2);
           }
-        for (int r = max(lo, PRr); r < P; ++r) {
-          const double x = fabs(Bs[(r - PRr) * Rs + tid]) / am;
+        for (int r = max(lo, S0); r < S1; ++r) {
+          const double x = fabs(Bs[(r - S0) * Rs + tid]) / am;
           s2 = __fma_rn(x, x, s2);
         }
         myn = am * sqrt(s2);
@@ -343,24 +355,25 @@ __global__ void __launch_bounds__(kPanelThreads, 1) panel_kernel(PanelParams pin
     // values bit-identical to applying each reflector eagerly.
     auto reflect_fused = [&](const double* vc, const double* vp, int jj, double coef, int skip) {
       double d0 = 0.0, d1 = 0.0, d2 = 0.0, d3 = 0.0;
-      const bool regs_live = jj < PRr;  // uniform: register rows are all finished once jj >= PRr
+      const bool regs_live = jj < RR0 + PRr;  // uniform: false once every register row is finished
+      const double* vcr = vc + RR0;           // reflector entries of the register rows
       if (!skip && regs_live) {
 #pragma unroll
         for (int r = 0; r < kRegRows; r += 4) {
-          if (r >= jj && r < PRr) d0 = __fma_rn(vc[r], rg[r], d0);
-          if (r + 1 >= jj && r + 1 < PRr) d1 = __fma_rn(vc[r + 1], rg[r + 1], d1);
-          if (r + 2 >= jj && r + 2 < PRr) d2 = __fma_rn(vc[r + 2], rg[r + 2], d2);
-          if (r + 3 >= jj && r + 3 < PRr) d3 = __fma_rn(vc[r + 3], rg[r + 3], d3);
+          if (RR0 + r >= jj && r < PRr) d0 = __fma_rn(vcr[r], rg[r], d0);
+          if (RR0 + r + 1 >= jj && r + 1 < PRr) d1 = __fma_rn(vcr[r + 1], rg[r + 1], d1);
+          if (RR0 + r + 2 >= jj && r + 2 < PRr) d2 = __fma_rn(vcr[r + 2], rg[r + 2], d2);
+          if (RR0 + r + 3 >= jj && r + 3 < PRr) d3 = __fma_rn(vcr[r + 3], rg[r + 3], d3);
         }
       }
-      const int rs = max(jj, PRr);
+      const int rs = max(jj, S0);
       double xjj = 0.0;  // x at row jj (smem rows) after the pending update
       {
         int r = rs;
-        double* bw = Bs + (size_t)(r - PRr) * Rs + tid;
+        double* bw = Bs + (size_t)(r - S0) * Rs + tid;
         if (pend) {
           const double wp = wpend;
-          for (; r + 4 <= P; r += 4, bw += 4 * Rs) {
+          for (; r + 4 <= S1; r += 4, bw += 4 * Rs) {
             double x0 = bw[0], x1 = bw[Rs], x2 = bw[2 * Rs], x3 = bw[3 * Rs];
             x0 = __fma_rn(-vp[r], wp, x0);
             x1 = __fma_rn(-vp[r + 1], wp, x1);
@@ -378,14 +391,14 @@ __global__ void __launch_bounds__(kPanelThreads, 1) panel_kernel(PanelParams pin
               d3 = __fma_rn(vc[r + 3], x3, d3);
             }
           }
-          for (; r < P; ++r, bw += Rs) {
+          for (; r < S1; ++r, bw += Rs) {
             const double x = __fma_rn(-vp[r], wp, *bw);
             *bw = x;
             if (r == jj) xjj = x;
             if (!skip) d0 = __fma_rn(vc[r], x, d0);
           }
         } else {
-          for (; r + 4 <= P; r += 4, bw += 4 * Rs) {
+          for (; r + 4 <= S1; r += 4, bw += 4 * Rs) {
             const double x0 = bw[0], x1 = bw[Rs], x2 = bw[2 * Rs], x3 = bw[3 * Rs];
             if (r == jj) xjj = x0;
             if (!skip) {
@@ -395,7 +408,7 @@ __global__ void __launch_bounds__(kPanelThreads, 1) panel_kernel(PanelParams pin
               d3 = __fma_rn(vc[r + 3], x3, d3);
             }
           }
-          for (; r < P; ++r, bw += Rs) {
+          for (; r < S1; ++r, bw += Rs) {
             const double x = *bw;
             if (r == jj) xjj = x;
             if (!skip) d0 = __fma_rn(vc[r], x, d0);
@@ -408,15 +421,15 @@ __global__ void __launch_bounds__(kPanelThreads, 1) panel_kernel(PanelParams pin
         if (regs_live) {
 #pragma unroll
           for (int r2 = 0; r2 < kRegRows; ++r2)
-            if (r2 >= jj && r2 < PRr) rg[r2] = __fma_rn(-vc[r2], wv, rg[r2]);
+            if (RR0 + r2 >= jj && r2 < PRr) rg[r2] = __fma_rn(-vcr[r2], wv, rg[r2]);
         }
       }
       double yj;
-      if (jj < PRr) {
+      if (jj >= RR0 && jj < RR0 + PRr) {
         yj = 0.0;
 #pragma unroll
         for (int r2 = 0; r2 < kRegRows; ++r2)
-          if (r2 == jj) yj = rg[r2];
+          if (RR0 + r2 == jj) yj = rg[r2];
       } else {
         yj = skip ? xjj : __fma_rn(-vc[jj], wv, xjj);
       }
@@ -425,8 +438,8 @@ __global__ void __launch_bounds__(kPanelThreads, 1) panel_kernel(PanelParams pin
       if (exact_only || !(n2 > 1e-6 * myn2x) || !(n2 > 1e-280)) {
         // the exact recompute needs the current values: apply this step's reflector now
         if (!skip) {
-          double* bw = Bs + (size_t)(rs - PRr) * Rs + tid;
-          for (int r = rs; r < P; ++r, bw += Rs) *bw = __fma_rn(-vc[r], wv, *bw);
+          double* bw = Bs + (size_t)(rs - S0) * Rs + tid;
+          for (int r = rs; r < S1; ++r, bw += Rs) *bw = __fma_rn(-vc[r], wv, *bw);
           wpend = 0.0;  // already applied; x - v * 0 leaves the values unchanged next step
         }
         exact_norm(jj + 1);
@@ -500,15 +513,15 @@ __global__ void __launch_bounds__(kPanelThreads, 1) panel_kernel(PanelParams pin
         const int lane = tid & 31;
         const int hwarp = lb.slot < 0 ? -1 : (regmode ? (lb.slot >> 5) : 0);
         if ((tid >> 5) == hwarp) {
-          if (regmode && j < PRr && lane == (lb.slot & 31)) {
+          if (regmode && j < RR0 + PRr && lane == (lb.slot & 31)) {
 #pragma unroll
             for (int r = 0; r < kRegRows; ++r)
-              if (r >= j && r < PRr) vcur[r] = rg[r];
+              if (RR0 + r >= j && r < PRr) vcur[RR0 + r] = rg[r];
           }
           const double wc = __shfl_sync(0xffffffffu, wpend, lb.slot & 31);  // candidate's pending w
-          for (int r = max(j, PRr) + lane; r < P; r += 32) {
+          for (int r = max(j, S0) + lane; r < S1; r += 32) {
             if (regmode) {
-              const double x = Bs[(r - PRr) * Rs + lb.slot];
+              const double x = Bs[(r - S0) * Rs + lb.slot];
               vcur[r] = pend ? __fma_rn(-vprv[r], wc, x) : x;
             } else {
               vcur[r] = bsm(r, lb.slot);
