@@ -25,7 +25,8 @@ def main() -> None:
         name = r[ik]
         if name.startswith("void "):
             name = name[5:]
-        name = name.split("(")[0].split("<")[0].replace("rcp::", "").replace("(anonymous namespace)::", "")
+        name = name.replace("<unnamed>::", "").replace("(anonymous namespace)::", "")
+        name = name.split("(")[0].split("<")[0].replace("rcp::", "")
         try:
             v = float(r[iv].replace(",", "")) * scale.get(r[iu], 1e-6)
         except ValueError:
