@@ -17,6 +17,9 @@ reps = int(sys.argv[2]) if len(sys.argv) > 2 else 2
 if wl == "c2":
     a = gallery.type6_device(8192, 0) if hasattr(gallery, "type6_device") else torch.from_numpy(gallery.type6(8192, 0)).cuda()
     cfg = api.FactorConfig(strategy="rcp", b=64, q=64, p=74, seed=0)
+elif wl == "c1":
+    a = torch.from_numpy(gallery.type6(1000, 0)).cuda()
+    cfg = api.FactorConfig(strategy="rcp", b=32, q=32, p=42, seed=0)
 elif wl == "c4":
     a = torch.from_numpy(gallery.kkt_c4(16000, 4000, 0)).cuda()
     cfg = api.FactorConfig(strategy="rcp", b=64, q=64, p=74, seed=0)
@@ -34,4 +37,13 @@ h = hashlib.sha1()
 h.update(f.perm.cpu().numpy().tobytes())
 lsum = float(f.L.sum().item())
 h2 = hashlib.sha1(f.d_diag.cpu().numpy().tobytes()).hexdigest()[:12]
+b = torch.from_numpy(gallery.rhs(a.shape[0], 1)).cuda()
+torch.cuda.synchronize()
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+x = api.solve_device(f, b)
+e0.record()
+x = api.solve_device(f, b)
+e1.record()
+torch.cuda.synchronize()
+best["t_solve_ms"] = e0.elapsed_time(e1)
 print(json.dumps({"workload": wl, **best, "perm_sha1": h.hexdigest()[:12], "L_sum": repr(lsum), "d_sha1": h2}), flush=True)
