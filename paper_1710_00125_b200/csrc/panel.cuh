@@ -9,7 +9,14 @@ namespace rcp {
 
 #define RCP_PG __host__ __device__ inline
 
-constexpr int kPanelRowsMin = 32;   // fewest rows per CTA before the panel uses fewer CTAs
+#ifndef RCP_PANEL_ROWS_MIN
+#define RCP_PANEL_ROWS_MIN 128
+#endif
+// Fewest rows per CTA before the panel uses fewer CTAs.  One row / sketch column per thread costs the same
+// wall time for 32 or 128 rows per CTA, while every exchange gets cheaper with fewer CTAs (fewer records
+// for the reducer, less arrival skew): 128 vs 32 measured -5 % panel time at C2 / C4, -1.5 % at C3
+// (profiles/r02_panel_experiments.txt); results are bit-identical for any value.
+constexpr int kPanelRowsMin = RCP_PANEL_ROWS_MIN;
 constexpr int kPanelMaxCTAs = 160;  // == kMaxSMs (exchange buffers are sized for it)
 constexpr int kPanelRegRows = 32;   // QRCP register mode: sketch rows [0, 32) in registers
 
