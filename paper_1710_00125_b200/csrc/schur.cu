@@ -135,7 +135,7 @@ const CUtensorMap* operand_map(const double* ptr, int64_t rows, int tpad) {
   if (enc && ptr && rows > 0 && tpad % 4 == 0 && reinterpret_cast<uintptr_t>(ptr) % 16 == 0) {
     const cuuint64_t dims[3] = {4, (cuuint64_t)rows, (cuuint64_t)(tpad / 4)};
     const cuuint64_t strides[2] = {(cuuint64_t)tpad * 8, 32};
-    const cuuint32_t box[3] = {4, (cuuint32_t)ws::BM, (cuuint32_t)(kBK / 4)};
+    const cuuint32_t box[3] = {4, (cuuint32_t)ws::BM, (cuuint32_t)(ws2::KS / 4)};
     const cuuint32_t es[3] = {1, 1, 1};
     c.ok = enc(&c.tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(ptr), dims, strides, box, es,
                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,

@@ -34,7 +34,11 @@ using ws::mbar_init;
 using ws::mbar_wait;
 using ws::named_sync;
 constexpr int SN = 2 * BN;  // supertile width
-constexpr int STAGES = 3;
+#ifndef RCP_WS2_KS
+#define RCP_WS2_KS 16
+#endif
+constexpr int KS = RCP_WS2_KS;        // k-columns per operand stage (8 or 16)
+constexpr int STAGES = 48 / KS;       // 96 KB of operand stages either way
 constexpr int kMmaWarps = 8, kThreads = 384, kProdThreads = 64, kEpiThreads = 64;
 constexpr int kCStride = BM + 2;
 #ifndef RCP_WS2_MMAREGS
@@ -46,8 +50,8 @@ constexpr int kCStride = BM + 2;
 constexpr int kMmaRegs = RCP_WS2_MMAREGS, kAuxRegs = RCP_WS2_AUXREGS;
 
 struct Smem {
-  double a[STAGES][BM * kBK];  // element (row, k) at opidx(BM, row, k)
-  double b[STAGES][SN * kBK];
+  double a[STAGES][BM * KS];  // element (row, k) at opidx(BM, row, k)
+  double b[STAGES][SN * KS];
   double c[2][BN][kCStride];
   int colmap[2][BN];
   unsigned long long full[STAGES], empty[STAGES], cin[2], accd[2];
@@ -168,7 +172,7 @@ schur_ws2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
   extern __shared__ __align__(128) unsigned char smem_ws2[];
   Smem& sm = *reinterpret_cast<Smem*>(smem_ws2);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int KT = Kl / kBK;
+  const int KT = Kl / KS;
   const long long x0 = blockIdx.x, xs = gridDim.x;
   if (tid == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -226,9 +230,9 @@ schur_ws2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
           nphase ^= 1;
         }
 #pragma unroll
-        for (int c = 0; c < kBK / 4; ++c) {
+        for (int c = 0; c < KS / 4; ++c) {
           const int cb = c & 1;
-          if (c + 1 < kBK / 4) {
+          if (c + 1 < KS / 4) {
 #pragma unroll
             for (int i = 0; i < MF; ++i) af[cb ^ 1][i] = as[(c + 1) * BM * 4 + i * 32];
 #pragma unroll
@@ -270,9 +274,11 @@ schur_ws2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
     if (warp < kMmaWarps + 2) {
       // ======================= producer warps =======================
       const int pt = tid - 32 * kMmaWarps;  // 0..63
-      const int srow = pt >> 3, c16 = pt & 7;
+      constexpr int TPR = KS / 2;           // threads per operand row (16 bytes each)
+      constexpr int RPP = 64 / TPR;         // rows per pass of the 64 producer threads
+      const int srow = pt / TPR, c16 = pt % TPR;
       const int soff = c16 * 2;
-      const int dofs = opidx(BM, srow, soff);  // opidx(row = srow + 8u, soff) = dofs + 32 u  (BM == SN)
+      const int dofs = opidx(BM, srow, soff);  // opidx(row = srow + RPP u, soff) = dofs + 4 RPP u  (BM == SN)
       static_assert(BM == SN, "operand stages share the row count");
       unsigned stage = 0, ephase = 1;  // fresh "empty" barriers count as released
       const u64a pol_keep = kHints >= 1 ? policy_evict_last() : 0;
@@ -284,10 +290,10 @@ schur_ws2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
             const CUtensorMap* tb = skt ? &tmY : &tmB;
             for (int kt = 0; kt < KT; ++kt) {
               mbar_wait(&sm.empty[stage], ephase);
-              mbar_expect_tx(&sm.full[stage], (unsigned)(sizeof(double) * (BM + SN) * kBK));
-              tma_load_3d<(kHints >= 1)>(ws::sa(sm.a[stage]), &tmA, 0, (int)m0, kt * (kBK / 4), ws::sa(&sm.full[stage]),
+              mbar_expect_tx(&sm.full[stage], (unsigned)(sizeof(double) * (BM + SN) * KS));
+              tma_load_3d<(kHints >= 1)>(ws::sa(sm.a[stage]), &tmA, 0, (int)m0, kt * (KS / 4), ws::sa(&sm.full[stage]),
                                          pol_keep);
-              tma_load_3d<(kHints >= 1)>(ws::sa(sm.b[stage]), tb, 0, (int)n0, kt * (kBK / 4), ws::sa(&sm.full[stage]),
+              tma_load_3d<(kHints >= 1)>(ws::sa(sm.b[stage]), tb, 0, (int)n0, kt * (KS / 4), ws::sa(&sm.full[stage]),
                                          pol_keep);
               if (++stage == STAGES) {
                 stage = 0;
@@ -304,21 +310,21 @@ schur_ws2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
         const double* bsrc = skt ? ysk : Wg;
         const int64_t blim = skt ? P : mp;
         const double* bb = bsrc + (n0 + srow) * (int64_t)tpad + soff;
-        const int64_t step = 8 * (int64_t)tpad;
+        const int64_t step = RPP * (int64_t)tpad;
         const bool interior = m0 + BM <= mp && n0 + SN <= blim;
         for (int kt = 0; kt < KT; ++kt) {
           mbar_wait(&sm.empty[stage], ephase);
-          const int64_t k0 = (int64_t)kt * kBK;
+          const int64_t k0 = (int64_t)kt * KS;
           double* da = sm.a[stage] + dofs;
           double* db = sm.b[stage] + dofs;
           if (interior) {  // no predicates, immediate strides
-            const unsigned t64 = (unsigned)tpad * 64u;  // bytes between rows r and r + 8
+            const unsigned t64 = (unsigned)tpad * (8u * RPP);  // bytes between rows r and r + RPP
             const u64a ua = (u64a)(ab + k0), ub = (u64a)(bb + k0);
             const unsigned sda = ws::sa(da), sdb = ws::sa(db);
 #pragma unroll
-            for (int u = 0; u < BM / 8; ++u) cpa16<(kHints >= 1)>(sda + u * 32 * 8, ua + (u64a)u * t64, pol_keep);
+            for (int u = 0; u < BM / RPP; ++u) cpa16<(kHints >= 1)>(sda + u * 4 * RPP * 8, ua + (u64a)u * t64, pol_keep);
 #pragma unroll
-            for (int u = 0; u < SN / 8; ++u) cpa16<(kHints >= 1)>(sdb + u * 32 * 8, ub + (u64a)u * t64, pol_keep);
+            for (int u = 0; u < SN / RPP; ++u) cpa16<(kHints >= 1)>(sdb + u * 4 * RPP * 8, ub + (u64a)u * t64, pol_keep);
             mbar_arrive_cpasync(&sm.full[stage]);
             if (++stage == STAGES) {
               stage = 0;
@@ -327,14 +333,14 @@ schur_ws2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
             continue;
           }
 #pragma unroll
-          for (int u = 0; u < BM / 8; ++u) {
-            const bool ok = m0 + srow + 8 * u < mp;
-            cp_async16(da + u * 32, ok ? ab + u * step + k0 : Lneg, ok);
+          for (int u = 0; u < BM / RPP; ++u) {
+            const bool ok = m0 + srow + RPP * u < mp;
+            cp_async16(da + u * 4 * RPP, ok ? ab + u * step + k0 : Lneg, ok);
           }
 #pragma unroll
-          for (int u = 0; u < SN / 8; ++u) {
-            const bool ok = n0 + srow + 8 * u < blim;
-            cp_async16(db + u * 32, ok ? bb + u * step + k0 : Lneg, ok);
+          for (int u = 0; u < SN / RPP; ++u) {
+            const bool ok = n0 + srow + RPP * u < blim;
+            cp_async16(db + u * 4 * RPP, ok ? bb + u * step + k0 : Lneg, ok);
           }
           mbar_arrive_cpasync(&sm.full[stage]);
           if (++stage == STAGES) {
