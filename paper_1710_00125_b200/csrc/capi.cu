@@ -504,7 +504,13 @@ static int factor_core(const rcp_config* cfg, int64_t n, const double* a, int64_
   // chain, the host rolls back to that panel and handles them.
   const bool q1 = rcp_strat && (c.q == 1);
   const int q_eff = rcp_strat ? c.q : 0;  // no sketch selection outside rcp (factor.py:548, 608)
-  const int sms_cap = std::min(num_sms, kMaxSMs);
+  int sms_cap = std::min(num_sms, kMaxSMs);
+  // Experiment knob (SM-partition model): RCP_PANEL_SMS caps the panel grid as if
+  // only that many SMs were reserved for the panel.  Unset in production.
+  if (const char* e = std::getenv("RCP_PANEL_SMS")) {
+    const int v = std::atoi(e);
+    if (v >= 1 && v < sms_cap) sms_cap = v;
+  }
   // launch grid: the largest G any panel can ask for (G(m0) is not monotone in m0); CTAs
   // beyond a panel's own G return at once
   const int gmax = sms_cap;

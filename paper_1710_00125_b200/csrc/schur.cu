@@ -213,6 +213,12 @@ cudaError_t launch_schur_update(int64_t n, int64_t k, int64_t mp, const double* 
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    // experiment knob: RCP_SCHUR_SMS runs the update on a partition of the SMs
+    static const int sms_env = [] {
+      const char* e = std::getenv("RCP_SCHUR_SMS");
+      return e ? std::atoi(e) : 0;
+    }();
+    if (sms_env >= 1 && sms_env < sms) sms = sms_env;
     if (nparts > 1)
       schur_ws_kernel<true><<<(unsigned)sms, ws::kThreads, schur_ws_smem_bytes(), st>>>(
           Lneg, Wg, tpad, 0, A_in, A_out, phys, n, 0, 0, 0, d, part, nparts, nullptr, nullptr, nullptr, nullptr, 0,
