@@ -87,11 +87,15 @@ bool schur_tma_requested() {
   }();
   return v;
 }
-using Ws2Kernel = decltype(&schur_ws2_kernel<0, false>);
-Ws2Kernel ws2_kernel(bool tma) {
+using Ws2Kernel = decltype(&schur_ws2_kernel<0, false, false>);
+template <bool kTma, bool kMulti>
+Ws2Kernel ws2_pick(int h) {
+  return h == 2 ? schur_ws2_kernel<2, kTma, kMulti> : (h == 1 ? schur_ws2_kernel<1, kTma, kMulti> : schur_ws2_kernel<0, kTma, kMulti>);
+}
+Ws2Kernel ws2_kernel(bool tma, bool multi) {
   const int h = schur_hints();
-  if (tma) return h == 2 ? schur_ws2_kernel<2, true> : (h == 1 ? schur_ws2_kernel<1, true> : schur_ws2_kernel<0, true>);
-  return h == 2 ? schur_ws2_kernel<2, false> : (h == 1 ? schur_ws2_kernel<1, false> : schur_ws2_kernel<0, false>);
+  if (multi) return tma ? ws2_pick<true, true>(h) : ws2_pick<false, true>(h);
+  return tma ? ws2_pick<true, false>(h) : ws2_pick<false, false>(h);
 }
 
 // Tensor maps of the operand panels: a K-contiguous [rows][tpad] fp64 array viewed as
@@ -121,12 +125,12 @@ struct OperandMap {
 };
 // Returns nullptr when the panel cannot be described (the caller then uses the cp.async kernel).
 const CUtensorMap* operand_map(const double* ptr, int64_t rows, int tpad) {
-  thread_local OperandMap cache[4];
+  thread_local OperandMap cache[16];  // rank 0's three panels + the emulated workers' copies
   thread_local int next = 0;
   for (auto& c : cache)
     if (c.ptr == ptr && c.rows == rows && c.tpad == tpad) return c.ok ? &c.tm : nullptr;
   OperandMap& c = cache[next];
-  next = (next + 1) % 4;
+  next = (next + 1) % 16;
   c.ptr = ptr;
   c.rows = rows;
   c.tpad = tpad;
@@ -148,7 +152,7 @@ const CUtensorMap* operand_map(const double* ptr, int64_t rows, int tpad) {
 cudaError_t launch_ws2(unsigned grid, cudaStream_t st, const double* Lneg, const double* Wg, int tpad, int Kl,
                        const double* A_in, double* A_out, const int* phys, int64_t n, int64_t k, int64_t mp,
                        const PanelDesc* d, const double* ysk, const double* bin, double* bout, int P,
-                       unsigned long long* tstamp) {
+                       unsigned long long* tstamp, int part = 0, int nparts = 1, const SchurDyn* dyn = nullptr) {
   const int64_t rows_pad = ((n + ws::BM - 1) / ws::BM) * ws::BM;  // layout.cuh: rows of Lneg / Wg
   const CUtensorMap* ta = nullptr;
   const CUtensorMap* tb = nullptr;
@@ -160,9 +164,9 @@ cudaError_t launch_ws2(unsigned grid, cudaStream_t st, const double* Lneg, const
   }
   const bool tma = ta && tb && ty;
   static const CUtensorMap none{};
-  ws2_kernel(tma)<<<grid, ws2::kThreads, schur_ws2_smem_bytes(), st>>>(
+  ws2_kernel(tma, nparts > 1)<<<grid, ws2::kThreads, schur_ws2_smem_bytes(), st>>>(
       tma ? *ta : none, tma ? *tb : none, tma ? *ty : none, Lneg, Wg, tpad, Kl, A_in, A_out, phys, n, k, mp, d, ysk, bin,
-      bout, P, tstamp);
+      bout, P, tstamp, part, nparts, dyn);
   return cudaGetLastError();
 }
 
@@ -180,11 +184,12 @@ cudaError_t gemm_init_attributes() {
   e = cudaFuncSetAttribute(schur_ws_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)schur_ws_smem_bytes());
   if (e != cudaSuccess) return e;
-  for (Ws2Kernel f : {schur_ws2_kernel<0, false>, schur_ws2_kernel<1, false>, schur_ws2_kernel<2, false>,
-                      schur_ws2_kernel<0, true>, schur_ws2_kernel<1, true>, schur_ws2_kernel<2, true>}) {
-    e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)schur_ws2_smem_bytes());
-    if (e != cudaSuccess) return e;
-  }
+  for (int h = 0; h < 3; ++h)
+    for (Ws2Kernel f : {ws2_pick<false, false>(h), ws2_pick<true, false>(h), ws2_pick<false, true>(h),
+                        ws2_pick<true, true>(h)}) {
+      e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)schur_ws2_smem_bytes());
+      if (e != cudaSuccess) return e;
+    }
   e = cudaFuncSetAttribute(dmma_gemm_kernel<64, 128, kRectStages, 2, RectMap, SketchEpi>,
                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gemm_smem_bytes<64, 128, kRectStages>());
   if (e != cudaSuccess) return e;
@@ -219,12 +224,13 @@ cudaError_t launch_schur_update(int64_t n, int64_t k, int64_t mp, const double* 
       return e ? std::atoi(e) : 0;
     }();
     if (sms_env >= 1 && sms_env < sms) sms = sms_env;
+    if (schur_version() == 2)  // nparts > 1: rank 0's share, no fused sketch tiles
+      return launch_ws2((unsigned)sms, st, Lneg, Wg, tpad, 0, A_in, A_out, phys, n, 0, 0, d,
+                        nparts > 1 ? nullptr : ysk, bin, bout, P, tstamp, part, nparts, nullptr);
     if (nparts > 1)
       schur_ws_kernel<true><<<(unsigned)sms, ws::kThreads, schur_ws_smem_bytes(), st>>>(
           Lneg, Wg, tpad, 0, A_in, A_out, phys, n, 0, 0, 0, d, part, nparts, nullptr, nullptr, nullptr, nullptr, 0,
           tstamp);
-    else if (schur_version() == 2)
-      return launch_ws2((unsigned)sms, st, Lneg, Wg, tpad, 0, A_in, A_out, phys, n, 0, 0, d, ysk, bin, bout, P, tstamp);
     else
       schur_ws_kernel<false><<<(unsigned)sms, ws::kThreads, schur_ws_smem_bytes(), st>>>(
           Lneg, Wg, tpad, 0, A_in, A_out, phys, n, 0, 0, 0, d, part, nparts, nullptr, ysk, bin, bout, P, tstamp);
@@ -258,6 +264,9 @@ cudaError_t launch_schur_update_dyn(int64_t n, const double* Lneg, const double*
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (schur_version() == 2)
+    return launch_ws2((unsigned)sms, st, Lneg, Wg, tpad, 0, nullptr, nullptr, phys, n, 0, 0, nullptr, nullptr, nullptr,
+                      nullptr, 0, nullptr, part, nparts, dyn);
   schur_ws_kernel<true><<<(unsigned)sms, ws::kThreads, schur_ws_smem_bytes(), st>>>(
         Lneg, Wg, tpad, 0, nullptr, nullptr, phys, n, 0, 0, 0, nullptr, part, nparts, dyn);
   return cudaGetLastError();
@@ -340,17 +349,36 @@ extern "C" int64_t rcp_schur_tile_plan(int64_t mp, int32_t P, int32_t part, int3
   const int nbp = P > 0 ? (P + ws::BN - 1) / ws::BN : 0;
   const long long tiles = tiles_tri + nbi * nbp;
   int64_t cnt = 0;
+  auto emit = [&](int64_t a, int64_t b, bool sk) {
+    if (cnt < cap) {
+      if (m0) m0[cnt] = a;
+      if (n0) n0[cnt] = b;
+      if (sketch) sketch[cnt] = sk ? 1 : 0;
+    }
+    ++cnt;
+  };
+  if (schur_version() == 2) {  // schur_ws2_kernel: supertiles = two 128x64 tiles each
+    const int nbp2 = P > 0 ? (P + ws2::SN - 1) / ws2::SN : 0;
+    const long long s_tri = nbi * (nbi + 1) / 2, s_all = s_tri + nbi * nbp2;
+    for (int cta = 0; cta < grid; ++cta) {
+      long long x0, xs;
+      ws2::super_sequence(nparts > 1, part, nparts, cta, grid, x0, xs);
+      for (long long x = x0; x < s_all; x += xs) {
+        int64_t a, b;
+        const bool sk = ws2::super_at(x, s_tri, nbp2, a, b);
+        for (int h = 0; h < 2; ++h)  // halves beyond the last sketch row are loaded as zeros and never stored
+          if (!sk || b + h * ws::BN < P) emit(a, b + h * ws::BN, sk);
+      }
+    }
+    return cnt;
+  }
   for (int cta = 0; cta < grid; ++cta) {
     long long x0, xs;
     ws::tile_sequence(nparts > 1, part, nparts, cta, grid, x0, xs);
-    for (long long x = x0; x < tiles; x += xs, ++cnt) {
-      if (cnt < cap) {
-        int64_t a, b;
-        const bool sk = ws::tile_at(x, tiles_tri, nbp, a, b);
-        if (m0) m0[cnt] = a;
-        if (n0) n0[cnt] = b;
-        if (sketch) sketch[cnt] = sk ? 1 : 0;
-      }
+    for (long long x = x0; x < tiles; x += xs) {
+      int64_t a, b;
+      const bool sk = ws::tile_at(x, tiles_tri, nbp, a, b);
+      emit(a, b, sk);
     }
   }
   return cnt;

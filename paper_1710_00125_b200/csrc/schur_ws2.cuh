@@ -87,6 +87,13 @@ RCP_HD bool super_at(long long s, long long s_tri, int nbp2, int64_t& m0, int64_
 #ifndef RCP_WS2_SETMAXNREG
 #define RCP_WS2_SETMAXNREG 1
 #endif
+// The supertiles CTA `cta` of a `grid`-CTA launch takes on device `part` of `nparts` sharing the update:
+// s = first, first + step, ...  (supertiles dealt round robin to the devices, then to their CTAs).
+RCP_HD void super_sequence(bool multi, int part, int nparts, int cta, int grid, long long& first, long long& step) {
+  first = multi ? part + (long long)nparts * cta : (long long)cta;
+  step = multi ? (long long)nparts * grid : (long long)grid;
+}
+
 template <int N>
 RCP_D void setmaxnreg_inc() {
 #if RCP_WS2_SETMAXNREG
@@ -146,17 +153,25 @@ RCP_D u64a policy_evict_last() {
 }  // namespace ws2
 
 // kHints: 0 none, 1 operand panels evict_last, 2 also C-in / C-out evict_first
+// kMulti: the update is shared by `nparts` devices (dist.cuh): this launch takes every nparts-th
+// supertile; a worker resolves C-in / C-out / the descriptor from rank 0's signal (dyn)
 // kTma: operand stages filled by TMA (one elected thread, mbarrier transaction counts) instead of
 // 64 threads' cp.async.
-template <int kHints, bool kTma>
+template <int kHints, bool kTma, bool kMulti>
 __global__ void __launch_bounds__(ws2::kThreads, 1)
 schur_ws2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                  const __grid_constant__ CUtensorMap tmY, const double* __restrict__ Lneg, const double* __restrict__ Wg, int tpad, int Kl,
                  const double* __restrict__ ain, double* __restrict__ aout, const int* __restrict__ phys, int64_t n,
                  int64_t k, int64_t mp, const PanelDesc* __restrict__ d, const double* __restrict__ ysk,
                  const double* __restrict__ bin, double* __restrict__ bout, int P,
-                 unsigned long long* __restrict__ tstamp) {
+                 unsigned long long* __restrict__ tstamp, int part, int nparts, const SchurDyn* __restrict__ dyn) {
   using namespace ws2;
+  if (kMulti && dyn) {  // multi-GPU worker: buffers resolved on the device from rank 0's signal
+    if (!dyn->go) return;
+    ain = dyn->ain;
+    aout = dyn->aout;
+    d = dyn->d;
+  }
   if (d) {  // device-driven: the panel outcome comes from the committed descriptor
     if (!d->ok || d->t <= 0 || d->k_end >= n) return;
     k = d->k_end;
@@ -173,7 +188,8 @@ schur_ws2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
   Smem& sm = *reinterpret_cast<Smem*>(smem_ws2);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int KT = Kl / KS;
-  const long long x0 = blockIdx.x, xs = gridDim.x;
+  long long x0, xs;
+  super_sequence(kMulti, part, nparts, (int)blockIdx.x, (int)gridDim.x, x0, xs);
   if (tid == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&sm.full[s], kTma ? 1 : kProdThreads);
