@@ -474,8 +474,8 @@ def run_b200(args, rank: int, world: int, local_rank: int):
             cpu = {"value": None, "unit": "GFLOP/s", "cores": cores_used(), "kind": "port",
                    "sample": "host out of memory for the n=32768 oracle sample"}
     achieved = schur_flops / (schur_ms / 1e3) / 1e12 if schur_ms > 0 else None
-    # the single-GPU trailing update is schur_ws2_kernel (N > 1: the tile-dealing schur_ws_kernel)
-    schur_name = "schur_ws2_kernel" if world == 1 else "schur_ws_kernel"
+    # the trailing update is schur_ws2_kernel (N > 1: each rank's share of its supertiles)
+    schur_name = "schur_ws2_kernel"
     schur_key = schur_name if args.workload == "c3" else f"{schur_name}@{args.workload}"
     line = {
         "metric": metric_name(args), "value": value, "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
