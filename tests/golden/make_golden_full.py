@@ -50,6 +50,9 @@ CONFIGS = {
     "c2": (dict(gen="type6", n=8192, seed=0), dict(strategy="rcp", b=64, q=64, p=74, seed=0)),
     "c4": (dict(gen="kkt_c4", n1=16000, n2=4000, seed=0), dict(strategy="rcp", b=64, q=64, p=74, seed=0)),
     "c3": (dict(gen="type6", n=32768, seed=0), dict(strategy="rcp", b=128, q=128, p=144, seed=0)),
+    # the comparison strategies of the reference's benchmark grid at the C2 size
+    "c2_bkpp": (dict(gen="type6", n=8192, seed=0), dict(strategy="bkpp", b=64, q=1, p=5, seed=0)),
+    "c2_bbk": (dict(gen="type6", n=8192, seed=0), dict(strategy="bbk", b=64, q=1, p=5, seed=0)),
 }
 
 

@@ -49,7 +49,8 @@ def _divergence_report(g, perm, pattern):
         lines.append(f"  reference SBKP decision at k={int(ks[jj])}: lambda top-2 gap {g['sbkp_lam_gap'][jj]:.3e}, "
                      f"|a_kk| vs alpha*lambda {g['sbkp_akk_margin'][jj]:.3e}, "
                      f"|d_r| vs alpha*lambda {g['sbkp_dr_margin'][jj]:.3e}")
-    lines.append(f"  smallest QRCP residual-norm top-2 gap in the run: {np.nanmin(g['qrcp_gap']):.3e}")
+    if g["qrcp_gap"].size:
+        lines.append(f"  smallest QRCP residual-norm top-2 gap in the run: {np.nanmin(g['qrcp_gap']):.3e}")
     return "\n".join(lines)
 
 
@@ -153,3 +154,15 @@ def test_c3_full_size(cuda_ok):
     f = _check(a, api.FactorConfig(strategy="rcp", b=128, q=128, p=144, seed=0), 1e-10, 1e-13, min_2x2=8000)
     assert f.stats["n_panels"] >= 32768 // 128
     _compare_reference(f, g, a, "C3")
+
+
+@pytest.mark.parametrize("strategy", ["bkpp", "bbk"])
+def test_c2_size_comparison_strategies(cuda_ok, strategy):
+    """The reference grid's comparison strategies (bkpp, bbk) at the C2 size,
+    pinned to the reference's own run like the rcp configurations."""
+    import torch
+    from paper_1710_00125_b200 import api, gallery
+    g = _golden(f"c2_{strategy}")
+    a = torch.from_numpy(gallery.type6(8192, 0)).cuda()
+    f = _check(a, api.FactorConfig(strategy=strategy, b=64, q=1, p=5, seed=0), 1e-11, 1e-13, min_2x2=1000)
+    _compare_reference(f, g, a, f"C2/{strategy}")
