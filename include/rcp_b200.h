@@ -221,9 +221,10 @@ int rcp_schur_worker(const rcp_config* cfg, int64_t n, int rank, int world, void
  * column or, for a sketch tile, first sketch row; sketch = 1 for the fused sketch-correction tiles,
  * which exist only when P > 0 on a single device) that device `part` of `nparts` processes, in the
  * order its `grid` CTAs take them (CTA 0's tiles, then CTA 1's, ...).  Computed with the same
- * functions the kernel uses (schur_ws.cuh tile_sequence / tile_at); lets the distributed host
- * logic and its tests check the dealing without a GPU.  Returns the tile count (entries beyond
- * cap are not written), -1 on bad arguments. */
+ * functions the kernel uses (schur_ws2.cuh super_sequence / super_at: a CTA takes 128x128 supertiles,
+ * reported as their two 128x64 tiles; with RCP_SCHUR_V=1 schur_ws.cuh tile_sequence / tile_at); lets
+ * the distributed host logic and its tests check the dealing without a GPU.  Returns the tile count
+ * (entries beyond cap are not written), -1 on bad arguments. */
 int64_t rcp_schur_tile_plan(int64_t mp, int32_t P, int32_t part, int32_t nparts, int32_t grid,
                             int64_t* m0, int64_t* n0, int8_t* sketch, int64_t cap);
 /* Dense host copy of a device unit-lower L (row-major n x n): the lower trapezoid is copied,
